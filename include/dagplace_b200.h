@@ -30,6 +30,9 @@
 #ifdef __cplusplus
 extern "C" {
 #endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
 
 /* ---------------------------------------------------------------- status codes */
 enum {
@@ -348,6 +351,9 @@ int dp_gen_layered(int64_t n, int64_t width, int64_t fan_lo, int64_t fan_hi, uin
                    int64_t* node_id, int64_t* compute_us, int64_t* memory_bytes,
                    int64_t* edge_src, int64_t* edge_dst, int64_t* edge_bytes, int64_t* n_edges);
 
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,625 @@
+// graph.cu — graph core on the GPU: upload, id->index, CSR/CSC, validation flags,
+// comm costs, Kahn frontier levels with t/b-level max-plus relaxation.
+//
+// Reference behaviour followed (paths relative to /root/reference/proj):
+//   GraphIndex::GraphIndex        src/graph_index.cpp:8-42  (stable CSR/CSC of edge ids)
+//   validate / require_valid      src/graph.cpp:98-198      (detection order + messages)
+//   find_cycle_witness            src/graph.cpp:71-94
+//   comm_time                     src/graph.cpp:200-204     (no FMA; llround)
+//   compute_levels                src/graph.cpp:217-269     (int64 max-plus; any topo order)
+#include <algorithm>
+#include <cstring>
+#include <sstream>
+
+#include "graph.cuh"
+
+namespace dpb {
+
+std::string join_ids(const std::vector<int64_t>& ids) {
+  std::ostringstream out;
+  for (size_t i = 0; i < ids.size(); ++i) {
+    if (i) out << ",";
+    out << ids[i];
+  }
+  return out.str();
+}
+
+// ------------------------------------------------------------------ kernels
+namespace {
+
+__global__ void k_dense_check(const int64_t* id, int32_t n, int* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (id[i] != i) atomicExch(flag, 0);
+}
+
+__global__ void k_id_keys(const int64_t* id, int32_t n, uint64_t* keys, int32_t* vals) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = static_cast<uint64_t>(id[i]) ^ (1ull << 63);
+    vals[i] = static_cast<int32_t>(i);
+  }
+}
+
+__device__ __forceinline__ int32_t find_sorted(const uint64_t* keys, const int32_t* idx, int32_t n,
+                                               int64_t id) {
+  uint64_t k = static_cast<uint64_t>(id) ^ (1ull << 63);
+  int32_t lo = 0, hi = n;
+  while (lo < hi) {
+    int32_t mid = lo + ((hi - lo) >> 1);
+    if (keys[mid] < k) lo = mid + 1; else hi = mid;
+  }
+  return (lo < n && keys[lo] == k) ? idx[lo] : -1;
+}
+
+__global__ void k_resolve(const int64_t* src_id, const int64_t* dst_id, int32_t m, int32_t n, bool dense,
+                          const uint64_t* keys, const int32_t* idx, int32_t* esrc, int32_t* edst) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t s = src_id[e], d = dst_id[e];
+    if (dense) {
+      esrc[e] = (s >= 0 && s < n) ? static_cast<int32_t>(s) : -1;
+      edst[e] = (d >= 0 && d < n) ? static_cast<int32_t>(d) : -1;
+    } else {
+      esrc[e] = find_sorted(keys, idx, n, s);
+      edst[e] = find_sorted(keys, idx, n, d);
+    }
+  }
+}
+
+__global__ void k_ids_to_index(const int64_t* ids, int64_t k, int32_t n, bool dense, const uint64_t* keys,
+                               const int32_t* idx, int32_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t s = ids[i];
+    out[i] = dense ? ((s >= 0 && s < n) ? static_cast<int32_t>(s) : -1) : find_sorted(keys, idx, n, s);
+  }
+}
+
+// Row keys for the stable CSR/CSC sorts; edges with an unresolved endpoint go to row n.
+__global__ void k_row_keys(const int32_t* esrc, const int32_t* edst, int32_t m, int32_t n, bool by_src,
+                           uint32_t* keys, int32_t* vals, int32_t* counts) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+    int32_t s = esrc[e], d = edst[e];
+    bool ok = s >= 0 && d >= 0;
+    int32_t r = by_src ? s : d;
+    keys[e] = ok ? static_cast<uint32_t>(r) : static_cast<uint32_t>(n);
+    vals[e] = static_cast<int32_t>(e);
+    if (ok) atomicAdd(&counts[r], 1);
+  }
+}
+
+// 1 when every edge resolves and esrc is non-decreasing (generator output order), so the
+// CSR permutation is the identity and the sort can be skipped.
+__global__ void k_sorted_check(const int32_t* esrc, const int32_t* edst, int32_t m, int* flag) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+    bool ok = esrc[e] >= 0 && edst[e] >= 0 && (e == 0 || esrc[e - 1] <= esrc[e]);
+    if (!ok) atomicExch(flag, 0);
+  }
+}
+
+__global__ void k_iota(int32_t* a, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = static_cast<int32_t>(i);
+}
+
+__global__ void k_gather_i32(const int32_t* src, const int32_t* perm, int32_t* dst, int64_t k) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[perm[i]];
+}
+
+__global__ void k_gather_i64(const int64_t* src, const int32_t* perm, int64_t* dst, int64_t k) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[perm[i]];
+}
+
+__global__ void k_costs(const int64_t* bytes, int32_t m, double k, double b, int64_t* cost) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x)
+    cost[e] = comm_cost_dev(bytes[e], k, b);
+}
+
+// Duplicate ids: runs of equal keys in the sorted id table; the first index of a run
+// (smallest node index) carries the count (graph.cpp:105-113).
+__global__ void k_dup_runs(const uint64_t* keys, const int32_t* idx, int32_t n, int32_t* dupcount) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+    if (s > 0 && keys[s] == keys[s - 1]) continue;
+    int64_t t = s + 1;
+    while (t < n && keys[t] == keys[s]) ++t;
+    if (t - s > 1) dupcount[idx[s]] = static_cast<int32_t>(t - s);
+  }
+}
+
+// Node flags: bit0 duplicate id (first occurrence), bit1 negative compute, bit2 negative memory.
+__global__ void k_node_flags(const int64_t* w, const int64_t* mem, const int32_t* dupcount, int32_t n,
+                             uint8_t* flags, int* first) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint8_t f = (dupcount && dupcount[i] > 1 ? 1 : 0) | (w[i] < 0 ? 2 : 0) | (mem[i] < 0 ? 4 : 0);
+    flags[i] = f;
+    if (f) atomicMin(first, static_cast<int>(i));
+  }
+}
+
+// Duplicate edges among edges with ok endpoints (resolved, not a self-loop): an edge is
+// a duplicate when an earlier edge of the same row (stable CSR = earlier edge index) has
+// the same destination (graph.cpp:122,149-154).  Rows longer than 64 are left to the
+// sort-based pass.
+__global__ void k_dup_edges(const int32_t* out_off, const int32_t* out_eid, const int32_t* out_dst,
+                            int32_t n, uint8_t* dupflag, int* big) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+    int32_t b = out_off[u], e = out_off[u + 1];
+    if (e - b > 64) {
+      atomicExch(big, 1);
+      continue;
+    }
+    for (int32_t k = b + 1; k < e; ++k) {
+      int32_t x = out_dst[k];
+      if (x == u) continue;
+      for (int32_t q = b; q < k; ++q) {
+        if (out_dst[q] == x) {
+          dupflag[out_eid[k]] = 1;
+          break;
+        }
+      }
+    }
+  }
+}
+
+__global__ void k_pair_keys(const int32_t* esrc, const int32_t* edst, int32_t m, uint64_t* keys,
+                            int32_t* vals) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+    int32_t s = esrc[e], d = edst[e];
+    bool ok = s >= 0 && d >= 0 && s != d;
+    keys[e] = ok ? ((static_cast<uint64_t>(s) << 32) | static_cast<uint32_t>(d)) : ~0ull;
+    vals[e] = static_cast<int32_t>(e);
+  }
+}
+
+__global__ void k_pair_dups(const uint64_t* keys, const int32_t* vals, int32_t m, uint8_t* dupflag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    if (i > 0 && keys[i] != ~0ull && keys[i] == keys[i - 1]) dupflag[vals[i]] = 1;
+}
+
+// Edge flags: bit0 dangling src, bit1 dangling dst, bit2 self-loop, bit3 negative bytes,
+// bit4 duplicate (graph.cpp:124-156 order).
+__global__ void k_edge_flags(const int64_t* src_id, const int64_t* dst_id, const int64_t* bytes,
+                             const int32_t* esrc, const int32_t* edst, const uint8_t* dupflag, int32_t m,
+                             uint8_t* flags, int* first) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+    bool ds = esrc[e] < 0, dd = edst[e] < 0, sl = src_id[e] == dst_id[e];
+    bool ok = !ds && !dd && !sl;
+    uint8_t f = (ds ? 1 : 0) | (dd ? 2 : 0) | (sl ? 4 : 0) | (bytes[e] < 0 ? 8 : 0) |
+                (ok && dupflag[e] ? 16 : 0);
+    flags[e] = f;
+    if (f) atomicMin(first, static_cast<int>(e));
+  }
+}
+
+struct KahnArgs {
+  int32_t n;
+  const int32_t* out_off;
+  const int32_t* out_dst;
+  const int64_t* out_cost;
+  const int64_t* w;
+  int32_t* indeg;
+  int32_t* order;
+  int32_t* level_off;
+  int64_t* tlevel;
+  int64_t* blevel;
+  int32_t* level_of;
+  int* counters;  // [0] tail, [1] levels
+  unsigned* bar;
+};
+
+// Persistent level-synchronous Kahn frontier.  Forward: each frontier node relaxes
+// tlevel of its children with atomicMax (max-plus, order-insensitive) and releases them
+// when their remaining in-degree hits zero; released nodes form the next frontier,
+// appended to `order` (so order is a topological order grouped by level).  Backward:
+// frontiers in reverse, blevel pulled over CSR (graph.cpp:253-261).
+__global__ void __launch_bounds__(512) k_kahn(KahnArgs a) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = tid; v < a.n; v += nth) {
+    bool src = a.indeg[v] == 0;
+    if (a.tlevel) a.tlevel[v] = 0;
+    int slot = warp_append(&a.counters[0], src);
+    if (src) a.order[slot] = static_cast<int32_t>(v);
+  }
+  grid_barrier(a.bar, gridDim.x);
+  int32_t lb = 0, level = 0;
+  for (;;) {
+    int32_t le = *((volatile int*)&a.counters[0]);
+    if (le == lb) break;
+    if (tid == 0) a.level_off[level] = lb;
+    for (int64_t i = lb + tid; i < le; i += nth) {
+      int32_t u = a.order[i];
+      if (a.level_of) a.level_of[u] = level;
+      int64_t t = a.tlevel ? a.tlevel[u] + a.w[u] : 0;
+      int32_t kb = a.out_off[u], ke = a.out_off[u + 1];
+      for (int32_t k = kb; k < ke; ++k) {
+        int32_t v = a.out_dst[k];
+        if (a.tlevel) atomic_max_i64(&a.tlevel[v], t + a.out_cost[k]);
+        bool freed = atomicSub(&a.indeg[v], 1) == 1;
+        int slot = warp_append(&a.counters[0], freed);
+        if (freed) a.order[slot] = v;
+      }
+    }
+    grid_barrier(a.bar, gridDim.x);
+    lb = le;
+    ++level;
+  }
+  if (tid == 0) {
+    a.level_off[level] = lb;
+    a.counters[1] = level;
+  }
+  if (!a.blevel) return;
+  grid_barrier(a.bar, gridDim.x);
+  for (int32_t L = level - 1; L >= 0; --L) {
+    int32_t b = a.level_off[L], e = a.level_off[L + 1];
+    for (int64_t i = b + tid; i < e; i += nth) {
+      int32_t v = a.order[i];
+      int64_t best = 0;
+      for (int32_t k = a.out_off[v]; k < a.out_off[v + 1]; ++k) {
+        int64_t c = a.blevel[a.out_dst[k]] + a.out_cost[k];
+        best = c > best ? c : best;
+      }
+      a.blevel[v] = best + a.w[v];
+    }
+    grid_barrier(a.bar, gridDim.x);
+  }
+}
+
+__global__ void k_indeg(const int32_t* in_off, int32_t n, int32_t* indeg) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+    indeg[v] = in_off[v + 1] - in_off[v];
+}
+
+__global__ void k_min_remaining_id(const int32_t* indeg, const int64_t* id, int32_t n,
+                                   unsigned long long* best) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+    if (indeg[v] > 0) atomicMin(best, static_cast<unsigned long long>(id[v]) ^ (1ull << 63));
+}
+
+// find_cycle_witness (graph.cpp:71-94), single thread: from the smallest remaining id,
+// follow the smallest-id successor inside the remaining set until an id repeats.
+__global__ void k_witness(const int32_t* indeg, const int64_t* id, const int32_t* out_off,
+                          const int32_t* out_dst, int32_t n, int32_t start, int32_t* pos_in_path,
+                          int32_t* path, int32_t* result) {
+  if (threadIdx.x || blockIdx.x) return;
+  int32_t len = 0, cur = start;
+  for (;;) {
+    if (pos_in_path[cur] >= 0) {
+      result[0] = pos_in_path[cur];
+      result[1] = len;
+      return;
+    }
+    pos_in_path[cur] = len;
+    path[len++] = cur;
+    int32_t best = -1;
+    for (int32_t k = out_off[cur]; k < out_off[cur + 1]; ++k) {
+      int32_t x = out_dst[k];
+      if (indeg[x] > 0 && (best < 0 || id[x] < id[best])) best = x;
+    }
+    if (best < 0) {
+      result[0] = 0;
+      result[1] = len;
+      return;
+    }
+    cur = best;
+  }
+}
+
+int coop_grid(const void* kernel, int block, int64_t work, int num_sms) {
+  int per_sm = 0;
+  DP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0));
+  if (per_sm < 1) per_sm = 1;
+  int64_t want = (work + block - 1) / block;
+  int64_t cap = static_cast<int64_t>(per_sm) * num_sms;
+  if (cap > 2 * num_sms) cap = 2 * num_sms;  // barrier cost grows with CTA count
+  if (want < 1) want = 1;
+  return static_cast<int>(want < cap ? want : cap);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ host orchestration
+void graph_upload(DevGraph& g, dp_ctx* ctx, const dp_graph_t* h) {
+  if (h->n_nodes < 0 || h->n_edges < 0 || h->n_nodes > INT32_MAX - 2 || h->n_edges > INT32_MAX - 2)
+    fail(DP_E_ARGUMENT, "graph sizes out of range (n=%lld, m=%lld)", (long long)h->n_nodes,
+         (long long)h->n_edges);
+  g.ctx = ctx;
+  g.n = static_cast<int32_t>(h->n_nodes);
+  g.m = static_cast<int32_t>(h->n_edges);
+  g.id.alloc(ctx, g.n);
+  g.w.alloc(ctx, g.n);
+  g.mem.alloc(ctx, g.n);
+  g.id.upload(h->node_id, g.n);
+  g.w.upload(h->compute_us, g.n);
+  g.mem.upload(h->memory_bytes, g.n);
+  g.has_group = false;
+  if (h->group) {
+    for (int64_t i = 0; i < h->n_nodes; ++i) {
+      if (h->group[i] >= 0) { g.has_group = true; break; }
+    }
+  }
+  if (g.has_group) {
+    g.group.alloc(ctx, g.n);
+    g.group.upload(h->group, g.n);
+  }
+  g.src_id.alloc(ctx, g.m);
+  g.dst_id.alloc(ctx, g.m);
+  g.bytes.alloc(ctx, g.m);
+  g.src_id.upload(h->edge_src, g.m);
+  g.dst_id.upload(h->edge_dst, g.m);
+  g.bytes.upload(h->edge_bytes, g.m);
+}
+
+void graph_adopt_dense(DevGraph& g, dp_ctx* ctx, int32_t n, int32_t m, DevBuf<int64_t>&& w,
+                       DevBuf<int64_t>&& mem, DevBuf<int32_t>&& esrc, DevBuf<int32_t>&& edst,
+                       DevBuf<int64_t>&& bytes) {
+  g.ctx = ctx;
+  g.n = n;
+  g.m = m;
+  g.w = std::move(w);
+  g.mem = std::move(mem);
+  g.esrc = std::move(esrc);
+  g.edst = std::move(edst);
+  g.bytes = std::move(bytes);
+  g.dense_ids = true;
+  g.has_group = false;
+}
+
+void graph_resolve(DevGraph& g) {
+  dp_ctx* ctx = g.ctx;
+  const int B = 256;
+  DevBuf<int> flag(ctx, 1);
+  int one = 1;
+  flag.upload(&one, 1);
+  DP_LAUNCH(ctx, k_dense_check, grid_for(g.n, B), B, 0, g.id.p, g.n, flag.p);
+  g.dense_ids = scalar_to_host(ctx, flag.p) == 1;
+  if (!g.dense_ids) {
+    DevBuf<uint64_t> keys(ctx, g.n);
+    DevBuf<int32_t> vals(ctx, g.n);
+    g.sorted_key.alloc(ctx, g.n);
+    g.sorted_idx.alloc(ctx, g.n);
+    DP_LAUNCH(ctx, k_id_keys, grid_for(g.n, B), B, 0, g.id.p, g.n, keys.p, vals.p);
+    sort_pairs_u64(ctx, keys.p, g.sorted_key.p, vals.p, g.sorted_idx.p, g.n, 0, 64);
+  }
+  g.esrc.alloc(ctx, g.m);
+  g.edst.alloc(ctx, g.m);
+  DP_LAUNCH(ctx, k_resolve, grid_for(g.m, B), B, 0, g.src_id.p, g.dst_id.p, g.m, g.n, g.dense_ids,
+            g.sorted_key.p, g.sorted_idx.p, g.esrc.p, g.edst.p);
+}
+
+void graph_ids_to_index(DevGraph& g, const int64_t* ids, int32_t* out, int64_t k) {
+  DP_LAUNCH(g.ctx, k_ids_to_index, grid_for(k, 256), 256, 0, ids, k, g.n, g.dense_ids, g.sorted_key.p,
+            g.sorted_idx.p, out);
+}
+
+int32_t graph_index_of(DevGraph& g, int64_t id) {
+  DevBuf<int64_t> d(g.ctx, 1);
+  DevBuf<int32_t> o(g.ctx, 1);
+  d.upload(&id, 1);
+  graph_ids_to_index(g, d.p, o.p, 1);
+  return scalar_to_host(g.ctx, o.p);
+}
+
+void graph_adjacency(DevGraph& g) {
+  dp_ctx* ctx = g.ctx;
+  const int B = 256;
+  int32_t n = g.n, m = g.m;
+  g.out_off.alloc(ctx, (size_t)n + 1);
+  g.in_off.alloc(ctx, (size_t)n + 1);
+  g.out_eid.alloc(ctx, m);
+  g.in_eid.alloc(ctx, m);
+  DevBuf<int32_t> cnt(ctx, (size_t)n + 1);
+  DevBuf<uint32_t> keys(ctx, m), keys_out(ctx, m);
+  DevBuf<int32_t> vals(ctx, m);
+  int endbit = bits_for(static_cast<uint64_t>(n));
+  // CSR by source
+  DevBuf<int> sorted(ctx, 1);
+  int one = 1;
+  sorted.upload(&one, 1);
+  DP_LAUNCH(ctx, k_sorted_check, grid_for(m, B), B, 0, g.esrc.p, g.edst.p, m, sorted.p);
+  cnt.zero();
+  DP_LAUNCH(ctx, k_row_keys, grid_for(m, B), B, 0, g.esrc.p, g.edst.p, m, n, true, keys.p, vals.p, cnt.p);
+  exclusive_scan_i32(ctx, cnt.p, g.out_off.p, (int64_t)n + 1);
+  if (scalar_to_host(ctx, sorted.p) == 1) {
+    DP_LAUNCH(ctx, k_iota, grid_for(m, B), B, 0, g.out_eid.p, (int64_t)m);
+  } else {
+    sort_pairs_u32(ctx, keys.p, keys_out.p, vals.p, g.out_eid.p, m, endbit);
+  }
+  // CSC by destination
+  cnt.zero();
+  DP_LAUNCH(ctx, k_row_keys, grid_for(m, B), B, 0, g.esrc.p, g.edst.p, m, n, false, keys.p, vals.p, cnt.p);
+  exclusive_scan_i32(ctx, cnt.p, g.in_off.p, (int64_t)n + 1);
+  sort_pairs_u32(ctx, keys.p, keys_out.p, vals.p, g.in_eid.p, m, endbit);
+  g.m_ok = scalar_to_host(ctx, g.out_off.p + n);
+  g.out_dst.alloc(ctx, g.m_ok);
+  g.in_src.alloc(ctx, g.m_ok);
+  DP_LAUNCH(ctx, k_gather_i32, grid_for(g.m_ok, B), B, 0, g.edst.p, g.out_eid.p, g.out_dst.p, (int64_t)g.m_ok);
+  DP_LAUNCH(ctx, k_gather_i32, grid_for(g.m_ok, B), B, 0, g.esrc.p, g.in_eid.p, g.in_src.p, (int64_t)g.m_ok);
+  g.has_adj = true;
+}
+
+void graph_costs(DevGraph& g, dp_comm_t comm) {
+  dp_ctx* ctx = g.ctx;
+  if (g.has_cost && g.ck == comm.k_us_per_byte && g.cb == comm.b_us) return;
+  const int B = 256;
+  g.cost.alloc(ctx, g.m);
+  DP_LAUNCH(ctx, k_costs, grid_for(g.m, B), B, 0, g.bytes.p, g.m, comm.k_us_per_byte, comm.b_us, g.cost.p);
+  if (g.has_adj) {
+    g.out_cost.alloc(ctx, g.m_ok);
+    g.in_cost.alloc(ctx, g.m_ok);
+    DP_LAUNCH(ctx, k_gather_i64, grid_for(g.m_ok, B), B, 0, g.cost.p, g.out_eid.p, g.out_cost.p, (int64_t)g.m_ok);
+    DP_LAUNCH(ctx, k_gather_i64, grid_for(g.m_ok, B), B, 0, g.cost.p, g.in_eid.p, g.in_cost.p, (int64_t)g.m_ok);
+  }
+  g.has_cost = true;
+  g.ck = comm.k_us_per_byte;
+  g.cb = comm.b_us;
+}
+
+void graph_kahn(DevGraph& g, int64_t* tlevel, int64_t* blevel, int32_t* level_of) {
+  dp_ctx* ctx = g.ctx;
+  int32_t n = g.n;
+  g.order.alloc(ctx, n > 0 ? n : 1);
+  g.level_off.alloc(ctx, (size_t)n + 2);
+  if (n == 0) {
+    g.processed = 0;
+    g.num_levels = 0;
+    return;
+  }
+  DevBuf<int32_t> indeg(ctx, n);
+  DP_LAUNCH(ctx, k_indeg, grid_for(n, 256), 256, 0, g.in_off.p, n, indeg.p);
+  DevBuf<int> counters(ctx, 2);
+  DevBuf<unsigned> bar(ctx, 2);
+  counters.zero();
+  bar.zero();
+  KahnArgs a;
+  a.n = n;
+  a.out_off = g.out_off.p;
+  a.out_dst = g.out_dst.p;
+  a.out_cost = (tlevel || blevel) ? g.out_cost.p : nullptr;
+  a.w = g.w.p;
+  a.indeg = indeg.p;
+  a.order = g.order.p;
+  a.level_off = g.level_off.p;
+  a.tlevel = tlevel;
+  a.blevel = blevel;
+  a.level_of = level_of;
+  a.counters = counters.p;
+  a.bar = bar.p;
+  const int B = 512;
+  int grid = coop_grid(reinterpret_cast<const void*>(k_kahn), B, n, ctx->num_sms);
+  void* args[] = {&a};
+  DP_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_kahn), grid, B, args, 0, ctx->stream));
+  ++ctx->launches;
+  int host[2];
+  counters.download(host, 2);
+  sync(ctx);
+  g.processed = host[0];
+  g.num_levels = host[1];
+  if (g.processed != n) {
+    // keep the residual in-degrees for the witness
+    g.level_off.release();
+    g.level_off.alloc(ctx, n);
+    DP_CUDA(cudaMemcpyAsync(g.level_off.p, indeg.p, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+}
+
+std::vector<int64_t> graph_cycle_witness(DevGraph& g) {
+  dp_ctx* ctx = g.ctx;
+  int32_t n = g.n;
+  const int32_t* indeg = g.level_off.p;  // residual in-degrees (graph_kahn)
+  DevBuf<unsigned long long> best(ctx, 1);
+  best.fill_bytes(0xff);
+  DP_LAUNCH(ctx, k_min_remaining_id, grid_for(n, 256), 256, 0, indeg, g.id.p, n, best.p);
+  unsigned long long key = scalar_to_host(ctx, best.p);
+  int64_t start_id = static_cast<int64_t>(key ^ (1ull << 63));
+  int32_t start = graph_index_of(g, start_id);
+  DevBuf<int32_t> pos(ctx, n), path(ctx, (size_t)n + 1), res(ctx, 2);
+  pos.fill_bytes(0xff);
+  DP_LAUNCH(ctx, k_witness, 1, 1, 0, indeg, g.id.p, g.out_off.p, g.out_dst.p, n, start, pos.p, path.p, res.p);
+  int32_t r[2];
+  res.download(r, 2);
+  sync(ctx);
+  std::vector<int32_t> idx = to_host(ctx, path.p + r[0], static_cast<size_t>(r[1] - r[0]));
+  std::vector<int64_t> ids = to_host(ctx, g.id.p, n);
+  std::vector<int64_t> out;
+  for (int32_t v : idx) out.push_back(ids[v]);
+  return out;
+}
+
+Validation graph_validate(DevGraph& g, const dp_graph_t* h, bool all, bool cycle_check) {
+  dp_ctx* ctx = g.ctx;
+  const int B = 256;
+  int32_t n = g.n, m = g.m;
+  Validation out;
+  DevBuf<int32_t> dupcount;
+  if (!g.dense_ids && n > 0) {
+    dupcount.alloc(ctx, n);
+    dupcount.zero();
+    DP_LAUNCH(ctx, k_dup_runs, grid_for(n, B), B, 0, g.sorted_key.p, g.sorted_idx.p, n, dupcount.p);
+  }
+  if (!g.has_adj) graph_adjacency(g);
+  DevBuf<uint8_t> nflags(ctx, n > 0 ? n : 1), eflags(ctx, m > 0 ? m : 1), dupflag(ctx, m > 0 ? m : 1);
+  dupflag.zero();
+  DevBuf<int> first(ctx, 3);
+  int init[3] = {INT32_MAX, INT32_MAX, 0};
+  first.upload(init, 3);
+  DP_LAUNCH(ctx, k_dup_edges, grid_for(n, B), B, 0, g.out_off.p, g.out_eid.p, g.out_dst.p, n, dupflag.p,
+            first.p + 2);
+  int big = 0;
+  DP_CUDA(cudaMemcpyAsync(&big, first.p + 2, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  if (big) {
+    DevBuf<uint64_t> k(ctx, m), ko(ctx, m);
+    DevBuf<int32_t> v(ctx, m), vo(ctx, m);
+    DP_LAUNCH(ctx, k_pair_keys, grid_for(m, B), B, 0, g.esrc.p, g.edst.p, m, k.p, v.p);
+    sort_pairs_u64(ctx, k.p, ko.p, v.p, vo.p, m, 0, 64);
+    DP_LAUNCH(ctx, k_pair_dups, grid_for(m, B), B, 0, ko.p, vo.p, m, dupflag.p);
+  }
+  DP_LAUNCH(ctx, k_node_flags, grid_for(n, B), B, 0, g.w.p, g.mem.p, dupcount.p, n, nflags.p, first.p);
+  DP_LAUNCH(ctx, k_edge_flags, grid_for(m, B), B, 0, g.src_id.p, g.dst_id.p, g.bytes.p, g.esrc.p, g.edst.p,
+            dupflag.p, m, eflags.p, first.p + 1);
+  int fh[2];
+  first.download(fh, 2);
+  sync(ctx);
+
+  auto add = [&](int code, std::string msg, std::vector<int64_t> nodes) {
+    if (!out.code) {
+      out.code = code;
+      out.message = msg;
+      out.nodes = nodes;
+    }
+    if (all) {
+      out.kinds.push_back(code);
+      out.messages.push_back(std::move(msg));
+      out.witnesses.push_back(std::move(nodes));
+    }
+  };
+  auto S = [](int64_t v) { return std::to_string(v); };
+  std::vector<uint8_t> nf, ef;
+  std::vector<int32_t> dc;
+  bool any_dup = false, edges_resolvable = true;
+  if (all || fh[0] != INT32_MAX || fh[1] != INT32_MAX) {
+    nf = to_host(ctx, nflags.p, n);
+    ef = to_host(ctx, eflags.p, m);
+    if (dupcount.p) dc = to_host(ctx, dupcount.p, n);
+  }
+  int32_t nb = all ? 0 : (fh[0] == INT32_MAX ? n : fh[0]);
+  for (int32_t i = nb; i < n; ++i) {
+    uint8_t f = nf[i];
+    if (!f) continue;
+    int64_t id = h->node_id[i];
+    if (f & 1) {
+      any_dup = true;
+      add(DP_E_DUPLICATE_ID, "node id " + S(id) + " appears " + S(dc[i]) + " times", {id});
+    }
+    if (f & 2) add(DP_E_INVALID_VALUE, "node " + S(id) + " has negative compute_us", {id});
+    if (f & 4) add(DP_E_INVALID_VALUE, "node " + S(id) + " has negative memory_bytes", {id});
+    if (!all) break;
+  }
+  if (!all && out.code) return out;
+  int32_t eb = all ? 0 : (fh[1] == INT32_MAX ? m : fh[1]);
+  for (int32_t e = eb; e < m; ++e) {
+    uint8_t f = ef[e];
+    if (!f) continue;
+    int64_t s = h->edge_src[e], d = h->edge_dst[e];
+    std::string pair = "(" + S(s) + "," + S(d) + ")";
+    if (f & 1) add(DP_E_DANGLING_EDGE, "edge " + pair + " references missing node " + S(s), {s, d});
+    if (f & 2) add(DP_E_DANGLING_EDGE, "edge " + pair + " references missing node " + S(d), {s, d});
+    if (f & 4) add(DP_E_CYCLE_DETECTED, "self-loop on node " + S(s), {s});
+    if (f & 8) add(DP_E_INVALID_VALUE, "edge " + pair + " has negative tensor_bytes", {s, d});
+    if (f & 16)
+      add(DP_E_DUPLICATE_EDGE, "parallel edge " + pair + "; aggregate tensor bytes upstream", {s, d});
+    if (f & 7) edges_resolvable = false;
+    if (!all) break;
+  }
+  if (!all && out.code) return out;
+  if (cycle_check && edges_resolvable && !any_dup && n > 0) {
+    graph_kahn(g, nullptr, nullptr, nullptr);
+    if (g.processed != n) {
+      std::vector<int64_t> wit = graph_cycle_witness(g);
+      add(DP_E_CYCLE_DETECTED, "cycle: [" + join_ids(wit) + "]", wit);
+    }
+  }
+  return out;
+}
+
+}  // namespace dpb

@@ -1,0 +1,76 @@
+// graph.cuh — device-resident ComputationGraph (SoA in HBM) and the graph-core stages.
+#pragma once
+
+#include "common.cuh"
+
+namespace dpb {
+
+// Layout in HBM (n nodes, m edges; indices are int32, ids/costs int64):
+//   nodes:  id[n] w[n] mem[n] (+ group[n])                 24-28 B/node
+//   edges:  src_id[m] dst_id[m] bytes[m] -> esrc[m] edst[m] cost[m]
+//   CSR:    out_off[n+1] out_eid[m] out_dst[m] out_cost[m]  (stable in edge order)
+//   CSC:    in_off[n+1]  in_eid[m]  in_src[m]  in_cost[m]
+struct DevGraph {
+  dp_ctx* ctx = nullptr;
+  int32_t n = 0, m = 0;
+  DevBuf<int64_t> id, w, mem;
+  DevBuf<int32_t> group;
+  bool has_group = false;
+  DevBuf<int64_t> src_id, dst_id, bytes;
+  DevBuf<int32_t> esrc, edst;         // -1 when the endpoint id is not a node
+  bool dense_ids = false;             // id[i] == i for all i
+  DevBuf<uint64_t> sorted_key;        // sign-flipped ids, ascending (when !dense_ids)
+  DevBuf<int32_t> sorted_idx;         // node index per sorted key (ascending idx on ties)
+  // adjacency over edges whose endpoints both resolve
+  bool has_adj = false;
+  int32_t m_ok = 0;
+  DevBuf<int32_t> out_off, out_eid, in_off, in_eid, out_dst, in_src;
+  // costs
+  bool has_cost = false;
+  double ck = 0, cb = 0;
+  DevBuf<int64_t> cost, out_cost, in_cost;
+  // Kahn levels (filled by kahn())
+  int32_t processed = 0, num_levels = 0;
+  DevBuf<int32_t> order, level_off;
+};
+
+struct Validation {
+  // first violation, detection order of graph.cpp:98-191
+  int code = 0;                       // 0 = valid
+  std::string message;
+  std::vector<int64_t> nodes;
+  // full list (when requested)
+  std::vector<int32_t> kinds;
+  std::vector<std::string> messages;
+  std::vector<std::vector<int64_t>> witnesses;
+};
+
+// Host SoA -> HBM (async on ctx->stream).
+void graph_upload(DevGraph& g, dp_ctx* ctx, const dp_graph_t* h);
+// Adopt device arrays of a graph with dense ids 0..n-1 (coarse graph).
+void graph_adopt_dense(DevGraph& g, dp_ctx* ctx, int32_t n, int32_t m, DevBuf<int64_t>&& w,
+                       DevBuf<int64_t>&& mem, DevBuf<int32_t>&& esrc, DevBuf<int32_t>&& edst,
+                       DevBuf<int64_t>&& bytes);
+// id -> index map and edge endpoint resolution.
+void graph_resolve(DevGraph& g);
+// CSR/CSC over resolvable edges (stable in edge order).
+void graph_adjacency(DevGraph& g);
+// Per-edge comm_time and the CSR/CSC-ordered copies.
+void graph_costs(DevGraph& g, dp_comm_t comm);
+// validate(): needs host arrays for message text.  all=false stops at the first.
+// cycle_check=false skips the Kahn pass (callers that run graph_kahn with levels right
+// after check g.processed themselves and call graph_cycle_witness).
+Validation graph_validate(DevGraph& g, const dp_graph_t* h, bool all, bool cycle_check = true);
+// Kahn frontier (level-synchronous, persistent cooperative kernel): fills order /
+// level_off / processed, and when requested tlevel / blevel (graph.cpp:228-261).
+void graph_kahn(DevGraph& g, int64_t* tlevel, int64_t* blevel, int32_t* level_of);
+// CycleDetected witness after an incomplete Kahn pass (graph.cpp:71-94).
+std::vector<int64_t> graph_cycle_witness(DevGraph& g);
+// Node index of an id (UnknownNode when absent); host lookup helper via device search.
+int32_t graph_index_of(DevGraph& g, int64_t id);
+// Translate node ids (device array, count k) into indices (-1 when absent).
+void graph_ids_to_index(DevGraph& g, const int64_t* ids, int32_t* out, int64_t k);
+
+std::string join_ids(const std::vector<int64_t>& ids);
+
+}  // namespace dpb
