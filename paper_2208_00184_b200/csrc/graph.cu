@@ -352,6 +352,7 @@ void graph_upload(DevGraph& g, dp_ctx* ctx, const dp_graph_t* h) {
 void graph_adopt_dense(DevGraph& g, dp_ctx* ctx, int32_t n, int32_t m, DevBuf<int64_t>&& w,
                        DevBuf<int64_t>&& mem, DevBuf<int32_t>&& esrc, DevBuf<int32_t>&& edst,
                        DevBuf<int64_t>&& bytes) {
+  g = DevGraph();
   g.ctx = ctx;
   g.n = n;
   g.m = m;
@@ -435,6 +436,7 @@ void graph_adjacency(DevGraph& g) {
   DP_LAUNCH(ctx, k_gather_i32, grid_for(g.m_ok, B), B, 0, g.edst.p, g.out_eid.p, g.out_dst.p, (int64_t)g.m_ok);
   DP_LAUNCH(ctx, k_gather_i32, grid_for(g.m_ok, B), B, 0, g.esrc.p, g.in_eid.p, g.in_src.p, (int64_t)g.m_ok);
   g.has_adj = true;
+  g.has_cost = false;  // CSR/CSC-ordered cost copies must follow the new permutation
 }
 
 void graph_costs(DevGraph& g, dp_comm_t comm) {

@@ -1,0 +1,277 @@
+// pipeline.cu — evaluate_pipeline (pipeline.cpp:27-111, /root/reference/proj/src) with
+// every intermediate resident in HBM.  The generation window of pipeline.cpp:67-79
+// (fuse -> coarse levels + cpd_topo -> order_place + adjusting_placement -> 2x expand)
+// runs as one stream of kernels; only the results cross PCIe.
+#include <algorithm>
+
+#include "abi_util.cuh"
+#include "fusion.cuh"
+#include "peel.cuh"
+#include "placement.cuh"
+#include "results.h"
+#include "simulate.cuh"
+
+namespace dpb {
+
+dp_graph_out_t* graph_to_host(DevGraph& g, bool dense_ids_out);
+dp_placement_result_t* placement_to_host(dp_ctx* ctx, const Devices& devs, PlaceOut& p, int32_t n,
+                                         const std::vector<int64_t>* seq_ids, bool decisions);
+dp_sim_report_t* sim_report(DevGraph& g, const Devices& devs, const int32_t* dev_pos_dev, bool trace);
+
+namespace {
+
+__global__ void k_ccr(const int64_t* w, int32_t n, const int64_t* cost, int32_t m, unsigned long long* out) {
+  unsigned long long sc = 0, sm = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    sc += static_cast<unsigned long long>(w[i]);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x)
+    sm += static_cast<unsigned long long>(cost[e]);
+  for (int o = 16; o; o >>= 1) {
+    sc += __shfl_down_sync(0xffffffffu, sc, o);
+    sm += __shfl_down_sync(0xffffffffu, sm, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&out[0], sc);
+    atomicAdd(&out[1], sm);
+  }
+}
+
+}  // namespace
+
+struct Resident {
+  dp_ctx* ctx = nullptr;
+  const dp_graph_t* host = nullptr;  // only for error messages during generate
+  dp_graph_t host_copy{};
+  DevGraph g;
+  Devices devs;
+  dp_comm_t comm{};
+  dp_pipeline_config_t cfg{};
+  int64_t limit = 1;
+  bool decisions = true;
+  // window outputs
+  FuseOut f;
+  DevBuf<int64_t> ct, cb, cc;
+  DevBuf<int32_t> cseq, cpos;
+  PlaceOut po, pa;
+  DevBuf<int32_t> dev_order, dev_adjust;
+  DevBuf<int64_t> pdm_order, pdm_adjust;
+  double original_ccr = 0.0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
+
+double ccr_dev(DevGraph& g) {
+  dp_ctx* ctx = g.ctx;
+  DevBuf<unsigned long long> s(ctx, 2);
+  s.zero();
+  DP_LAUNCH(ctx, k_ccr, grid_for(std::max(g.n, g.m), 256, 4 * ctx->num_sms), 256, 0, g.w.p, g.n, g.cost.p, g.m, s.p);
+  unsigned long long h[2];
+  s.download(h, 2);
+  sync(ctx);
+  const int64_t tc = static_cast<int64_t>(h[0]);
+  if (tc <= 0) fail(DP_E_ZERO_COMPUTE_TIME, "total compute time is zero");
+  return static_cast<double>(static_cast<int64_t>(h[1])) / static_cast<double>(tc);
+}
+
+// Everything after the H2D upload: index, validation (pipeline.cpp:33), ccr (:58),
+// cluster limit (:60-65) and the generation window (:67-79).
+void resident_generate(Resident& r, bool with_ccr) {
+  dp_ctx* ctx = r.ctx;
+  DevGraph& g = r.g;
+  StageScope whole(ctx, "generate", 0.0);
+  {
+    StageScope st(ctx, "index+validate", 16.0 * g.m + 8.0 * g.n);
+    graph_resolve(g);
+    graph_adjacency(g);
+    Validation v = graph_validate(g, r.host, false, false);
+    if (v.code) fail(v.code, "%s", v.message.c_str());
+  }
+  graph_costs(g, r.comm);
+  if (with_ccr) r.original_ccr = ccr_dev(g);
+  fuse_dev(g, r.comm, r.cfg.fusion_range, r.limit, r.f);
+  DevGraph& coarse = r.f.coarse;
+  levels_dev(coarse, r.comm, r.ct, r.cb, r.cc);
+  const int32_t k = coarse.n;
+  r.cseq.alloc(ctx, k > 0 ? k : 1);
+  r.cpos.alloc(ctx, k > 0 ? k : 1);
+  topo_order(coarse, DP_TOPO_CPD, r.cc.p, r.cseq.p, r.cpos.p);
+  place_dev(coarse, r.cseq.p, r.devs, &r.po, &r.pa, r.decisions);
+  const int32_t D = r.devs.D;
+  r.dev_order.alloc(ctx, g.n > 0 ? g.n : 1);
+  r.dev_adjust.alloc(ctx, g.n > 0 ? g.n : 1);
+  r.pdm_order.alloc(ctx, D);
+  r.pdm_adjust.alloc(ctx, D);
+  {
+    StageScope st(ctx, "expand", 2.0 * (12.0 * g.n));
+    expand_dev(g, r.f.node_cluster.p, r.po.dev.p, D, r.dev_order.p, r.pdm_order.p);
+    expand_dev(g, r.f.node_cluster.p, r.pa.dev.p, D, r.dev_adjust.p, r.pdm_adjust.p);
+  }
+}
+
+void resident_init(Resident& r, dp_ctx* ctx, const dp_graph_t* h, const dp_devices_t* devices, dp_comm_t comm,
+                   const dp_pipeline_config_t* cfg) {
+  if (devices->count <= 0) fail(DP_E_INVALID_VALUE, "device list is empty");
+  r.ctx = ctx;
+  r.host = h;
+  r.comm = comm;
+  r.cfg = *cfg;
+  if (r.cfg.fusion_range == 0) r.cfg.fusion_range = 200;
+  r.devs = devices_sorted(devices);
+  int64_t min_cap = devices->memory_bytes[0];
+  for (int32_t i = 0; i < devices->count; ++i) min_cap = std::min(min_cap, devices->memory_bytes[i]);
+  r.limit = std::max<int64_t>(1, static_cast<int64_t>(static_cast<double>(min_cap) * r.cfg.cluster_mem_fraction));
+  graph_upload(r.g, ctx, h);
+}
+
+// Expanded placement with every device listed (present where it received nodes).
+dp_placement_result_t* expanded_to_host(dp_ctx* ctx, const Devices& devs, const int32_t* dev, const int64_t* pdm,
+                                        int32_t n) {
+  const int32_t D = devs.D;
+  dp_placement_result_t* p = new_placement(n, D, 0);
+  std::vector<int32_t> d = to_host(ctx, dev, n);
+  std::vector<int64_t> m = to_host(ctx, pdm, D);
+  std::vector<uint8_t> present(D, 0);
+  for (int32_t v = 0; v < n; ++v) {
+    p->device[v] = devs.ids[d[v]];
+    present[d[v]] = 1;
+  }
+  for (int32_t i = 0; i < D; ++i) {
+    p->device_ids[i] = devs.ids[i];
+    p->per_device_memory[i] = present[i] ? m[i] : 0;
+    p->device_present[i] = present[i];
+  }
+  return p;
+}
+
+}  // namespace dpb
+
+struct dp_resident : dpb::Resident {};
+
+using namespace dpb;
+
+extern "C" {
+
+int dp_pipeline(dp_ctx_t* ctx, const dp_graph_t* h, const dp_devices_t* devices, dp_comm_t comm,
+                const dp_pipeline_config_t* cfg, dp_pipeline_result_t** out) {
+  DP_API_BEGIN(ctx)
+  Resident r;
+  resident_init(r, ctx, h, devices, comm, cfg);
+  cudaEvent_t e0, e1;
+  DP_CUDA(cudaEventCreate(&e0));
+  DP_CUDA(cudaEventCreate(&e1));
+  struct EvGuard {
+    cudaEvent_t a, b;
+    ~EvGuard() {
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+  } guard{e0, e1};
+  // require_valid + ccr precede the window (pipeline.cpp:33, :58)
+  {
+    DevGraph& g = r.g;
+    graph_resolve(g);
+    graph_adjacency(g);
+    Validation v = graph_validate(g, h, false, true);
+    if (v.code) fail(v.code, "%s", v.message.c_str());
+    graph_costs(g, comm);
+    r.original_ccr = ccr_dev(g);
+  }
+  DP_CUDA(cudaEventRecord(e0, ctx->stream));
+  fuse_dev(r.g, r.comm, r.cfg.fusion_range, r.limit, r.f);
+  DevGraph& coarse = r.f.coarse;
+  levels_dev(coarse, r.comm, r.ct, r.cb, r.cc);
+  const int32_t k = coarse.n, n = r.g.n, D = r.devs.D;
+  r.cseq.alloc(ctx, k > 0 ? k : 1);
+  r.cpos.alloc(ctx, k > 0 ? k : 1);
+  topo_order(coarse, DP_TOPO_CPD, r.cc.p, r.cseq.p, r.cpos.p);
+  place_dev(coarse, r.cseq.p, r.devs, &r.po, &r.pa, true);
+  r.dev_order.alloc(ctx, n > 0 ? n : 1);
+  r.dev_adjust.alloc(ctx, n > 0 ? n : 1);
+  r.pdm_order.alloc(ctx, D);
+  r.pdm_adjust.alloc(ctx, D);
+  expand_dev(r.g, r.f.node_cluster.p, r.po.dev.p, D, r.dev_order.p, r.pdm_order.p);
+  expand_dev(r.g, r.f.node_cluster.p, r.pa.dev.p, D, r.dev_adjust.p, r.pdm_adjust.p);
+  DP_CUDA(cudaEventRecord(e1, ctx->stream));
+  auto* res = halloc<dp_pipeline_result_t>(1);
+  res->original_nodes = n;
+  res->original_edges = r.g.m;
+  res->original_ccr = r.original_ccr;
+  res->coarse_nodes = k;
+  res->coarse_edges = coarse.m;
+  res->fusion = halloc<dp_fusion_result_t>(1);
+  res->fusion->coarse = graph_to_host(coarse, true);
+  res->fusion->map = fuse_map_to_host(r.g, r.f);
+  std::vector<int32_t> cs = to_host(ctx, r.cseq.p, k);
+  res->coarse_sequence = halloc<int64_t>(k);
+  std::vector<int64_t> cids(static_cast<size_t>(k));
+  for (int32_t i = 0; i < k; ++i) cids[i] = res->coarse_sequence[i] = cs[i];
+  res->coarse_order = placement_to_host(ctx, r.devs, r.po, k, &cids, false);
+  res->coarse_adjust = placement_to_host(ctx, r.devs, r.pa, k, &cids, true);
+  res->order_expanded = expanded_to_host(ctx, r.devs, r.dev_order.p, r.pdm_order.p, n);
+  res->adjust_expanded = expanded_to_host(ctx, r.devs, r.dev_adjust.p, r.pdm_adjust.p, n);
+  float ms = 0;
+  DP_CUDA(cudaEventSynchronize(e1));
+  DP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  res->generation_ms = ms;
+  res->coarse_ccr = 0.0;
+  if (coarse.m > 0) res->coarse_ccr = ccr_dev(coarse);  // pipeline.cpp:83
+  res->order_makespan = res->adjust_makespan = -1;
+  if (cfg->simulate) {  // pipeline.cpp:89-90
+    dp_sim_report_t* so = sim_report(r.g, r.devs, r.dev_order.p, false);
+    dp_sim_report_t* sa = sim_report(r.g, r.devs, r.dev_adjust.p, false);
+    res->order_makespan = so->makespan;
+    res->adjust_makespan = sa->makespan;
+    free_sim(so);
+    free_sim(sa);
+  }
+  *out = res;
+  DP_API_END
+}
+
+int dp_resident_create(dp_ctx_t* ctx, const dp_graph_t* h, const dp_devices_t* devices, dp_comm_t comm,
+                       const dp_pipeline_config_t* cfg, dp_resident_t** out) {
+  DP_API_BEGIN(ctx)
+  auto* r = new dp_resident;
+  try {
+    resident_init(*r, ctx, h, devices, comm, cfg);
+    // keep a private host copy of the ids/edges for error messages raised later
+    r->host_copy = *h;
+    r->host = &r->host_copy;
+    sync(ctx);
+  } catch (...) {
+    delete r;
+    throw;
+  }
+  *out = r;
+  DP_API_END
+}
+
+int dp_resident_generate(dp_resident_t* r) {
+  DP_API_BEGIN(r ? r->ctx : nullptr)
+  resident_generate(*r, false);
+  DP_API_END
+}
+
+int dp_resident_fetch(dp_resident_t* r, int32_t* order_device, int32_t* adjust_device, int64_t* coarse_nodes,
+                      int64_t* coarse_edges) {
+  DP_API_BEGIN(r ? r->ctx : nullptr)
+  dp_ctx* ctx = r->ctx;
+  const int32_t n = r->g.n;
+  // device positions -> ids on the host side of the copy
+  std::vector<int32_t> a = to_host(ctx, r->dev_order.p, n), b = to_host(ctx, r->dev_adjust.p, n);
+  for (int32_t v = 0; v < n; ++v) {
+    order_device[v] = r->devs.ids[a[v]];
+    adjust_device[v] = r->devs.ids[b[v]];
+  }
+  if (coarse_nodes) *coarse_nodes = r->f.coarse.n;
+  if (coarse_edges) *coarse_edges = r->f.coarse.m;
+  DP_API_END
+}
+
+void dp_resident_destroy(dp_resident_t* r) {
+  if (!r) return;
+  cudaSetDevice(r->ctx->device);
+  cudaStreamSynchronize(r->ctx->stream);
+  delete r;
+}
+
+}  // extern "C"

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdlib>
+#include <new>
 #include <cstring>
 
 #include "../../include/dagplace_b200.h"

@@ -96,3 +96,67 @@ def test_breakpoints_medium(gpu, oracle, n, w, r):
     from compare import same_graph, same_map
     same_graph(ca, cb)
     same_map(ma, mb)
+
+
+@pytest.mark.parametrize("name", sorted(VALID))
+def test_placement(gpu, oracle, name):
+    parity.check_placement(gpu, oracle, VALID[name], name)
+
+
+@pytest.mark.parametrize("name", sorted(VALID))
+def test_simulate(gpu, oracle, name):
+    parity.check_simulate(gpu, oracle, VALID[name], name)
+
+
+@pytest.mark.parametrize("name", sorted(VALID))
+def test_pipeline(gpu, oracle, name):
+    parity.check_pipeline(gpu, oracle, VALID[name], name)
+
+
+@pytest.mark.parametrize("name", ["layered_small", "groups_layered", "shuf_relabel"])
+def test_pipeline_vs_reference(gpu, ref, name):
+    parity.check_pipeline(gpu, ref, VALID[name], name)
+    parity.check_simulate(gpu, ref, VALID[name], name, seeds=(0,))
+
+
+def test_expand_errors(gpu, oracle):
+    from compare import outcome, same_placement
+    g = VALID["rdag3"]
+    m = oracle.fuse(g, GEN, 4, 10 ** 9)[1]
+    k = m.n_clusters
+    devs = np.arange(k, dtype=np.int32) % 3 + 5
+    a = outcome(gpu.expand_placement, g, m, devs)
+    b = outcome(oracle.expand_placement, g, m, devs)
+    assert a[0] == b[0] == "ok"
+    same_placement(a[1], b[1])
+    placed = np.ones(k, np.uint8)
+    placed[k // 2] = 0
+    assert outcome(gpu.expand_placement, g, m, devs, placed)[1:] == outcome(oracle.expand_placement, g, m, devs, placed)[1:]
+
+
+def test_bruteforce(gpu, oracle):
+    for s in range(4):
+        g = random_dag(50 + s, 6 + s, 0.2, max_bytes=40)
+        devs = [(7, 10 ** 6), (2, int(g.memory_bytes.sum()) // 2 + 1), (4, 10 ** 6)][: 2 + s % 2]
+        for comm in (UNIT, GEN):
+            a = gpu.brute_force_optimal(g, devs, comm)
+            b = oracle.brute_force_optimal(g, devs, comm)
+            assert a[1] == b[1]
+            same(a[0], b[0], "assignment")
+
+
+def test_candidates(gpu, oracle):
+    g = layered(8, 2000, 32)
+    _, m = oracle.fuse(g, GEN, 200, int(g.memory_bytes.sum()) // 8)
+    rng = np.random.default_rng(1)
+    cand = rng.integers(0, 8, (64, m.n_clusters)).astype(np.uint8)
+    devs = [(d, 10 ** 12) for d in range(8)]
+    ma, ia = gpu.simulate_candidates(g, m.node_cluster, m.n_clusters, cand, devs, GEN)
+    mb, ib = oracle.simulate_candidates(g, m.node_cluster, m.n_clusters, cand, devs, GEN)
+    same(ma, mb, "makespans")
+    assert ia == ib
+
+
+def test_pipeline_medium(gpu, oracle):
+    g = layered(77, 20000, 64)
+    parity.check_pipeline(gpu, oracle, g, "layered20k", d=8)
