@@ -351,6 +351,19 @@ int dp_gen_layered(int64_t n, int64_t width, int64_t fan_lo, int64_t fan_hi, uin
                    int64_t* node_id, int64_t* compute_us, int64_t* memory_bytes,
                    int64_t* edge_src, int64_t* edge_dst, int64_t* edge_bytes, int64_t* n_edges);
 
+/* Config #2 GNMT-like chains and config #3 BERT-like skip-layered graphs. */
+int dp_gen_gnmt(int64_t chains, int64_t T, uint64_t seed, int64_t* node_id, int64_t* compute_us,
+                int64_t* memory_bytes, int64_t* edge_src, int64_t* edge_dst, int64_t* edge_bytes, int64_t* n_edges);
+int dp_gen_bert(int64_t n, int64_t width, int64_t skip, uint64_t seed, int64_t* node_id, int64_t* compute_us,
+                int64_t* memory_bytes, int64_t* edge_src, int64_t* edge_dst, int64_t* edge_bytes, int64_t* n_edges);
+
+/* Config #5 candidate family: candidate 0 = base (device position per
+ * cluster); candidate k > 0 applies max(1, n_clusters/100) moves drawn from
+ * std::mt19937_64(k): cluster rk() % n_clusters -> device rk() % D.  Writes candidates
+ * first .. first+count-1 into out[count * n_clusters]. */
+int dp_gen_candidates(const uint8_t* base, int64_t n_clusters, int32_t D, int64_t first, int64_t count,
+                      uint8_t* out);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

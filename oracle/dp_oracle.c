@@ -1817,6 +1817,11 @@ int dpo_pipeline(const dp_graph_t* g, const dp_devices_t* devices, dp_comm_t com
   r->coarse_edges = coarse.n_edges;
   if (coarse.n_edges == 0) r->coarse_ccr = 0.0;
   else if ((rc = dpo_ccr(&coarse, comm, &r->coarse_ccr))) { dpr_pipeline_free_(r); return rc; }
+  r->order_makespan = r->adjust_makespan = -1;
+  if (!cfg->simulate) {
+    *out = r;
+    return 0;
+  }
   dp_sim_report_t* sr = NULL;
   if ((rc = dpo_simulate(g, r->order_expanded->device, devices, comm, 0, &sr))) { dpr_pipeline_free_(r); return rc; }
   r->order_makespan = sr->makespan;

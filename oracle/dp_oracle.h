@@ -88,6 +88,11 @@ int dpr_pipeline_replicas(const dp_graph_t* g, const dp_devices_t* devices, dp_c
                           const dp_pipeline_config_t* cfg, int32_t threads, int64_t* wall_us,
                           double* total_wall_s);
 
+/* Reference-only: gen_graph (generator.cpp:203-209). */
+int dpr_gen_graph(int32_t kind, int64_t n, int32_t width, double target_ccr, uint64_t seed, int64_t* node_id,
+                  int64_t* compute_us, int64_t* memory_bytes, int64_t* edge_src, int64_t* edge_dst,
+                  int64_t* edge_bytes, int64_t* n_edges);
+
 #ifdef __cplusplus
 }
 #endif

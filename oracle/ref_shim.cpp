@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "dagplace/fusion.hpp"
+#include "dagplace/generator.hpp"
 #include "dagplace/graph.hpp"
 #include "dagplace/graph_index.hpp"
 #include "dagplace/ordering.hpp"
@@ -558,6 +559,34 @@ int dpr_pipeline(const dp_graph_t* g, const dp_devices_t* devices, dp_comm_t com
     o->adjust_makespan = rep.adjusting.makespan_us;
     o->generation_ms = static_cast<double>(rep.generation_wall_us) / 1000.0;
     *out = o;
+    return 0;
+  } catch (const DagError& e) { return fail(e); }
+}
+
+// gen_graph (generator.cpp:203-209) flattened; kind 0 layered, 1 random, 2 chains;
+// target_ccr <= 0 means none.  Arrays sized by the caller (n nodes, n*3 edges).
+int dpr_gen_graph(int32_t kind, int64_t n, int32_t width, double target_ccr, uint64_t seed, int64_t* node_id,
+                  int64_t* compute_us, int64_t* memory_bytes, int64_t* edge_src, int64_t* edge_dst,
+                  int64_t* edge_bytes, int64_t* n_edges) {
+  try {
+    SyntheticSpec spec;
+    spec.kind = kind == 0 ? GenKind::Layered : kind == 1 ? GenKind::RandomDag : GenKind::ParallelChains;
+    spec.node_count = static_cast<int>(n);
+    spec.layer_width = width;
+    if (target_ccr > 0) spec.target_ccr = target_ccr;
+    spec.seed = seed;
+    ComputationGraph g = gen_graph(spec);
+    for (size_t i = 0; i < g.nodes.size(); ++i) {
+      node_id[i] = g.nodes[i].id;
+      compute_us[i] = g.nodes[i].compute_us;
+      memory_bytes[i] = g.nodes[i].memory_bytes;
+    }
+    for (size_t e = 0; e < g.edges.size(); ++e) {
+      edge_src[e] = g.edges[e].src;
+      edge_dst[e] = g.edges[e].dst;
+      edge_bytes[e] = g.edges[e].tensor_bytes;
+    }
+    *n_edges = static_cast<int64_t>(g.edges.size());
     return 0;
   } catch (const DagError& e) { return fail(e); }
 }

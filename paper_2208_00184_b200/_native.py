@@ -22,6 +22,7 @@ HEADER_SYMBOLS = [
     "dp_placement_result_free", "dp_simulate", "dp_sim_report_free", "dp_simulate_candidates",
     "dp_brute_force_optimal", "dp_pipeline", "dp_pipeline_result_free", "dp_resident_create",
     "dp_resident_generate", "dp_resident_fetch", "dp_resident_destroy", "dp_gen_layered",
+    "dp_gen_candidates", "dp_gen_gnmt", "dp_gen_bert",
 ]
 
 
@@ -57,6 +58,17 @@ def declare(lib: C.CDLL) -> None:
     lib.dp_gen_layered.restype = C.c_int
     lib.dp_gen_layered.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_uint64,
                                    I64P, I64P, I64P, I64P, I64P, I64P, I64P]
+    _declare_gen(lib)
+
+
+def _declare_gen(lib):
+    lib.dp_gen_gnmt.restype = C.c_int
+    lib.dp_gen_gnmt.argtypes = [C.c_int64, C.c_int64, C.c_uint64] + [I64P] * 7
+    lib.dp_gen_bert.restype = C.c_int
+    lib.dp_gen_bert.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_uint64] + [I64P] * 7
+    lib.dp_gen_candidates.restype = C.c_int
+    lib.dp_gen_candidates.argtypes = [C.POINTER(C.c_uint8), C.c_int64, C.c_int32, C.c_int64, C.c_int64,
+                                      C.POINTER(C.c_uint8)]
 
 
 def stage_times(lib: C.CDLL, ctx) -> list:

@@ -60,17 +60,19 @@ void ctx_activate(dp_ctx* ctx);
 
 // Stage timing: CUDA events recorded on the context stream around each stage.
 void stage_reset(dp_ctx* ctx);
-void stage_begin(dp_ctx* ctx, const char* name, double bytes);
-void stage_end(dp_ctx* ctx);
+size_t stage_begin(dp_ctx* ctx, const char* name, double bytes);
+void stage_end(dp_ctx* ctx, size_t idx);
 void stage_resolve(dp_ctx* ctx);
 
 struct StageScope {
   dp_ctx* ctx;
-  StageScope(dp_ctx* c, const char* name, double bytes = 0.0) : ctx(c) {
-    if (ctx->timing) stage_begin(ctx, name, bytes);
+  size_t idx = 0;
+  bool on;
+  StageScope(dp_ctx* c, const char* name, double bytes = 0.0) : ctx(c), on(c->timing) {
+    if (on) idx = stage_begin(ctx, name, bytes);
   }
   ~StageScope() {
-    if (ctx->timing) stage_end(ctx);
+    if (on) stage_end(ctx, idx);
   }
 };
 

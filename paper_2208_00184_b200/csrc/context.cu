@@ -64,7 +64,7 @@ void stage_reset(dp_ctx* ctx) {
   ctx->stage_ms.clear();
 }
 
-void stage_begin(dp_ctx* ctx, const char* name, double bytes) {
+size_t stage_begin(dp_ctx* ctx, const char* name, double bytes) {
   Stage s;
   if (!ctx->event_pool.empty()) {
     s = ctx->event_pool.back();
@@ -77,11 +77,12 @@ void stage_begin(dp_ctx* ctx, const char* name, double bytes) {
   s.bytes = bytes;
   DP_CUDA(cudaEventRecord(s.a, ctx->stream));
   ctx->stages.push_back(s);
+  return ctx->stages.size() - 1;
 }
 
-void stage_end(dp_ctx* ctx) {
-  if (ctx->stages.empty()) return;
-  DP_CUDA(cudaEventRecord(ctx->stages.back().b, ctx->stream));
+void stage_end(dp_ctx* ctx, size_t idx) {
+  if (idx >= ctx->stages.size()) return;
+  DP_CUDA(cudaEventRecord(ctx->stages[idx].b, ctx->stream));
 }
 
 void stage_resolve(dp_ctx* ctx) {

@@ -27,6 +27,28 @@ def layered(n: int, width: int, fan_lo: int = 2, fan_hi: int = 6, seed: int = 12
     return Graph(a[0], a[1], a[2], a[3][:k].copy(), a[4][:k].copy(), a[5][:k].copy())
 
 
+def _run(fn, n, cap_edges, *lead):
+    lib = _lib()
+    a = [np.zeros(n, np.int64) for _ in range(3)] + [np.zeros(cap_edges, np.int64) for _ in range(3)]
+    m = C.c_int64()
+    p = lambda x: x.ctypes.data_as(C.POINTER(C.c_int64))  # noqa: E731
+    rc = getattr(lib, fn)(*lead, *[p(x) for x in a], C.byref(m))
+    if rc:
+        raise RuntimeError(lib.dp_last_error_message().decode())
+    k = m.value
+    return Graph(a[0], a[1], a[2], a[3][:k].copy(), a[4][:k].copy(), a[5][:k].copy())
+
+
+def gnmt(chains: int = 8, T: int = 6250, seed: int = 2) -> Graph:
+    """Config #2: GNMT-like chains (dp_gen_gnmt)."""
+    return _run("dp_gen_gnmt", chains * T, chains * T * 3, chains, T, seed)
+
+
+def bert(n: int = 200_000, width: int = 512, skip: int = 16, seed: int = 3) -> Graph:
+    """Config #3: BERT-like layered + skip edges (dp_gen_bert)."""
+    return _run("dp_gen_bert", n, n * 7, n, width, skip, seed)
+
+
 def capacity_125(g: Graph, d: int) -> int:
     """#4/#5 device capacity: total/D + total/(4D) in integer arithmetic."""
     total = int(g.memory_bytes.sum())
@@ -45,3 +67,15 @@ def config5_graph():
     g = layered(100_000, 256, 2, 6, 12345)
     cap = capacity_125(g, 8)
     return g, [(d, cap) for d in range(8)]
+
+
+def candidates(base_dev_pos: np.ndarray, D: int, first: int, count: int) -> np.ndarray:
+    """Config #5 candidate family rows first..first+count-1 (dp_gen_candidates)."""
+    lib = _lib()
+    base = np.ascontiguousarray(base_dev_pos, dtype=np.uint8)
+    out = np.zeros((count, base.size), np.uint8)
+    u8 = C.POINTER(C.c_uint8)
+    rc = lib.dp_gen_candidates(base.ctypes.data_as(u8), base.size, D, first, count, out.ctypes.data_as(u8))
+    if rc:
+        raise RuntimeError(lib.dp_last_error_message().decode())
+    return out
