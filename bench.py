@@ -312,7 +312,7 @@ def candidates(args, be, lib, rank, world):
     B = args.candidates
     per = (B + world - 1) // world
     lo, hi = rank * per, min(B, (rank + 1) * per)
-    cand = synth.candidates(base, rep.coarse_nodes, len(devs), lo, max(0, hi - lo))
+    cand = synth.candidates(base, len(devs), lo, max(0, hi - lo))
     # warm-up on a slice, then the timed batch
     be.simulate_candidates(g, rep.map.node_cluster, rep.coarse_nodes, cand[:min(len(cand), 64)], devs, COMM)
     if world > 1:
