@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--stages", action="store_true", help="print per-stage device times to stderr")
+    p.add_argument("--replicas", type=int, default=32,
+                   help="independent graphs generated concurrently per GPU (one stream + host thread each)")
     return p.parse_args()
 
 
@@ -125,6 +127,14 @@ def pinned_graph(g):
     return pg
 
 
+def _new_ctx(lib, device, stream):
+    ctx = C.c_void_p()
+    rc = lib.dp_ctx_create(device, C.c_void_p(stream), C.byref(ctx))
+    if rc:
+        raise RuntimeError(lib.dp_last_error_message().decode())
+    return ctx
+
+
 def flush_l2(buf):
     buf.add_(1)  # 256 MiB write > 126 MB L2
 
@@ -161,6 +171,7 @@ def ours(args):
         if rc:
             raise RuntimeError(lib.dp_last_error_message().decode())
 
+    # ---- single-graph latency (one placement generation at a time)
     launches0 = lib.dp_ctx_launch_count(ctx)
     for _ in range(args.warmup):
         flush_l2(flush)
@@ -168,31 +179,83 @@ def ours(args):
     torch.cuda.synchronize()
     launches_w = lib.dp_ctx_launch_count(ctx)
     per_step_launches = (launches_w - launches0) / max(1, args.warmup)
-    # timed region: K steps, device-timed with CUDA events on the launching stream
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush_l2(flush)
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    single_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+
+    # ---- throughput: R independent graphs per GPU at once (own stream, context and host
+    # thread each), like the reference arm's independent graphs on all host cores
+    R = max(1, args.replicas)
+    reps = []
+    for r in range(R):
+        st = torch.cuda.Stream()
+        rbe = pkg.Backend(lib, "dp_", ctx=_new_ctx(lib, local, st.cuda_stream), name=f"rep{r}")
+        rres = C.c_void_p()
+        rc = lib.dp_resident_create(rbe.ctx, C.byref(gc), C.byref(dc), comm_c(COMM), C.byref(cfg), C.byref(rres))
+        if rc:
+            raise RuntimeError(lib.dp_last_error_message().decode())
+        reps.append((st, rbe, rres))
+    torch.cuda.synchronize()
+
+    def run_all():
+        errs = []
+
+        def work(rres):
+            rc = lib.dp_resident_generate(rres)
+            if rc:
+                errs.append(lib.dp_last_error_message().decode())
+        ths = [threading.Thread(target=work, args=(rr,)) for _, _, rr in reps]
+        for t_ in ths:
+            t_.start()
+        for t_ in ths:
+            t_.join()
+        if errs:
+            raise RuntimeError(errs[0])
+
+    for _ in range(max(1, args.warmup // 2)):
+        flush_l2(flush)
+        run_all()
+    torch.cuda.synchronize()
+    master = stream
+    evs = []
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    l0 = lib.dp_ctx_launch_count(ctx)
+    l0 = sum(lib.dp_ctx_launch_count(rb.ctx) for _, rb, _ in reps)
     with Clocks(local) as clocks:
         t0 = time.perf_counter()
         for i in range(args.steps):
             flush_l2(flush)
-            ev[i][0].record(stream)
-            step()
-            ev[i][1].record(stream)
+            start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            start.record(master)
+            for st, _, _ in reps:
+                st.wait_event(start)
+            run_all()
+            for st, _, _ in reps:
+                e = torch.cuda.Event()
+                e.record(st)
+                master.wait_event(e)
+            stop.record(master)
+            evs.append((start, stop))
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
     if world > 1:
         torch.distributed.barrier()
-    launches = lib.dp_ctx_launch_count(ctx) - l0
-    step_ms = [a.elapsed_time(b) for a, b in ev]
+    launches = sum(lib.dp_ctx_launch_count(rb.ctx) for _, rb, _ in reps) - l0
+    step_ms = [a.elapsed_time(b) for a, b in evs]
     mean_ms = float(np.mean(step_ms))
     t = torch.tensor([mean_ms], device="cuda")
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     max_ms = float(t.item())
-    value = world * g.m / (max_ms / 1e3)
+    value = world * R * g.m / (max_ms / 1e3)
+    for _, rb, rres in reps:
+        lib.dp_resident_destroy(rres)
 
     # per-stage device times of one extra, separately-timed step (roofline evidence)
     lib.dp_ctx_enable_stage_timing(ctx, 1)
@@ -237,39 +300,56 @@ def ours(args):
     # e2e through the public C-ABI (dp_pipeline): pinned H2D + generation + D2H of the report
     e2e = None
     if not args.no_e2e:
+        # the public C-ABI call (dp_pipeline) with pinned host buffers: H2D upload,
+        # generation, D2H of the report; R calls at once like the device-resident step
         pg = pinned_graph(g)
         pgc = pg.c()
         from paper_2208_00184_b200._abi import PipelineC
         pcfg = PipelineCfgC(200, 0.25, 1, 0)
-        f = lib.dp_pipeline
+        d2h_box = [0]
+
+        def e2e_all():
+            errs = []
+
+            def work(rb):
+                p = C.POINTER(PipelineC)()
+                rc = lib.dp_pipeline(rb.ctx, C.byref(pgc), C.byref(dc), comm_c(COMM), C.byref(pcfg), C.byref(p))
+                if rc:
+                    errs.append(lib.dp_last_error_message().decode())
+                    return
+                r = p.contents
+                k, mc, n = r.coarse_nodes, r.coarse_edges, g.n
+                # coarse graph, cluster map, two coarse placements (+ decisions), two
+                # expanded placements, coarse sequence
+                d2h_box[0] = (k * 8 * 3 + mc * 8 * 3) + (n * 4 + n * 8 + k * 8 * 3) + 2 * (k * 4 + 8 * 8) + \
+                    k * (8 + 4 + 8 + 8 * 8 + 4 + 2) + 2 * (n * 4 + 8 * 8) + k * 8
+                lib.dp_pipeline_result_free(p)
+            ths = [threading.Thread(target=work, args=(rb,)) for _, rb, _ in reps]
+            for t_ in ths:
+                t_.start()
+            for t_ in ths:
+                t_.join()
+            if errs:
+                raise RuntimeError(errs[0])
+
+        e2e_all()  # warm-up
         times = []
-        d2h = 0
-        for i in range(max(1, min(3, args.steps)) + 1):
+        for i in range(max(1, min(3, args.steps))):
             flush_l2(flush)
             torch.cuda.synchronize()
             t1 = time.perf_counter()
-            p = C.POINTER(PipelineC)()
-            rc = f(ctx, C.byref(pgc), C.byref(dc), comm_c(COMM), C.byref(pcfg), C.byref(p))
+            e2e_all()
             torch.cuda.synchronize()
-            dt = time.perf_counter() - t1
-            if rc:
-                raise RuntimeError(lib.dp_last_error_message().decode())
-            r = p.contents
-            k, mc, n = r.coarse_nodes, r.coarse_edges, g.n
-            # bytes copied back: coarse graph, cluster map, two coarse placements (+ decisions),
-            # two expanded placements, coarse sequence
-            d2h = (k * 8 * 3 + mc * 8 * 3) + (n * 4 + n * 8 + k * 8 * 3) + 2 * (k * 4 + 8 * 8) + \
-                k * (8 + 4 + 8 + 8 * 8 + 4 + 2) + 2 * (n * 4 + 8 * 8) + k * 8
-            lib.dp_pipeline_result_free(p)
-            if i > 0:
-                times.append(dt)
+            times.append(time.perf_counter() - t1)
         e2e_s = float(np.mean(times))
         tt = torch.tensor([e2e_s], device="cuda")
         if world > 1:
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        e2e = {"value": world * g.m / float(tt.item()), "unit": "edges/s", "ms_per_step": float(tt.item()) * 1e3,
-               "h2d_bytes_per_step": int(8 * (3 * g.n + 3 * g.m)), "d2h_bytes_per_step": int(d2h),
-               "api": "dp_pipeline (C-ABI, pinned host buffers)"}
+        e2e = {"value": world * R * g.m / float(tt.item()), "unit": "edges/s", "ms_per_step": float(tt.item()) * 1e3,
+               "h2d_bytes_per_step": int(R * 8 * (3 * g.n + 3 * g.m)), "d2h_bytes_per_step": int(R * d2h_box[0]),
+               "api": f"dp_pipeline (C-ABI, pinned host buffers), {R} concurrent calls"}
+    for _, rb, _ in reps:
+        lib.dp_ctx_destroy(rb.ctx)
 
     cand = candidates(args, be, lib, rank, world) if args.candidates > 0 else None
 
@@ -281,12 +361,15 @@ def ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms, "higher_is_better": True, "scaling": "weak",
+            "single_graph": {"ms": single_ms, "edges_per_s": g.m / (single_ms / 1e3),
+                             "note": "one placement generation at a time (latency)"},
             "vs_baseline": None, "dtype": "int64", "data": "synthetic (SURVEY §8(d) layered recipe, seed 12345)",
             "config": {"workload": f"config#4 {args.variant}: 1M-op layered DAG "
                                    f"(W={'1024' if deep else '65536'}, fan-in 2..6), 8 devices, R=200, "
-                                   f"M=0.25*capacity, replicas per GPU",
+                                   f"M=0.25*capacity; {R} independent graphs per GPU generated concurrently",
+                       "replicas_per_gpu": R,
                        "nodes": g.n, "edges": g.m, "coarse_nodes": cn.value, "coarse_edges": ce.value,
-                       "parallelism": f"replicas x{world}", "l2": "flushed between steps (256 MiB write)"},
+                       "parallelism": f"independent graphs: {R} per GPU x {world} GPU(s)", "l2": "flushed between steps (256 MiB write)"},
             "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": int(launches),
             "gpu_launches_per_step": per_step_launches, "wall_s_timed_region": wall,
             "step_ms_all": [round(x, 3) for x in step_ms],

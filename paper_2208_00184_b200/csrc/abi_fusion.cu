@@ -45,9 +45,10 @@ __global__ void __launch_bounds__(256) k_bfs(BfsArgs a) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
   int32_t lb = 0;
+  int32_t le = a.counters[0];
+  grid_barrier(a.bar, gridDim.x);
   for (;;) {
-    int32_t le = *((volatile int*)&a.counters[0]);
-    if (le == lb || *((volatile int*)&a.counters[1])) break;
+    if (le == lb) break;  // run to completion: an early exit on `found` could split the barrier
     for (int64_t i = lb + tid; i < le; i += nth) {
       int32_t u = a.queue[i];
       for (int32_t k = a.out_off[u]; k < a.out_off[u + 1]; ++k) {
@@ -62,8 +63,9 @@ __global__ void __launch_bounds__(256) k_bfs(BfsArgs a) {
         if (fresh) a.queue[slot] = x;
       }
     }
-    grid_barrier(a.bar, gridDim.x);
+    grid_barrier(a.bar, gridDim.x, &a.counters[0], &a.counters[2]);
     lb = le;
+    le = *((volatile int*)&a.counters[2]);
   }
 }
 
@@ -126,9 +128,9 @@ int dp_merge_is_safe(dp_ctx_t* ctx, const dp_graph_t* h, int64_t u, int64_t v, i
   int one = 1;
   DP_CUDA(cudaMemcpyAsync(visited.p + ui, &one, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
   DP_CUDA(cudaMemcpyAsync(queue.p, &ui, sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
-  DevBuf<int> counters(ctx, 2);
-  int c0[2] = {1, 0};
-  counters.upload(c0, 2);
+  DevBuf<int> counters(ctx, 3);
+  int c0[3] = {1, 0, 0};
+  counters.upload(c0, 3);
   DevBuf<unsigned> bar(ctx, 2);
   bar.zero();
   BfsArgs a{g.out_off.p, g.out_dst.p, g.out_eid.p, ui, vi, de, visited.p, queue.p, counters.p, bar.p};

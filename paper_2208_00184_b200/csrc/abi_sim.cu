@@ -175,7 +175,6 @@ int dp_simulate_candidates(dp_ctx_t* ctx, const dp_graph_t* h, const int32_t* no
   simulate_batch_dev(g, in, o);
   o.makespan.download(makespans, B);
   sync(ctx);
-  if (ctx->timing) stage_resolve(ctx);
   int64_t best = -1;
   for (int64_t b = 0; b < B; ++b)
     if (best < 0 || makespans[b] < makespans[best]) best = b;  // first strict minimum

@@ -5,13 +5,32 @@
 
 #include "common.cuh"
 
+namespace dpb {
+// Resolves the stage events of a timed call when the entry point returns normally.
+struct StageResolver {
+  dp_ctx* ctx;
+  bool ok = false;
+  explicit StageResolver(dp_ctx* c) : ctx(c) {}
+  ~StageResolver() {
+    if (ok && ctx && ctx->timing) {
+      try {
+        stage_resolve(ctx);
+      } catch (...) {
+      }
+    }
+  }
+};
+}  // namespace dpb
+
 #define DP_API_BEGIN(ctx)                                                    \
+  ::dpb::StageResolver dp_stage_resolver_(ctx);                              \
   try {                                                                      \
     if (!(ctx)) ::dpb::fail(DP_E_ARGUMENT, "null dp_ctx_t");                 \
     ::dpb::ctx_activate(ctx);                                                \
     if ((ctx)->timing) ::dpb::stage_reset(ctx);
 
 #define DP_API_END                                                           \
+    dp_stage_resolver_.ok = true;                                            \
   }                                                                          \
   catch (const ::dpb::DpFail& f_) {                                          \
     ::dpb::set_last_error(f_.code, f_.msg);                                  \

@@ -205,19 +205,25 @@ __device__ __forceinline__ int warp_append(int* counter, bool want) {
 }
 
 // Sense-reversing grid barrier for persistent kernels launched cooperatively (every CTA
-// resident).  `bar[0]` = arrival count, `bar[1]` = generation.
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
+// resident).  `bar[0]` = arrival count, `bar[1]` = generation.  When `snap_src` is set,
+// the last CTA to arrive copies *snap_src into *snap_dst before releasing the others, so
+// every CTA reads one consistent value produced before the barrier (e.g. the end of the
+// next frontier) even though fast CTAs start appending right after it.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks, const int* snap_src = nullptr,
+                                             int* snap_dst = nullptr) {
   __syncthreads();
   if (threadIdx.x == 0) {
     volatile unsigned* gen = bar + 1;
     unsigned g = *gen;
     __threadfence();
     if (atomicAdd(bar, 1u) == nblocks - 1) {
+      if (snap_src) *((volatile int*)snap_dst) = *((volatile const int*)snap_src);
       bar[0] = 0;
       __threadfence();
       atomicAdd(bar + 1, 1u);
     } else {
       while (*gen == g) {
+        __nanosleep(32);
       }
     }
     __threadfence();

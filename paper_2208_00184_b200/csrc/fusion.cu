@@ -15,6 +15,7 @@
 
 #include "fusion.cuh"
 #include "peel.cuh"
+#include "peel_dp.cuh"
 #include "results.h"
 
 namespace dpb {
@@ -506,9 +507,18 @@ void breakpoints_dev(DevGraph& g, const int32_t* seq, const int32_t* pos_of, int
                 prev_cut.p);
     }
   }
+  clusters_from_prev_cut(g, seq, prev_cut.p, out);
+}
+
+// Cut traceback and clusters_from_cuts (fusion.cpp:61-81, 164-170) on the device.
+void clusters_from_prev_cut(DevGraph& g, const int32_t* seq, const int32_t* prev_cut, Clusters& out) {
+  dp_ctx* ctx = g.ctx;
+  const int B = 256;
+  const int32_t n = g.n;
+  out.n = n;
   DevBuf<uint8_t> is_cut(ctx, (size_t)n + 1);
   is_cut.zero();
-  DP_LAUNCH(ctx, k_traceback, 1, 256, 0, prev_cut.p, n, is_cut.p);
+  DP_LAUNCH(ctx, k_traceback, 1, 256, 0, prev_cut, n, is_cut.p);
   DevBuf<int32_t> f(ctx, (size_t)n + 1), fx(ctx, (size_t)n + 1);
   f.zero();
   DP_LAUNCH(ctx, k_cut_scan_in, grid_for(n, B), B, 0, is_cut.p, n, f.p);
@@ -665,10 +675,27 @@ void fuse_dev(DevGraph& g, dp_comm_t comm, int32_t range, int64_t limit, FuseOut
   const int32_t n = work.n;
   out.seq.alloc(ctx, n > 0 ? n : 1);
   out.pos_of.alloc(ctx, n > 0 ? n : 1);
-  topo_order(work, DP_TOPO_CPD, c.p, out.seq.p, out.pos_of.p);
-  if (range < 1) fail(DP_E_INVALID_VALUE, "exploration range must be >= 1");
-  if (limit <= 0) fail(DP_E_INVALID_VALUE, "cluster memory limit must be > 0");
-  breakpoints_dev(work, out.seq.p, out.pos_of.p, range, limit, out.cl);
+  if (range >= 1 && range <= 256 && limit > 0 && n > 0) {
+    // cpd_topo streamed into optimal_breakpoints (peel_dp.cu)
+    DevBuf<int32_t> prev_cut(ctx, (size_t)n + 1);
+    DevBuf<int> first(ctx, 1);
+    int big = INT32_MAX;
+    first.upload(&big, 1);
+    peel_dp_stream(work, c.p, range, limit, out.seq.p, out.pos_of.p, prev_cut.p, first.p);
+    const int fe = scalar_to_host(ctx, first.p);
+    if (fe != INT32_MAX) {  // fusion.cpp:110-115, first position in sequence order
+      const int32_t v = scalar_to_host(ctx, out.seq.p + fe);
+      fail(DP_E_NODE_EXCEEDS_CLUSTER_LIMIT, "node %lld needs %lld bytes, cluster limit is %lld",
+           (long long)scalar_to_host(ctx, work.id.p + v), (long long)scalar_to_host(ctx, work.mem.p + v),
+           (long long)limit);
+    }
+    clusters_from_prev_cut(work, out.seq.p, prev_cut.p, out.cl);
+  } else {
+    topo_order(work, DP_TOPO_CPD, c.p, out.seq.p, out.pos_of.p);
+    if (range < 1) fail(DP_E_INVALID_VALUE, "exploration range must be >= 1");
+    if (limit <= 0) fail(DP_E_INVALID_VALUE, "cluster memory limit must be > 0");
+    breakpoints_dev(work, out.seq.p, out.pos_of.p, range, limit, out.cl);
+  }
   DevBuf<int32_t> cl_work(ctx, n > 0 ? n : 1);
   DP_LAUNCH(ctx, k_cl_of_node, grid_for(n, B), B, 0, out.cl.cl_of_pos.p, out.pos_of.p, n, cl_work.p);
   coarse_graph_dev(work, cl_work.p, out.cl.k, out.cl.tot_w.p, out.cl.tot_mem.p, out.coarse);

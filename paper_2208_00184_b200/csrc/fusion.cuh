@@ -20,6 +20,9 @@ struct Clusters {
 void breakpoints_dev(DevGraph& g, const int32_t* seq, const int32_t* pos_of, int32_t range, int64_t limit,
                      Clusters& out);
 
+// Traceback of prev_cut[1..n] and the clusters of the sequence.
+void clusters_from_prev_cut(DevGraph& g, const int32_t* seq, const int32_t* prev_cut, Clusters& out);
+
 // Coarse graph (build_coarse_graph, fusion.cpp:205-225): cluster nodes and crossing
 // edges aggregated by byte sum in (cu, cv) order.  cl_of_node: cluster by node index.
 void coarse_graph_dev(DevGraph& g, const int32_t* cl_of_node, int32_t k, const int64_t* tot_w,

@@ -202,63 +202,197 @@ struct KahnArgs {
   int64_t* tlevel;
   int64_t* blevel;
   int32_t* level_of;
-  int* counters;  // [0] tail, [1] levels
+  int* counters;  // [0] tail, [1] level, [2] lb (start of the current frontier), [3] max width
   unsigned* bar;
+  int32_t narrow_max;  // narrow kernel hands over when a frontier exceeds this
 };
 
-// Persistent level-synchronous Kahn frontier.  Forward: each frontier node relaxes
-// tlevel of its children with atomicMax (max-plus, order-insensitive) and releases them
-// when their remaining in-degree hits zero; released nodes form the next frontier,
-// appended to `order` (so order is a topological order grouped by level).  Backward:
-// frontiers in reverse, blevel pulled over CSR (graph.cpp:253-261).
-__global__ void __launch_bounds__(512) k_kahn(KahnArgs a) {
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t v = tid; v < a.n; v += nth) {
-    bool src = a.indeg[v] == 0;
-    if (a.tlevel) a.tlevel[v] = 0;
-    int slot = warp_append(&a.counters[0], src);
-    if (src) a.order[slot] = static_cast<int32_t>(v);
+// Level-synchronous Kahn frontier (graph.cpp:228-244 emits the same node set per
+// level; any topological order gives the same levels).  Each frontier node relaxes the
+// tlevel of its children with atomicMax (int64 max-plus is order-insensitive) and
+// releases them when their remaining in-degree reaches zero; released nodes are
+// appended to `order`, which therefore lists the nodes level by level.
+__device__ __forceinline__ void kahn_relax_edge(const KahnArgs& a, int32_t k, int64_t t, bool* freed, int32_t* v) {
+  *v = a.out_dst[k];
+  if (a.tlevel) atomic_max_i64(&a.tlevel[*v], t + a.out_cost[k]);
+  *freed = atomicSub(&a.indeg[*v], 1) == 1;
+}
+
+// Frontier node u (or none when u < 0): short rows are handled by the owning thread with
+// up to 8 in-degree atomics in flight; rows longer than 8 are taken by the whole warp,
+// lanes striding the row.  Every lane of the warp must call this together.
+__device__ __forceinline__ void kahn_relax_warp(const KahnArgs& a, int32_t u, int32_t level, int* tail) {
+  const int lane = threadIdx.x & 31;
+  int32_t kb = 0, ke = 0;
+  int64_t t = 0;
+  if (u >= 0) {
+    if (a.level_of) a.level_of[u] = level;
+    t = a.tlevel ? a.tlevel[u] + a.w[u] : 0;
+    kb = a.out_off[u];
+    ke = a.out_off[u + 1];
   }
-  grid_barrier(a.bar, gridDim.x);
-  int32_t lb = 0, level = 0;
-  for (;;) {
-    int32_t le = *((volatile int*)&a.counters[0]);
-    if (le == lb) break;
-    if (tid == 0) a.level_off[level] = lb;
-    for (int64_t i = lb + tid; i < le; i += nth) {
-      int32_t u = a.order[i];
-      if (a.level_of) a.level_of[u] = level;
-      int64_t t = a.tlevel ? a.tlevel[u] + a.w[u] : 0;
-      int32_t kb = a.out_off[u], ke = a.out_off[u + 1];
-      for (int32_t k = kb; k < ke; ++k) {
-        int32_t v = a.out_dst[k];
-        if (a.tlevel) atomic_max_i64(&a.tlevel[v], t + a.out_cost[k]);
-        bool freed = atomicSub(&a.indeg[v], 1) == 1;
-        int slot = warp_append(&a.counters[0], freed);
-        if (freed) a.order[slot] = v;
+  const bool small = u >= 0 && ke - kb <= 8;
+  int32_t fv[8];
+  bool ff[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    ff[q] = false;
+    if (small && kb + q < ke) kahn_relax_edge(a, kb + q, t, &ff[q], &fv[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int slot = warp_append(tail, ff[q]);
+    if (ff[q]) a.order[slot] = fv[q];
+  }
+  unsigned big = __ballot_sync(0xffffffffu, u >= 0 && !small);
+  while (big) {
+    const int src = __ffs(big) - 1;
+    big &= big - 1;
+    const int32_t bkb = __shfl_sync(0xffffffffu, kb, src), bke = __shfl_sync(0xffffffffu, ke, src);
+    const int64_t bt = __shfl_sync(0xffffffffu, t, src);
+    for (int32_t k0 = bkb; k0 < bke; k0 += 32) {
+      bool fr = false;
+      int32_t v = 0;
+      if (k0 + lane < bke) kahn_relax_edge(a, k0 + lane, bt, &fr, &v);
+      const int slot = warp_append(tail, fr);
+      if (fr) a.order[slot] = v;
+    }
+  }
+}
+
+// blevel(v) = w(v) + max_s(blevel(s) + c(v,s)) pulled over CSR (graph.cpp:253-261);
+// long rows are reduced by the whole warp.  Warp-collective like kahn_relax_warp.
+__device__ __forceinline__ void kahn_pull_warp(const KahnArgs& a, int32_t v) {
+  const int lane = threadIdx.x & 31;
+  int32_t kb = 0, ke = 0;
+  if (v >= 0) {
+    kb = a.out_off[v];
+    ke = a.out_off[v + 1];
+  }
+  const bool small = v >= 0 && ke - kb <= 8;
+  if (small) {
+    int64_t best = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (kb + q < ke) {
+        const int64_t c = a.blevel[a.out_dst[kb + q]] + a.out_cost[kb + q];
+        best = c > best ? c : best;
       }
     }
-    grid_barrier(a.bar, gridDim.x);
+    a.blevel[v] = best + a.w[v];
+  }
+  unsigned big = __ballot_sync(0xffffffffu, v >= 0 && !small);
+  while (big) {
+    const int src = __ffs(big) - 1;
+    big &= big - 1;
+    const int32_t bkb = __shfl_sync(0xffffffffu, kb, src), bke = __shfl_sync(0xffffffffu, ke, src);
+    const int32_t bv = __shfl_sync(0xffffffffu, v, src);
+    int64_t best = 0;
+    for (int32_t k = bkb + lane; k < bke; k += 32) {
+      const int64_t c = a.blevel[a.out_dst[k]] + a.out_cost[k];
+      best = c > best ? c : best;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const int64_t y = __shfl_xor_sync(0xffffffffu, best, o);
+      best = y > best ? y : best;
+    }
+    if (lane == 0) a.blevel[bv] = best + a.w[bv];
+  }
+}
+
+__global__ void k_kahn_init(KahnArgs a) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < a.n; v += (int64_t)gridDim.x * blockDim.x) {
+    const bool src = a.indeg[v] == 0;
+    if (a.tlevel) a.tlevel[v] = 0;
+    const int slot = warp_append(&a.counters[0], src);
+    if (src) a.order[slot] = static_cast<int32_t>(v);
+  }
+}
+
+// One CTA, __syncthreads between levels (deep DAGs: hundreds to thousands of narrow
+// levels, where a grid barrier per level would dominate).
+__global__ void __launch_bounds__(1024) k_kahn_fwd_narrow(KahnArgs a) {
+  __shared__ int tail;
+  __shared__ int maxw;
+  __shared__ int s_le;
+  if (threadIdx.x == 0) {
+    tail = a.counters[0];
+    maxw = a.counters[3];
+  }
+  int32_t lb = a.counters[2], level = a.counters[1];
+  for (;;) {
+    __syncthreads();  // every append of the previous level is done
+    if (threadIdx.x == 0) s_le = tail;
+    __syncthreads();  // frontier end snapshot taken before anyone appends again
+    const int32_t le = s_le;
+    if (le == lb || le - lb > a.narrow_max) break;
+    if (threadIdx.x == 0) {
+      a.level_off[level] = lb;
+      if (le - lb > maxw) maxw = le - lb;
+    }
+    for (int32_t i0 = lb; i0 < le; i0 += blockDim.x) {
+      const int32_t i = i0 + threadIdx.x;
+      kahn_relax_warp(a, i < le ? a.order[i] : -1, level, &tail);
+    }
     lb = le;
     ++level;
   }
-  if (tid == 0) {
-    a.level_off[level] = lb;
+  if (threadIdx.x == 0) {
+    a.counters[0] = tail;
     a.counters[1] = level;
+    a.counters[2] = lb;
+    a.counters[3] = maxw;
+    __threadfence();
   }
-  if (!a.blevel) return;
+}
+
+// Persistent multi-CTA variant (cooperative launch) for wide frontiers.
+__global__ void __launch_bounds__(512) k_kahn_fwd_wide(KahnArgs a) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  int32_t lb = a.counters[2], level = a.counters[1], maxw = a.counters[3];
+  int32_t le = a.counters[0];  // nobody appends before every CTA has read this (no relax yet)
   grid_barrier(a.bar, gridDim.x);
-  for (int32_t L = level - 1; L >= 0; --L) {
-    int32_t b = a.level_off[L], e = a.level_off[L + 1];
-    for (int64_t i = b + tid; i < e; i += nth) {
-      int32_t v = a.order[i];
-      int64_t best = 0;
-      for (int32_t k = a.out_off[v]; k < a.out_off[v + 1]; ++k) {
-        int64_t c = a.blevel[a.out_dst[k]] + a.out_cost[k];
-        best = c > best ? c : best;
-      }
-      a.blevel[v] = best + a.w[v];
+  for (;;) {
+    if (le == lb) break;
+    if (le - lb > maxw) maxw = le - lb;
+    if (tid == 0) a.level_off[level] = lb;
+    for (int64_t i0 = lb + (tid - (tid & 31)); i0 < le; i0 += nth) {
+      const int64_t i = i0 + (tid & 31);
+      kahn_relax_warp(a, i < le ? a.order[i] : -1, level, &a.counters[0]);
+    }
+    grid_barrier(a.bar, gridDim.x, &a.counters[0], &a.counters[4]);
+    lb = le;
+    le = *((volatile int*)&a.counters[4]);
+    ++level;
+  }
+  if (tid == 0) {
+    a.counters[1] = level;
+    a.counters[2] = lb;
+    a.counters[3] = maxw;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_kahn_bwd_narrow(KahnArgs a, int32_t levels) {
+  for (int32_t L = levels - 1; L >= 0; --L) {
+    const int32_t b = a.level_off[L], e = a.level_off[L + 1];
+    for (int32_t i0 = b; i0 < e; i0 += blockDim.x) {
+      const int32_t i = i0 + threadIdx.x;
+      kahn_pull_warp(a, i < e ? a.order[i] : -1);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(512) k_kahn_bwd_wide(KahnArgs a, int32_t levels) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  for (int32_t L = levels - 1; L >= 0; --L) {
+    const int32_t b = a.level_off[L], e = a.level_off[L + 1];
+    for (int64_t i0 = b + (tid - (tid & 31)); i0 < e; i0 += nth) {
+      const int64_t i = i0 + (tid & 31);
+      kahn_pull_warp(a, i < e ? a.order[i] : -1);
     }
     grid_barrier(a.bar, gridDim.x);
   }
@@ -458,7 +592,7 @@ void graph_costs(DevGraph& g, dp_comm_t comm) {
 
 void graph_kahn(DevGraph& g, int64_t* tlevel, int64_t* blevel, int32_t* level_of) {
   dp_ctx* ctx = g.ctx;
-  int32_t n = g.n;
+  const int32_t n = g.n;
   g.order.alloc(ctx, n > 0 ? n : 1);
   g.level_off.alloc(ctx, (size_t)n + 2);
   if (n == 0) {
@@ -468,7 +602,7 @@ void graph_kahn(DevGraph& g, int64_t* tlevel, int64_t* blevel, int32_t* level_of
   }
   DevBuf<int32_t> indeg(ctx, n);
   DP_LAUNCH(ctx, k_indeg, grid_for(n, 256), 256, 0, g.in_off.p, n, indeg.p);
-  DevBuf<int> counters(ctx, 2);
+  DevBuf<int> counters(ctx, 5);
   DevBuf<unsigned> bar(ctx, 2);
   counters.zero();
   bar.zero();
@@ -486,17 +620,44 @@ void graph_kahn(DevGraph& g, int64_t* tlevel, int64_t* blevel, int32_t* level_of
   a.level_of = level_of;
   a.counters = counters.p;
   a.bar = bar.p;
-  const int B = 512;
-  int grid = coop_grid(reinterpret_cast<const void*>(k_kahn), B, n, ctx->num_sms);
-  void* args[] = {&a};
-  DP_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_kahn), grid, B, args, 0, ctx->stream));
-  ++ctx->launches;
-  int host[2];
-  counters.download(host, 2);
+  a.narrow_max = 16384;
+  DP_LAUNCH(ctx, k_kahn_init, grid_for(n, 256), 256, 0, a);
+  DP_LAUNCH(ctx, k_kahn_fwd_narrow, 1, 1024, 0, a);
+  int host[4];
+  counters.download(host, 4);
   sync(ctx);
+  if (host[2] != host[0]) {  // a wide frontier remains: continue with the whole GPU
+    const int B = 512;
+    int grid = coop_grid(reinterpret_cast<const void*>(k_kahn_fwd_wide), B, n, ctx->num_sms);
+    void* args[] = {&a};
+    DP_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_kahn_fwd_wide), grid, B, args, 0,
+                                        ctx->stream));
+    ++ctx->launches;
+    counters.download(host, 4);
+    sync(ctx);
+  }
   g.processed = host[0];
   g.num_levels = host[1];
-  if (g.processed != n) {
+  if (g.processed == n) {
+    int32_t last = n;
+    DP_CUDA(cudaMemcpyAsync(g.level_off.p + g.num_levels, &last, sizeof(int32_t), cudaMemcpyHostToDevice,
+                            ctx->stream));
+    if (blevel) {
+      if (host[3] <= a.narrow_max) {
+        DP_LAUNCH(ctx, k_kahn_bwd_narrow, 1, 1024, 0, a, g.num_levels);
+      } else {
+        bar.zero();
+        const int B = 512;
+        int grid = coop_grid(reinterpret_cast<const void*>(k_kahn_bwd_wide), B, n, ctx->num_sms);
+        int32_t lv = g.num_levels;
+        void* args[] = {&a, &lv};
+        DP_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_kahn_bwd_wide), grid, B, args, 0,
+                                            ctx->stream));
+        ++ctx->launches;
+      }
+    }
+    sync(ctx);
+  } else {
     // keep the residual in-degrees for the witness
     g.level_off.release();
     g.level_off.alloc(ctx, n);

@@ -1,0 +1,932 @@
+// peel_dp.cu — latency-engineered topological peel (ordering.cpp:40-114) and the
+// streaming breakpoint DP (fusion.cpp:126-162) that consumes its output.
+//
+// Peel (one warp).  Per CSR slot the warp loads one 16-byte record
+//   { child, rank(child), row_start(child), out_degree(child) }
+// so a popped stack entry already names its own row and a freed child can be pushed
+// with its row descriptor without another dependent load.  The stack top lives in a
+// shared-memory window (spilled to / refilled from HBM in halves when deep).  While the
+// in-degree decrements of a node's children are in flight, the rows of all children are
+// prefetched into L1, so when the next popped node is a just-freed child its record
+// load is already close.  Dependent HBM/L2 round trips per node: ~2 -> ~1.
+//
+// Streaming DP (second CTA of the same cooperative launch).  The peel publishes its
+// progress (positions emitted); the DP warp follows it in chunks of 256 positions: it
+// stages position data (node, memory prefix, lo[j], out-cost sum, in-edges as source
+// positions) into shared memory with coalesced loads, then runs the register-window
+// recurrence of fusion.cu on shared-memory operands.  Peel and DP overlap, so the
+// sequential part of fuse() costs max(peel, DP) instead of their sum.
+#include <algorithm>
+#include <cstdlib>
+
+#include "fusion.cuh"
+#include "graph.cuh"
+#include "peel.cuh"
+#include "peel_dp.cuh"
+
+namespace dpb {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int kStackCache = 4096;  // stack entries in shared memory (power of 2)
+constexpr int kFreedCap = 2048;
+
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+struct PeelArgs {
+  int32_t n;
+  const int4* slot;     // per CSR slot: child, rank(child), row_start(child), deg(child)
+  int32_t* indeg;       // working in-degrees
+  int4* gstack;         // global stack backing store (n entries), initial sources at [0, nsrc)
+  int32_t nsrc;
+  bool stack_mode;      // false: FIFO (M-TOPO)
+  int32_t* seq;         // node index by position
+  int32_t* pos_of;
+  int* progress;        // positions emitted (published with release semantics)
+  int* emitted;         // final count
+  int64_t* freed_spill; // rank<<32|slot-index spill for huge fan-outs
+  // stack-mode layout (peel_warp_v5)
+  int2* nr2;             // { remaining in-degree, rank | min(out-degree, 255) << 24 }
+  const int32_t* ell;    // padded rows, -1 past the degree
+  int32_t ellw;
+  const int32_t* out_off;
+  const int32_t* out_dst;
+  int2* gstack2;         // { node, min(out-degree, 255) }
+};
+
+// The peel warp.  Shared memory: stack cache (kStackCache int4) + freed buffer.
+__device__ void peel_warp(const PeelArgs& a, int4* sstack, int64_t* sfreed) {
+  const int lane = threadIdx.x & 31;
+  const int32_t SC = kStackCache;
+  // ---------------- stack (stack mode): logical entries [0, top]; [base, top] cached
+  int32_t top = a.nsrc - 1, base = 0;
+  // ---------------- queue (FIFO mode): entries [head, tail) in gstack
+  int32_t head = 0, tail = a.nsrc;
+  if (a.stack_mode) {
+    base = max(0, a.nsrc - SC / 2);
+    for (int32_t i = base + lane; i <= top; i += 32) sstack[i & (SC - 1)] = a.gstack[i];
+  }
+  __syncwarp();
+  int32_t p = 0;
+  for (;;) {
+    int4 e;
+    if (a.stack_mode) {
+      if (top < 0) break;
+      if (top < base) {  // refill the cache from HBM
+        base = max(0, top + 1 - SC / 2);
+        for (int32_t i = base + lane; i <= top; i += 32) sstack[i & (SC - 1)] = a.gstack[i];
+        __syncwarp();
+      }
+      e = sstack[top & (SC - 1)];
+      --top;
+    } else {
+      if (head == tail) break;
+      e = a.gstack[head++];
+    }
+    const int32_t v = e.x, rs = e.y, deg = e.z;
+    if (lane == 0) {
+      a.seq[p] = v;
+      a.pos_of[v] = p;
+    }
+    ++p;
+    if (a.progress && (p & 63) == 0) {
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        st_release(a.progress, p);
+      }
+    }
+    int32_t nf = 0;
+    for (int32_t b0 = 0; b0 < deg; b0 += 32) {
+      const int32_t k = b0 + lane;
+      const bool act = k < deg;
+      int4 s = make_int4(0, 0, 0, 0);
+      if (act) s = a.slot[rs + k];
+      if (act) prefetch_l1(a.slot + s.z);  // child's row, in case it is popped next
+      bool fr = false;
+      if (act) {
+        const int32_t d = a.indeg[s.x] - 1;
+        a.indeg[s.x] = d;
+        fr = d == 0;
+      }
+      const unsigned m = __ballot_sync(FULL, fr);
+      if (deg <= 32) {
+        // fast path: freed children are in registers
+        nf = __popc(m);
+        if (nf == 0) break;
+        if (!a.stack_mode) {
+          // FIFO: append in ascending rank
+          int32_t cnt = 0;
+          for (unsigned mm = m; mm; mm &= mm - 1) {
+            const int32_t rb = __shfl_sync(FULL, s.y, __ffs(mm) - 1);
+            cnt += rb < s.y;
+          }
+          if (fr) a.gstack[tail + cnt] = make_int4(s.x, s.z, s.w, 0);
+          tail += nf;
+          __syncwarp();
+          break;
+        }
+        if (top + nf - base >= SC - 1) {  // spill the lower half of the cache
+          const int32_t half = SC / 2;
+          for (int32_t i = base + lane; i < base + half; i += 32) a.gstack[i] = sstack[i & (SC - 1)];
+          __syncwarp();
+          base += half;
+        }
+        int32_t cnt = 0;  // pushed in descending rank: lowest rank ends on top
+        for (unsigned mm = m; mm; mm &= mm - 1) {
+          const int32_t rb = __shfl_sync(FULL, s.y, __ffs(mm) - 1);
+          cnt += rb > s.y;
+        }
+        if (fr) sstack[(top + 1 + cnt) & (SC - 1)] = make_int4(s.x, s.z, s.w, 0);
+        top += nf;
+        __syncwarp();
+        break;
+      }
+      // general path (rows longer than 32): collect (rank, child entry index) first
+      if (fr) {
+        const int32_t at = nf + __popc(m & ((1u << lane) - 1));
+        const int64_t rec = (static_cast<int64_t>(s.y) << 32) | static_cast<uint32_t>(rs + k);
+        if (at < kFreedCap) sfreed[at] = rec; else a.freed_spill[at - kFreedCap] = rec;
+      }
+      nf += __popc(m);
+    }
+    if (deg > 32 && nf > 0) {
+      __syncwarp();
+      if (a.stack_mode && top + nf - base >= SC - 1) {
+        // make room: flush the whole cache window, keep nothing cached
+        for (int32_t i = base + lane; i <= top; i += 32) a.gstack[i] = sstack[i & (SC - 1)];
+        __syncwarp();
+        base = top + 1;
+      }
+      const bool big = a.stack_mode && (nf >= SC - 1);
+      for (int32_t i = lane; i < nf; i += 32) {
+        const int64_t ri = i < kFreedCap ? sfreed[i] : a.freed_spill[i - kFreedCap];
+        const int32_t rk = static_cast<int32_t>(ri >> 32);
+        int32_t cnt = 0;
+        for (int32_t j = 0; j < nf; ++j) {
+          const int64_t rj = j < kFreedCap ? sfreed[j] : a.freed_spill[j - kFreedCap];
+          const int32_t r2 = static_cast<int32_t>(rj >> 32);
+          cnt += a.stack_mode ? (r2 > rk) : (r2 < rk);
+        }
+        const int4 s = a.slot[static_cast<int32_t>(ri & 0xffffffff)];
+        const int4 ent = make_int4(s.x, s.z, s.w, 0);
+        if (!a.stack_mode) a.gstack[tail + cnt] = ent;
+        else if (big) a.gstack[top + 1 + cnt] = ent;
+        else sstack[(top + 1 + cnt) & (SC - 1)] = ent;
+      }
+      if (!a.stack_mode) {
+        tail += nf;
+      } else {
+        top += nf;
+        if (big) base = top + 1;  // everything lives in HBM; the next pop refills
+      }
+      __syncwarp();
+    }
+  }
+  if (lane == 0) {
+    *a.emitted = p;
+    if (a.progress) {
+      __threadfence();
+      st_release(a.progress, p);
+    }
+  }
+}
+
+// Stack-mode peel (DFS/CPD), lean version.  Data (peel_prepare):
+//   nr2[v] = { remaining in-degree, rank | min(deg,255) << 24 }   8 B / node
+//   ell[v] = first EW children, -1 padded (address = v * EW)    4*EW B / node
+// Stack entries are {node, deg}.  While lane k's nr2[c_k] is in flight the lane also
+// loads ell[c_k]; the warp loads the stack top's row.  After the freed decision the row
+// of whichever node is popped next (min-rank freed child, or the old top) is kept in
+// shared memory, so each node costs one dependent L2 round trip.  The emitted sequence
+// is buffered and stored 32 ids at a time; pos_of is scattered by the consumer.
+template <int EW>
+__device__ void peel_warp_v5(const PeelArgs& a, int2* sstack, int64_t* sfreed, int32_t* srow, int32_t* stop,
+                             int32_t* seqbuf) {
+  const int lane = threadIdx.x & 31;
+  const int32_t SC = 2 * kStackCache;
+  int32_t top = a.nsrc - 1;
+  int32_t base = max(0, a.nsrc - SC / 2);
+  for (int32_t i = base + lane; i <= top; i += 32) sstack[i & (SC - 1)] = a.gstack2[i];
+  __syncwarp();
+  int32_t p = 0;
+  int32_t exp_idx = -1;
+  int exp_src = 0;
+  while (top >= 0) {
+    if (top < base) {
+      base = max(0, top + 1 - SC / 2);
+      for (int32_t i = base + lane; i <= top; i += 32) sstack[i & (SC - 1)] = a.gstack2[i];
+      __syncwarp();
+    }
+    const int32_t my_idx = top;
+    const int2 e = sstack[top & (SC - 1)];
+    --top;
+    const int32_t v = e.x, deg = e.y;
+    if (lane == 0) seqbuf[p & 31] = v;
+    ++p;
+    if ((p & 31) == 0) {
+      __syncwarp();
+      a.seq[p - 32 + lane] = seqbuf[lane];
+      if (a.progress && lane == 0) {
+        __threadfence();
+        st_release(a.progress, p);
+      }
+    }
+    if (deg > EW) {
+      // ---- long row (CSR), children's rows not prefetched
+      const int32_t rs = a.out_off[v], dg = a.out_off[v + 1] - rs;
+      int32_t nf = 0;
+      for (int32_t b0 = 0; b0 < dg; b0 += 32) {
+        const int32_t k = b0 + lane;
+        const bool act = k < dg;
+        int32_t c = 0;
+        int2 r2 = make_int2(1, 0);
+        if (act) {
+          c = a.out_dst[rs + k];
+          r2 = a.nr2[c];
+        }
+        bool fr = false;
+        if (act) {
+          const int32_t d = r2.x - 1;
+          a.nr2[c].x = d;
+          fr = d == 0;
+        }
+        const unsigned m = __ballot_sync(FULL, fr);
+        if (fr) {
+          const int32_t at = nf + __popc(m & ((1u << lane) - 1));
+          const int64_t r = (static_cast<int64_t>(r2.y) << 32) | static_cast<uint32_t>(c);
+          if (at < kFreedCap) sfreed[at] = r; else a.freed_spill[at - kFreedCap] = r;
+        }
+        nf += __popc(m);
+      }
+      __syncwarp();
+      if (nf > 0) {
+        if (top + nf - base >= SC - 1) {
+          for (int32_t i = base + lane; i <= top; i += 32) a.gstack2[i] = sstack[i & (SC - 1)];
+          __syncwarp();
+          base = top + 1;
+        }
+        const bool big = nf >= SC - 1;
+        for (int32_t i = lane; i < nf; i += 32) {
+          const int64_t ri = i < kFreedCap ? sfreed[i] : a.freed_spill[i - kFreedCap];
+          const int32_t rk = static_cast<int32_t>(ri >> 32) & 0xffffff;
+          int32_t cnt = 0;
+          for (int32_t j = 0; j < nf; ++j) {
+            const int64_t rj = j < kFreedCap ? sfreed[j] : a.freed_spill[j - kFreedCap];
+            cnt += (static_cast<int32_t>(rj >> 32) & 0xffffff) > rk;
+          }
+          const int2 ent = make_int2(static_cast<int32_t>(ri & 0xffffffff),
+                                     static_cast<int32_t>(static_cast<uint32_t>(ri >> 32) >> 24));
+          if (big) a.gstack2[top + 1 + cnt] = ent; else sstack[(top + 1 + cnt) & (SC - 1)] = ent;
+        }
+        top += nf;
+        if (big) base = top + 1;
+        __syncwarp();
+      }
+      exp_idx = -1;
+      continue;
+    }
+    const int src = (my_idx == exp_idx) ? exp_src : 0;
+    int32_t c = -1;
+    if (lane < EW) c = src == 1 ? srow[lane] : (src == 2 ? stop[lane] : a.ell[static_cast<int64_t>(v) * EW + lane]);
+    const bool act = c >= 0;
+    int2 r2 = make_int2(1, 0);
+    int4 crow[EW / 4];
+    if (act) {
+      r2 = a.nr2[c];
+      const int4* rp = reinterpret_cast<const int4*>(a.ell + static_cast<int64_t>(c) * EW);
+#pragma unroll
+      for (int q = 0; q < EW / 4; ++q) crow[q] = rp[q];
+    }
+    const bool have_top = top >= base;
+    int32_t trow = -1;
+    if (have_top && lane < EW) {
+      const int2 te = sstack[top & (SC - 1)];
+      if (te.y <= EW) trow = a.ell[static_cast<int64_t>(te.x) * EW + lane];
+    }
+    bool fr = false;
+    if (act) {
+      const int32_t d = r2.x - 1;
+      a.nr2[c].x = d;
+      fr = d == 0;
+    }
+    const unsigned m = __ballot_sync(FULL, fr);
+    if (m == 0) {
+      if (have_top && lane < EW) stop[lane] = trow;
+      exp_idx = have_top ? top : -1;
+      exp_src = 2;
+      __syncwarp();
+      continue;
+    }
+    const int nf = __popc(m);
+    if (top + nf - base >= SC - 1) {
+      const int32_t half = SC / 2;
+      for (int32_t i = base + lane; i < base + half; i += 32) a.gstack2[i] = sstack[i & (SC - 1)];
+      __syncwarp();
+      base += half;
+    }
+    const int32_t rk = r2.y & 0xffffff;
+    int32_t cnt = 0;  // pushed in descending rank: the lowest rank ends on top
+    if (nf > 1) {
+      for (unsigned mm = m; mm; mm &= mm - 1) {
+        const int32_t rb = __shfl_sync(FULL, rk, __ffs(mm) - 1);
+        cnt += rb > rk;
+      }
+    }
+    if (fr) {
+      sstack[(top + 1 + cnt) & (SC - 1)] = make_int2(c, static_cast<int32_t>(static_cast<uint32_t>(r2.y) >> 24));
+      if (cnt == nf - 1) {
+        int4* dst = reinterpret_cast<int4*>(srow);
+#pragma unroll
+        for (int q = 0; q < EW / 4; ++q) dst[q] = crow[q];
+      }
+    }
+    top += nf;
+    exp_idx = top;
+    exp_src = 1;
+    __syncwarp();
+  }
+  __syncwarp();
+  if (lane < (p & 31)) a.seq[(p & ~31) + lane] = seqbuf[lane];
+  __syncwarp();
+  if (lane == 0) {
+    *a.emitted = p;
+    if (a.progress) {
+      __threadfence();
+      st_release(a.progress, p);
+    }
+  }
+}
+
+__device__ __forceinline__ void peel_dispatch(const PeelArgs& a, int4* smem4) {
+  int64_t* sfreed = reinterpret_cast<int64_t*>(smem4 + kStackCache);
+  int32_t* srow = reinterpret_cast<int32_t*>(sfreed + kFreedCap);
+  int32_t* stop = srow + 32;
+  int32_t* seqbuf = stop + 32;
+  if (!a.stack_mode) peel_warp(a, smem4, sfreed);
+  else if (a.ellw == 8) peel_warp_v5<8>(a, reinterpret_cast<int2*>(smem4), sfreed, srow, stop, seqbuf);
+  else peel_warp_v5<32>(a, reinterpret_cast<int2*>(smem4), sfreed, srow, stop, seqbuf);
+}
+
+__global__ void __launch_bounds__(32) k_peel2(PeelArgs a) {
+  extern __shared__ int4 smem4[];
+  peel_dispatch(a, smem4);
+}
+
+// ---------------------------------------------------------------- streaming DP
+constexpr int kCh = 256;      // positions per staged chunk
+constexpr int kInCap = 2048;  // staged in-edges per chunk
+constexpr int kRing = 1024;   // memory-prefix ring (>= R + kCh + 2)
+
+struct DpArgs {
+  int32_t n, range;
+  int64_t limit;
+  const int32_t* seq;
+  int32_t* pos_of;
+  const int64_t* mem;
+  const int64_t* out_sum;   // by node index
+  const int32_t* in_off;    // CSC
+  const int32_t* in_src;
+  const int64_t* in_cost;
+  const int* progress;
+  int32_t* prev_cut;        // [n+1]
+  int* first_exceed;
+  bool keys32;              // window values fit 32-bit keys (see peel_dp_stream)
+  long long* debug;         // optional: [total, waiting, staging] cycles of the DP warp
+};
+
+__device__ __forceinline__ void argmin_reduce(int64_t& v, int32_t& d) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const int64_t ov = __shfl_xor_sync(FULL, v, o);
+    const int32_t od = __shfl_xor_sync(FULL, d, o);
+    if (ov < v || (ov == v && od < d)) {
+      v = ov;
+      d = od;
+    }
+  }
+}
+
+struct DpSmem {
+  int32_t lo[kCh];
+  int64_t out[kCh];
+  int32_t off[kCh + 1];
+  int32_t ipos[kInCap];
+  int64_t ic[kInCap];
+  int64_t pref[kRing];
+  int32_t node[kCh];
+  int32_t ioff[kCh];
+};
+
+__device__ void dp_warp(const DpArgs& a, DpSmem& S) {
+  constexpr int SPL = 8, W = 256;
+  const int lane = threadIdx.x & 31;
+  const int32_t n = a.n;
+  int64_t D[SPL];
+#pragma unroll
+  for (int r = 0; r < SPL; ++r) D[r] = 0;
+  constexpr int32_t kUnfilled = 0x3f000000;
+  int32_t K[SPL];
+#pragma unroll
+  for (int r = 0; r < SPL; ++r) K[r] = kUnfilled;
+  int64_t off = 0;     // D = (K >> 8) + off
+  int32_t bvr = 0;     // best of the last query, relative to off
+  int64_t carry = 0;  // prefix[j0]
+  long long wait_cycles = 0, stage_cycles = 0;
+  const long long t_start = clock64();
+  if (lane == 0) S.pref[0] = 0;
+  int avail = 0;
+  for (int32_t j0 = 0; j0 < n; j0 += kCh) {
+    // positions [j0, j1] staged; steps j in [max(1,j0), j1+1] use them
+    const int32_t j1 = min(n - 1, j0 + kCh - 1);
+    const int32_t cnt = j1 - j0 + 1;
+    const long long tw0 = clock64();
+    while (avail < j1 + 1) {
+      avail = ld_acquire(a.progress);
+      if (avail < j1 + 1) __nanosleep(200);
+    }
+    wait_cycles += clock64() - tw0;
+    // node, memory, out-cost, in-degree per position
+    int32_t my_in = 0;
+    for (int32_t t = lane; t < kCh; t += 32) {
+      if (t < cnt) {
+        const int32_t v = a.seq[j0 + t];
+        S.node[t] = v;
+        S.out[t] = a.out_sum[v];
+        a.pos_of[v] = j0 + t;  // the peel does not write pos_of; in-edge sources read it below
+      }
+    }
+    __syncwarp();
+    __threadfence_block();
+    // memory prefix (warp scan in 32-wide pieces) + exceed check
+    for (int32_t t0 = 0; t0 < cnt; t0 += 32) {
+      const int32_t t = t0 + lane;
+      int64_t mv = t < cnt ? a.mem[S.node[t]] : 0;
+      if (t < cnt && mv > a.limit) atomicMin(a.first_exceed, j0 + t);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t x = __shfl_up_sync(FULL, mv, o);
+        if (lane >= o) mv += x;
+      }
+      if (t < cnt) S.pref[(j0 + t + 1) & (kRing - 1)] = carry + mv;
+      carry += __shfl_sync(FULL, mv, 31);
+    }
+    // in-edge offsets (per position) and each row's CSC start
+    for (int32_t t0 = 0; t0 < kCh; t0 += 32) {
+      const int32_t t = t0 + lane;
+      int32_t c = 0;
+      if (t < cnt) {
+        const int32_t v = S.node[t];
+        const int32_t b = a.in_off[v];
+        S.ioff[t] = b;
+        c = a.in_off[v + 1] - b;
+      }
+      int32_t x = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+      }
+      if (t < kCh) S.off[t + 1] = my_in + x;
+      my_in += __shfl_sync(FULL, x, 31);
+    }
+    if (lane == 0) S.off[0] = 0;
+    __syncwarp();
+    const bool staged = my_in <= kInCap;
+    if (staged) {
+      // flattened over the chunk's in-edges, 4 independent gathers in flight per lane
+      for (int32_t o0 = 0; o0 < my_in; o0 += 128) {
+        int32_t src[4], oo[4];
+        int64_t cc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int32_t o = o0 + u * 32 + lane;
+          oo[u] = o;
+          src[u] = 0;
+          cc[u] = 0;
+          if (o < my_in) {
+            int32_t lo = 0, hi = cnt - 1;  // last t with off[t] <= o
+            while (lo < hi) {
+              const int32_t mid = (lo + hi + 1) >> 1;
+              if (S.off[mid] <= o) lo = mid; else hi = mid - 1;
+            }
+            const int32_t k = S.ioff[lo] + (o - S.off[lo]);
+            src[u] = a.in_src[k];
+            cc[u] = a.in_cost[k];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (oo[u] < my_in) {
+            S.ipos[oo[u]] = a.pos_of[src[u]];
+            S.ic[oo[u]] = cc[u];
+          }
+        }
+      }
+    }
+    __syncwarp();
+    // lo[j] for the steps of this chunk that produce best[j]: j = j0+t+1?  Steps use
+    // lo[j] with j in [j0+1, j1+1] -> prefix indices up to j1+1 (staged above).
+    for (int32_t t = lane; t < cnt; t += 32) {
+      const int32_t j = j0 + t + 1;
+      int32_t lo = j > a.range ? j - a.range : 0, hi = j - 1;
+      const int64_t pj = S.pref[j & (kRing - 1)];
+      while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (pj - S.pref[mid & (kRing - 1)] <= a.limit) hi = mid; else lo = mid + 1;
+      }
+      S.lo[t] = lo;
+    }
+    __syncwarp();
+    stage_cycles += clock64() - tw0;
+    if (a.keys32) {
+      // ---- 32-bit keys: K = (D - OFFSET) * 256 + distance; argmin = one redux.sync
+      if (j0 == 0) {
+        off = S.out[0];  // candidate 0: D_1(0) = out(0)
+        if (lane == 0) K[0] = 0;
+      }
+      for (int32_t t = 0; t < cnt; ++t) {
+        const int32_t p = j0 + t;
+        if (p > 0) {
+          // transition into position p: distances +1, candidate p enters, in-edges of p
+#pragma unroll
+          for (int r = 0; r < SPL; ++r) K[r] += 1;
+          const int32_t sl = p & (W - 1);
+#pragma unroll
+          for (int r = 0; r < SPL; ++r)
+            if (lane * SPL + r == sl) K[r] = bvr * 256;
+          const int32_t kb = S.off[t], ke = S.off[t + 1];
+          for (int32_t k = kb; k < ke; ++k) {
+            int32_t av;
+            int64_t cv;
+            if (staged) {
+              av = S.ipos[k];
+              cv = S.ic[k];
+            } else {
+              av = a.pos_of[a.in_src[S.ioff[t] - kb + k]];
+              cv = a.in_cost[S.ioff[t] - kb + k];
+            }
+            if (av <= p - W) continue;  // source outside the window: no candidate moves
+            const int32_t thr = p - av;  // candidates i <= av  <=>  distance >= p - av
+            const int32_t sub = static_cast<int32_t>(cv) << 8;
+#pragma unroll
+            for (int r = 0; r < SPL; ++r)
+              if ((K[r] & 255) >= thr) K[r] -= sub;
+          }
+          off += S.out[t];
+        }
+        // best[p+1]
+        const int32_t maxd = p - S.lo[t];
+        int32_t mk = INT32_MAX;
+#pragma unroll
+        for (int r = 0; r < SPL; ++r)
+          if ((K[r] & 255) <= maxd && K[r] < mk) mk = K[r];
+        mk = __reduce_min_sync(FULL, mk);
+        bvr = mk >> 8;
+        if (lane == 0) a.prev_cut[p + 1] = p - (mk & 255);
+        if (bvr > (1 << 20) || bvr < -(1 << 20)) {  // rebase the relative values
+#pragma unroll
+          for (int r = 0; r < SPL; ++r)
+            if (K[r] < kUnfilled) K[r] -= bvr * 256;
+          off += bvr;
+          bvr = 0;
+        }
+      }
+      __syncwarp();
+      continue;
+    }
+    if (j0 == 0 && lane == 0) D[0] = S.out[0];  // candidate i = 0 for j = 1
+    // steps: for position p = j0+t, first compute best[j] for j = p+1?  Layout: the
+    // transition after best[p] uses position p's out-sum and in-edges; best[p+1] uses lo.
+    for (int32_t t = 0; t < cnt; ++t) {
+      const int32_t p = j0 + t;
+      if (p > 0) {
+        // transition from step p to p+1: position p enters (out-sum, in-edges)
+        const int64_t o = S.out[t];
+#pragma unroll
+        for (int r = 0; r < SPL; ++r) D[r] += o;
+        const int32_t kb = S.off[t], ke = S.off[t + 1];
+        const int32_t gkb = S.ioff[t] - kb;
+        for (int32_t base = kb; base < ke; base += 32) {
+          int32_t av = -1;
+          int64_t cv = 0;
+          if (base + lane < ke) {
+            if (staged) {
+              av = S.ipos[base + lane];
+              cv = S.ic[base + lane];
+            } else {
+              av = a.pos_of[a.in_src[gkb + base + lane]];
+              cv = a.in_cost[gkb + base + lane];
+            }
+          }
+          const int c = min(32, ke - base);
+          for (int q = 0; q < c; ++q) {
+            const int32_t at = __shfl_sync(FULL, av, q);
+            const int64_t ct = __shfl_sync(FULL, cv, q);
+            if (at <= p - W) continue;
+#pragma unroll
+            for (int r = 0; r < SPL; ++r) {
+              const int32_t s = lane * SPL + r;
+              const int32_t i2 = p - ((p - s) & (W - 1));
+              if (i2 <= at) D[r] -= ct;
+            }
+          }
+        }
+        // new candidate i = p: best[p] + out(p) — best[p] was broadcast as `bestp`
+      }
+      // best[p+1]
+      const int32_t j = p + 1;
+      const int32_t loj = S.lo[t];
+      int64_t bv = INT64_MAX;
+      int32_t bd = INT32_MAX;
+#pragma unroll
+      for (int r = 0; r < SPL; ++r) {
+        const int32_t s = lane * SPL + r;
+        const int32_t d = (j - 1 - s) & (W - 1);
+        if (j - 1 - d >= loj && (D[r] < bv || (D[r] == bv && d < bd))) {
+          bv = D[r];
+          bd = d;
+        }
+      }
+      argmin_reduce(bv, bd);
+      if (lane == 0) a.prev_cut[j] = j - 1 - bd;
+      // candidate i = j enters with best[j] + out(j); out(j) is added at the next
+      // transition, so store best[j] now
+      if (j < n) {
+        const int32_t sl = j & (W - 1);
+#pragma unroll
+        for (int r = 0; r < SPL; ++r)
+          if (lane * SPL + r == sl) D[r] = bv;
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && a.debug) {
+    a.debug[0] = clock64() - t_start;
+    a.debug[1] = wait_cycles;
+    a.debug[2] = stage_cycles - wait_cycles;
+  }
+}
+
+
+__global__ void __launch_bounds__(32) k_peel_dp(PeelArgs pa, DpArgs da) {
+  extern __shared__ int4 smem4[];
+  if (blockIdx.x == 0) {
+    peel_dispatch(pa, smem4);
+  } else {
+    dp_warp(da, *reinterpret_cast<DpSmem*>(smem4));
+  }
+}
+
+__global__ void k_slot16(const int32_t* out_off, const int32_t* out_dst, const int32_t* rank, int32_t m, int4* slot) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = out_dst[k];
+    slot[k] = make_int4(c, rank[c], out_off[c], out_off[c + 1] - out_off[c]);
+  }
+}
+
+__global__ void k_rank_keys2(const int64_t* cpath, const int32_t* by_id, int32_t n, uint64_t* keys, int32_t* vals) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = by_id[i];
+    keys[i] = ~(static_cast<uint64_t>(cpath[v]) ^ (1ull << 63));
+    vals[i] = v;
+  }
+}
+
+__global__ void k_rank_of2(const int32_t* by_rank, int32_t n, int32_t* rank) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    rank[by_rank[r]] = static_cast<int32_t>(r);
+}
+
+__global__ void k_src_flags2(const int32_t* by_rank, const int32_t* in_off, int32_t n, int32_t* flag) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = by_rank[r];
+    flag[r] = (in_off[v + 1] - in_off[v]) == 0 ? 1 : 0;
+  }
+}
+
+__global__ void k_src_place2(const int32_t* by_rank, const int32_t* flag, const int32_t* pos, const int32_t* out_off,
+                             int32_t n, int32_t nsrc, bool stack, int4* buf) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    if (!flag[r]) continue;
+    const int32_t v = by_rank[r], p = pos[r];
+    buf[stack ? nsrc - 1 - p : p] = make_int4(v, out_off[v], out_off[v + 1] - out_off[v], 0);
+  }
+}
+
+__global__ void k_node_rec2(const int32_t* in_off, const int32_t* out_off, const int32_t* rank, int32_t n, int2* nr2) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t deg = min(out_off[v + 1] - out_off[v], 255);
+    nr2[v] = make_int2(in_off[v + 1] - in_off[v], rank[v] | (deg << 24));
+  }
+}
+
+__global__ void k_ell(const int32_t* out_off, const int32_t* out_dst, int32_t n, int ew, int32_t* ell) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)n * ew; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = i / ew;
+    const int32_t q = static_cast<int32_t>(i - v * ew);
+    const int32_t b = out_off[v], d = out_off[v + 1] - b;
+    ell[i] = (q < d && d <= ew) ? out_dst[b + q] : -1;
+  }
+}
+
+__global__ void k_src_place_v5(const int32_t* by_rank, const int32_t* flag, const int32_t* pos, const int32_t* out_off,
+                               int32_t n, int32_t nsrc, int2* buf) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    if (!flag[r]) continue;
+    const int32_t v = by_rank[r], p = pos[r];
+    buf[nsrc - 1 - p] = make_int2(v, min(out_off[v + 1] - out_off[v], 255));
+  }
+}
+
+__global__ void k_scatter_pos_of(const int32_t* seq, int32_t n, int32_t* pos_of) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
+    pos_of[seq[p]] = static_cast<int32_t>(p);
+}
+
+__global__ void k_indeg_init2(const int32_t* in_off, int32_t n, int32_t* indeg) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+    indeg[v] = in_off[v + 1] - in_off[v];
+}
+
+__global__ void k_max_abs(const int64_t* x, int32_t n, unsigned long long* out) {
+  unsigned long long m = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = x[i] < 0 ? -x[i] : x[i];
+    m = static_cast<unsigned long long>(v) > m ? static_cast<unsigned long long>(v) : m;
+  }
+  atomicMax(out, m);
+}
+
+__global__ void k_out_sum(const int32_t* out_off, const int64_t* out_cost, int32_t n, int64_t* out_sum) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    int64_t s = 0;
+    for (int32_t k = out_off[v]; k < out_off[v + 1]; ++k) s += out_cost[k];
+    out_sum[v] = s;
+  }
+}
+
+size_t peel_smem() { return sizeof(int4) * kStackCache + sizeof(int64_t) * kFreedCap + sizeof(int32_t) * 96; }
+
+}  // namespace
+
+// Builds the peel inputs (ranks, 16-byte slot records, initial stack, in-degrees).
+void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st) {
+  dp_ctx* ctx = g.ctx;
+  const int B = 256;
+  const int32_t n = g.n, m = g.m_ok;
+  DevBuf<int32_t> by_id;
+  node_order_by_id(g, by_id);
+  DevBuf<int32_t> by_rank(ctx, n), rank(ctx, n);
+  if (policy == DP_TOPO_CPD) {
+    DevBuf<uint64_t> keys(ctx, n), keys_out(ctx, n);
+    DevBuf<int32_t> vals(ctx, n);
+    DP_LAUNCH(ctx, k_rank_keys2, grid_for(n, B), B, 0, cpath, by_id.p, n, keys.p, vals.p);
+    sort_pairs_u64(ctx, keys.p, keys_out.p, vals.p, by_rank.p, n, 0, 64);
+  } else {
+    DP_CUDA(cudaMemcpyAsync(by_rank.p, by_id.p, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  DP_LAUNCH(ctx, k_rank_of2, grid_for(n, B), B, 0, by_rank.p, n, rank.p);
+  DevBuf<int32_t> flag(ctx, (size_t)n + 1), fpos(ctx, (size_t)n + 1);
+  flag.zero();
+  DP_LAUNCH(ctx, k_src_flags2, grid_for(n, B), B, 0, by_rank.p, g.in_off.p, n, flag.p);
+  exclusive_scan_i32(ctx, flag.p, fpos.p, (int64_t)n + 1);
+  st.nsrc = scalar_to_host(ctx, fpos.p + n);
+  st.stack_mode = policy != DP_TOPO_M;
+  st.gstack.alloc(ctx, (size_t)n + 1);
+  if (st.stack_mode && n < (1 << 24)) {
+    st.ellw = n > 262144 ? 8 : 32;
+    st.nr2.alloc(ctx, n);
+    DP_LAUNCH(ctx, k_node_rec2, grid_for(n, B), B, 0, g.in_off.p, g.out_off.p, rank.p, n, st.nr2.p);
+    st.ell.alloc(ctx, (size_t)n * st.ellw);
+    DP_LAUNCH(ctx, k_ell, grid_for((int64_t)n * st.ellw, B), B, 0, g.out_off.p, g.out_dst.p, n, st.ellw, st.ell.p);
+    st.gstack2.alloc(ctx, (size_t)n + 1);
+    DP_LAUNCH(ctx, k_src_place_v5, grid_for(n, B), B, 0, by_rank.p, flag.p, fpos.p, g.out_off.p, n, st.nsrc,
+              st.gstack2.p);
+  } else {
+    if (st.stack_mode) fail(DP_E_UNSUPPORTED, "graphs with 2^24 or more nodes are not supported by the peel");
+    DP_LAUNCH(ctx, k_src_place2, grid_for(n, B), B, 0, by_rank.p, flag.p, fpos.p, g.out_off.p, n, st.nsrc,
+              st.stack_mode, st.gstack.p);
+    st.indeg.alloc(ctx, n);
+    DP_LAUNCH(ctx, k_indeg_init2, grid_for(n, B), B, 0, g.in_off.p, n, st.indeg.p);
+    st.slot.alloc(ctx, m > 0 ? m : 1);
+    DP_LAUNCH(ctx, k_slot16, grid_for(m, B), B, 0, g.out_off.p, g.out_dst.p, rank.p, m, st.slot.p);
+  }
+  st.spill.alloc(ctx, m > 0 ? m : 1);
+  st.counters.alloc(ctx, 3);
+  st.counters.zero();
+}
+
+static PeelArgs peel_args(DevGraph& g, PeelState& st, int32_t* seq, int32_t* pos_of, bool progress) {
+  PeelArgs a{};
+  a.n = g.n;
+  a.slot = st.slot.p;
+  a.indeg = st.indeg.p;
+  a.gstack = st.gstack.p;
+  a.nsrc = st.nsrc;
+  a.stack_mode = st.stack_mode;
+  a.seq = seq;
+  a.pos_of = pos_of;
+  a.progress = progress ? st.counters.p : nullptr;
+  a.emitted = st.counters.p + 1;
+  a.freed_spill = st.spill.p;
+  a.nr2 = st.nr2.p;
+  a.ell = st.ell.p;
+  a.ellw = st.ellw;
+  a.out_off = g.out_off.p;
+  a.out_dst = g.out_dst.p;
+  a.gstack2 = st.gstack2.p;
+  return a;
+}
+
+int32_t topo_order(DevGraph& g, int policy, const int64_t* cpath, int32_t* seq, int32_t* pos_of) {
+  dp_ctx* ctx = g.ctx;
+  if (g.n == 0) return 0;
+  PeelState st;
+  peel_prepare(g, policy, cpath, st);
+  PeelArgs a = peel_args(g, st, seq, pos_of, false);
+  const size_t sm = peel_smem();
+  static bool attr = false;
+  if (!attr) {
+    DP_CUDA(cudaFuncSetAttribute(k_peel2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    attr = true;
+  }
+  {
+    StageScope s(ctx, policy == DP_TOPO_CPD ? "cpd_peel" : "peel", 0.0);
+    DP_LAUNCH(ctx, k_peel2, 1, 32, sm, a);
+  }
+  const int32_t emitted = scalar_to_host(ctx, st.counters.p + 1);
+  if (st.stack_mode && emitted == g.n)
+    DP_LAUNCH(ctx, k_scatter_pos_of, grid_for(g.n, 256), 256, 0, seq, g.n, pos_of);
+  return emitted;
+}
+
+int32_t peel_dp_stream(DevGraph& g, const int64_t* cpath, int32_t range, int64_t limit, int32_t* seq, int32_t* pos_of,
+                       int32_t* prev_cut, int* first_exceed) {
+  dp_ctx* ctx = g.ctx;
+  const int32_t n = g.n;
+  if (n == 0) return 0;
+  PeelState st;
+  peel_prepare(g, DP_TOPO_CPD, cpath, st);
+  PeelArgs pa = peel_args(g, st, seq, pos_of, true);
+  DevBuf<int64_t> out_sum(ctx, n);
+  DP_LAUNCH(ctx, k_out_sum, grid_for(n, 256), 256, 0, g.out_off.p, g.out_cost.p, n, out_sum.p);
+  // 32-bit keys need every window value within +-2^22 of the window minimum: bounded
+  // by R x (largest out-cost sum of a position) + largest single cost.
+  DevBuf<unsigned long long> mx(ctx, 1);
+  mx.zero();
+  DP_LAUNCH(ctx, k_max_abs, grid_for(n, 256), 256, 0, out_sum.p, n, mx.p);
+  DP_LAUNCH(ctx, k_max_abs, grid_for(g.m_ok, 256), 256, 0, g.out_cost.p, g.m_ok, mx.p);
+  const unsigned long long max_out = scalar_to_host(ctx, mx.p);
+  DpArgs da{};
+  da.keys32 = static_cast<double>(max_out) * (range + 2) < static_cast<double>(1 << 21);
+  da.n = n;
+  da.range = range;
+  da.limit = limit;
+  da.seq = seq;
+  da.pos_of = pos_of;
+  da.mem = g.mem.p;
+  da.out_sum = out_sum.p;
+  da.in_off = g.in_off.p;
+  da.in_src = g.in_src.p;
+  da.in_cost = g.in_cost.p;
+  da.progress = st.counters.p;
+  da.prev_cut = prev_cut;
+  da.first_exceed = first_exceed;
+  const size_t sm = std::max(peel_smem(), sizeof(DpSmem));
+  static bool attr = false;
+  if (!attr) {
+    DP_CUDA(cudaFuncSetAttribute(k_peel_dp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    attr = true;
+  }
+  DevBuf<long long> dbg(ctx, 4);
+  dbg.zero();
+  da.debug = getenv("DP_DEBUG_DP") ? dbg.p : nullptr;
+  void* args[] = {&pa, &da};
+  {
+    StageScope s(ctx, "peel+dp (streamed)", 0.0);
+    DP_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_peel_dp), 2, 32, args, sm, ctx->stream));
+    ++ctx->launches;
+  }
+  if (da.debug) {
+    long long h[3];
+    dbg.download(h, 3);
+    sync(ctx);
+    fprintf(stderr, "[peel_dp] dp warp: total %.1f ms, waiting %.1f ms, staging %.1f ms (at 1.965 GHz)\n",
+            h[0] / 1.965e6, h[1] / 1.965e6, h[2] / 1.965e6);
+  }
+  return scalar_to_host(ctx, st.counters.p + 1);
+}
+
+}  // namespace dpb

@@ -1,0 +1,27 @@
+// peel_dp.cuh — latency-engineered peel and the streamed breakpoint DP.
+#pragma once
+#include "graph.cuh"
+
+namespace dpb {
+
+struct PeelState {
+  int32_t nsrc = 0;
+  bool stack_mode = true;
+  DevBuf<int4> gstack, slot;
+  DevBuf<int2> nr2, gstack2;
+  DevBuf<int32_t> ell;
+  int32_t ellw = 8;
+  DevBuf<int32_t> indeg;
+  DevBuf<int64_t> spill;
+  DevBuf<int> counters;  // [0] progress, [1] emitted
+};
+
+void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st);
+
+// CPD peel of g streamed into the breakpoint DP (R <= 256); writes seq/pos_of and
+// prev_cut[1..n]; *first_exceed = first position whose node exceeds `limit` (or
+// INT_MAX).  Returns the number of emitted nodes.
+int32_t peel_dp_stream(DevGraph& g, const int64_t* cpath, int32_t range, int64_t limit, int32_t* seq, int32_t* pos_of,
+                       int32_t* prev_cut, int* first_exceed);
+
+}  // namespace dpb

@@ -223,7 +223,6 @@ int dp_pipeline(dp_ctx_t* ctx, const dp_graph_t* h, const dp_devices_t* devices,
     free_sim(so);
     free_sim(sa);
   }
-  if (ctx->timing) stage_resolve(ctx);
   *out = res;
   DP_API_END
 }
@@ -249,7 +248,6 @@ int dp_resident_create(dp_ctx_t* ctx, const dp_graph_t* h, const dp_devices_t* d
 int dp_resident_generate(dp_resident_t* r) {
   DP_API_BEGIN(r ? r->ctx : nullptr)
   resident_generate(*r, false);
-  if (r->ctx->timing) stage_resolve(r->ctx);
   DP_API_END
 }
 
