@@ -160,3 +160,17 @@ def test_candidates(gpu, oracle):
 def test_pipeline_medium(gpu, oracle):
     g = layered(77, 20000, 64)
     parity.check_pipeline(gpu, oracle, g, "layered20k", d=8)
+
+
+def test_reference_suite_against_dropin():
+    """The reference's own doctest suite (/root/reference/proj/tests, 99 cases) compiled
+    unchanged against the C++ drop-in (paper_2208_00184_b200/host/dagplace_core.cpp ->
+    libdagplace_b200.so) and run on the GPU."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "build", "ref_tests_b200")
+    if not os.path.exists(exe):
+        pytest.skip("build/ref_tests_b200 not built (needs the reference headers at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-4000:]
+    assert "| 0 failed" in out.stdout

@@ -1,0 +1,68 @@
+"""N>1 path on CPU: world_size-2 gloo process group running the candidate sharding and
+the single MIN all-reduce of bench.py / paper_2208_00184_b200.shard; the makespans come
+from the oracle restatement (CPU) so the test runs without a GPU, and the result must
+equal the single-process first strict minimum (simulator.cpp:292-294)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, makespans, out):
+    import torch.distributed as dist
+
+    from paper_2208_00184_b200.shard import global_argmin, shard_range
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lo, hi = shard_range(len(makespans), rank, world)
+    ms, idx = global_argmin(np.asarray(makespans[lo:hi]), lo)
+    out[rank] = (ms, idx)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _run(makespans, world=2):
+    port = _free_port()
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_worker, args=(world, port, list(map(int, makespans)), out), nprocs=world, join=True)
+        return dict(out)
+
+
+def test_sharded_argmin_matches_single_process(oracle):
+    from graphs import layered
+    g = layered(3, 600, 12)
+    _, m = oracle.fuse(g, (0.001, 10.0), 200, int(g.memory_bytes.sum()) // 8)
+    rng = np.random.default_rng(5)
+    cand = rng.integers(0, 4, (37, m.n_clusters)).astype(np.uint8)
+    devs = [(d, 10 ** 12) for d in range(4)]
+    makespans, am = oracle.simulate_candidates(g, m.node_cluster, m.n_clusters, cand, devs, (0.001, 10.0))
+    res = _run(makespans)
+    assert res[0] == res[1] == (int(makespans[am]), am)
+
+
+def test_tie_goes_to_lowest_index():
+    makespans = np.array([9, 5, 7, 5, 5, 8, 5], np.int64)  # minimum 5 at 1, 3, 4, 6
+    res = _run(makespans)
+    assert res[0] == res[1] == (5, 1)
+
+
+def test_empty_shard_and_packing():
+    from paper_2208_00184_b200.shard import pack, shard_range, unpack
+    assert shard_range(3, 1, 4) == (1, 2) and shard_range(3, 3, 4) == (3, 3)
+    assert unpack(pack(123456789, 65535)) == (123456789, 65535)
+    with pytest.raises(ValueError):
+        pack(1, 1 << 20)
+    res = _run(np.array([4], np.int64))
+    assert res[0] == res[1] == (4, 0)
