@@ -30,6 +30,10 @@ import time
 
 import numpy as np
 
+# Each replica runs on its own stream; the default 8 hardware work queues would make
+# streams share queues and serialise long kernels of different replicas.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))

@@ -95,7 +95,7 @@ void levels_dev(DevGraph& g, dp_comm_t comm, DevBuf<int64_t>& t, DevBuf<int64_t>
   c.alloc(ctx, g.n > 0 ? g.n : 1);
   {
     StageScope st(ctx, "levels", 40.0 * g.m_ok + 48.0 * g.n);
-    graph_kahn(g, t.p, b.p, nullptr);
+    if (!graph_levels_indexorder(g, t.p, b.p)) graph_kahn(g, t.p, b.p, nullptr);
   }
   if (g.processed != g.n) {
     std::vector<int64_t> wit = graph_cycle_witness(g);

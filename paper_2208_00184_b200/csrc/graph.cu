@@ -301,6 +301,104 @@ __device__ __forceinline__ void kahn_pull_warp(const KahnArgs& a, int32_t v) {
   }
 }
 
+
+// ---- levels in index order (graphs whose node index order is topological, e.g. the
+// coarse graph of fuse(), whose clusters are runs of a topological order).  Such graphs
+// are chain-like (depth ~ n), where the level-synchronous frontier pays one grid-wide
+// step per node.  Here one CTA sweeps the nodes in index order: all warps stage a tile of
+// rows (CSC for tlevel, CSR backwards for blevel) into shared memory, then warp 0 walks
+// the tile with the running finish/blevel values in shared memory: per node one gather
+// per in-edge and a two-step 64-bit max (redux.sync on high then low words).
+constexpr int kSeqMaxN = 12288;
+constexpr int kSeqTile = 6144;   // edges staged per tile
+constexpr int kSeqTileN = 2048;  // nodes staged per tile
+
+__global__ void k_index_topo(const int32_t* in_off, const int32_t* in_src, int32_t n, int* ok) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+    for (int32_t k = in_off[v]; k < in_off[v + 1]; ++k)
+      if (in_src[k] >= v) atomicExch(ok, 0);
+}
+
+__device__ __forceinline__ int64_t warp_max_nonneg(int64_t x) {
+  const uint32_t hi = static_cast<uint32_t>(static_cast<uint64_t>(x) >> 32);
+  const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+  const uint32_t lo = hi == mh ? static_cast<uint32_t>(x) : 0u;
+  const uint32_t ml = __reduce_max_sync(0xffffffffu, lo);
+  return static_cast<int64_t>((static_cast<uint64_t>(mh) << 32) | ml);
+}
+
+// forward: tlevel[v] = max(0, max_{u->v} f[u] + c), f[u] = tlevel[u] + w[u]
+// backward (rev): blevel[v] = w[v] + max(0, max_{v->s} blevel[s] + c)
+__global__ void __launch_bounds__(1024) k_levels_seq(int32_t n, const int32_t* off, const int32_t* nbr,
+                                                     const int64_t* cost, const int64_t* w, int64_t* out,
+                                                     bool rev) {
+  extern __shared__ int64_t sm64[];
+  int64_t* val = sm64;                                         // [n]: f (fwd) or blevel (bwd)
+  int64_t* ec = val + kSeqMaxN;                                // [kSeqTile]
+  int64_t* wt = ec + kSeqTile;                                 // [kSeqTileN]
+  int32_t* en = reinterpret_cast<int32_t*>(wt + kSeqTileN);    // [kSeqTile]
+  int32_t* ot = en + kSeqTile;                                 // [kSeqTileN + 1]
+  __shared__ int32_t tile_hi;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t done = 0;  // nodes processed (in sweep order)
+  while (done < n) {
+    // tile: sweep positions [done, hi) with at most kSeqTile edges (at least one node)
+    if (threadIdx.x == 0) {
+      const int32_t v0 = rev ? n - 1 - done : done;
+      const int32_t base = rev ? off[v0 + 1] : off[v0];
+      int32_t lo = done + 1, hi = min(n, done + kSeqTileN);  // largest end with edge span <= kSeqTile
+      while (lo < hi) {
+        const int32_t mid = (lo + hi + 1) >> 1;
+        const int32_t span = rev ? base - off[n - mid] : off[mid] - base;
+        if (span <= kSeqTile) lo = mid; else hi = mid - 1;
+      }
+      tile_hi = lo;
+    }
+    __syncthreads();
+    const int32_t hi = tile_hi;
+    const int32_t e0 = rev ? off[n - hi] : off[done];
+    const int32_t e1 = rev ? off[n - done] : off[hi];
+    const bool fits = e1 - e0 <= kSeqTile;
+    if (fits) {
+      for (int32_t k = threadIdx.x; k < e1 - e0; k += blockDim.x) {
+        en[k] = nbr[e0 + k];
+        ec[k] = cost[e0 + k];
+      }
+    }
+    for (int32_t i = done + threadIdx.x; i <= hi; i += blockDim.x) {
+      const int32_t v = rev ? n - 1 - i : i;  // sweep position i -> row start of node v (i < hi)
+      if (i < hi) {
+        wt[i - done] = w[v];
+        ot[i - done] = rev ? off[v + 1] : off[v];  // row end (bwd) / start (fwd)
+      } else {
+        ot[i - done] = rev ? off[n - hi] : off[hi];
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      for (int32_t i = done; i < hi; ++i) {
+        const int32_t v = rev ? n - 1 - i : i;
+        const int32_t b = rev ? ot[i + 1 - done] : ot[i - done], e = rev ? ot[i - done] : ot[i + 1 - done];
+        int64_t mx = 0;
+        for (int32_t k = b + lane; k < e; k += 32) {
+          const int32_t u = fits ? en[k - e0] : nbr[k];
+          const int64_t c = fits ? ec[k - e0] : cost[k];
+          mx = max(mx, val[u] + c);
+        }
+        mx = warp_max_nonneg(mx);
+        if (lane == 0) {
+          const int64_t wv = wt[i - done];
+          val[v] = rev ? mx + wv : mx + wv;  // f[v] = tlevel + w (fwd); blevel (bwd)
+          out[v] = rev ? mx + wv : mx;
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    done = hi;
+  }
+}
+
 __global__ void k_kahn_init(KahnArgs a) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < a.n; v += (int64_t)gridDim.x * blockDim.x) {
     const bool src = a.indeg[v] == 0;
@@ -588,6 +686,29 @@ void graph_costs(DevGraph& g, dp_comm_t comm) {
   g.has_cost = true;
   g.ck = comm.k_us_per_byte;
   g.cb = comm.b_us;
+}
+
+// Levels by an index-order sweep when the node index order is topological and the graph
+// is small enough for on-chip values; returns false otherwise (caller uses graph_kahn).
+bool graph_levels_indexorder(DevGraph& g, int64_t* tlevel, int64_t* blevel) {
+  dp_ctx* ctx = g.ctx;
+  const int32_t n = g.n;
+  if (n == 0 || n > kSeqMaxN || getenv("DP_LEVELS_KAHN")) return false;
+  DevBuf<int> ok(ctx, 1);
+  int one = 1;
+  ok.upload(&one, 1);
+  DP_LAUNCH(ctx, k_index_topo, grid_for(n, 256), 256, 0, g.in_off.p, g.in_src.p, n, ok.p);
+  if (scalar_to_host(ctx, ok.p) != 1) return false;
+  const size_t sm = sizeof(int64_t) * (kSeqMaxN + kSeqTile + kSeqTileN) + sizeof(int32_t) * (kSeqTile + kSeqTileN + 1);
+  static bool attr = false;
+  if (!attr) {
+    DP_CUDA(cudaFuncSetAttribute(k_levels_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    attr = true;
+  }
+  DP_LAUNCH(ctx, k_levels_seq, 1, 1024, sm, n, g.in_off.p, g.in_src.p, g.in_cost.p, g.w.p, tlevel, false);
+  DP_LAUNCH(ctx, k_levels_seq, 1, 1024, sm, n, g.out_off.p, g.out_dst.p, g.out_cost.p, g.w.p, blevel, true);
+  g.processed = n;
+  return true;
 }
 
 void graph_kahn(DevGraph& g, int64_t* tlevel, int64_t* blevel, int32_t* level_of) {

@@ -63,6 +63,14 @@ struct PeelArgs {
   const int32_t* out_off;
   const int32_t* out_dst;
   int2* gstack2;         // { node, min(out-degree, 255) }
+  // stack-mode layout (peel_warp_v6)
+  bool v6;
+  const int4* ell6;      // 8 slots {child, rank | min(indeg,127) << 24 | (deg > 8) << 31} per node
+  const int2* cmeta;     // the same records over the CSR (rows longer than 8)
+  int32_t* rem_big;      // remaining in-degree of nodes with in-degree >= 127
+  int32_t* gsid;         // global stack of {node | long flag}
+  int32_t* gover;        // remaining in-degree of keys spilled from full buckets (0 = absent)
+  long long* debug;      // optional: peel warp cycles
 };
 
 // The peel warp.  Shared memory: stack cache (kStackCache int4) + freed buffer.
@@ -233,7 +241,10 @@ __device__ void peel_warp_v5(const PeelArgs& a, int2* sstack, int64_t* sfreed, i
     const int2 e = sstack[top & (SC - 1)];
     --top;
     const int32_t v = e.x, deg = e.y;
-    if (lane == 0) seqbuf[p & 31] = v;
+    if (lane == 0) {
+      seqbuf[p & 31] = v;
+      a.pos_of[v] = p;
+    }
     ++p;
     if ((p & 31) == 0) {
       __syncwarp();
@@ -369,7 +380,228 @@ __device__ void peel_warp_v5(const PeelArgs& a, int2* sstack, int64_t* sfreed, i
   }
 }
 
+// ---------------------------------------------------------------- peel v6
+// Stack-mode peel (DFS/CPD) with the remaining in-degrees on chip.
+//  * Remaining in-degrees of OPEN nodes (some but not all predecessors emitted) live in a
+//    2-way bucketed hash table in shared memory (one 8-byte load answers a lookup);
+//    a bucket whose two ways are taken spills further keys to a global counter array
+//    and counts them, so lookups only touch HBM in buckets that actually overflowed.
+//    A node's first decrement needs no lookup: its initial in-degree rides in its
+//    parent's row.
+//  * Rows hold 8 slots {child, rank | min(indeg,127) << 24 | (deg > 8) << 31} sorted by
+//    rank, so the push order of the freed children is a popcount of the freed mask.
+//  * Every cached stack entry carries its node's 64-byte row: a popped node's row is on
+//    chip.  The only global load of a step — the rows of the popped node's children, any
+//    of which may be pushed — is issued first and overlaps the table work; when a child
+//    is pushed, its children's rows are prefetched to L2.
+//  * Rows longer than 8 take a CSR path; in-degrees >= 127 use global counters.
+constexpr int kV6Stack = 512;
+constexpr int kV6BucketBits = 14;
+constexpr uint32_t kV6Empty = 0xffffffffu;
+constexpr int32_t kV6Long = 1 << 30;  // sid flag: out-degree > 8 (CSR path)
+constexpr int kV6FreedCap = 1024;
+
+struct V6Smem {
+  int4 row[kV6Stack][4];
+  int32_t sid[kV6Stack];
+  uint32_t ht[2 << kV6BucketBits];      // way 0 / way 1 of bucket b at [2b], [2b+1]
+  uint32_t ovc[1 << (kV6BucketBits - 1)];  // 16-bit overflow counts, two per word
+  int64_t freed[kV6FreedCap];
+  int32_t seqbuf[32];
+};
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+__device__ __forceinline__ uint32_t v6_bucket(int32_t c) {
+  return (static_cast<uint32_t>(c) * 0x9E3779B1u) >> (32 - kV6BucketBits);
+}
+
+// One decrement of child c (initial in-degree `code`, 2..126).  Returns true when c is freed.
+__device__ __forceinline__ bool v6_dec(V6Smem& S, int32_t* gover, int32_t c, int code) {
+  const uint32_t b = v6_bucket(c), uc = static_cast<uint32_t>(c);
+  const uint2 w = *reinterpret_cast<const uint2*>(&S.ht[2 * b]);
+  if ((w.x >> 7) == uc) {
+    const uint32_t r = (w.x & 127u) - 1;
+    S.ht[2 * b] = r ? w.x - 1 : kV6Empty;
+    return r == 0;
+  }
+  if ((w.y >> 7) == uc) {
+    const uint32_t r = (w.y & 127u) - 1;
+    S.ht[2 * b + 1] = r ? w.y - 1 : kV6Empty;
+    return r == 0;
+  }
+  const uint32_t sh = (b & 1u) * 16;
+  if ((S.ovc[b >> 1] >> sh) & 0xffffu) {
+    const int32_t g = gover[c];
+    if (g > 0) {
+      gover[c] = g - 1;
+      if (g == 1) atomicSub(&S.ovc[b >> 1], 1u << sh);
+      return g == 1;
+    }
+  }
+  const uint32_t nv = (uc << 7) | static_cast<uint32_t>(code - 1);
+  if (w.x == kV6Empty && atomicCAS(&S.ht[2 * b], kV6Empty, nv) == kV6Empty) return false;
+  if (w.y == kV6Empty && atomicCAS(&S.ht[2 * b + 1], kV6Empty, nv) == kV6Empty) return false;
+  gover[c] = code - 1;
+  atomicAdd(&S.ovc[b >> 1], 1u << sh);
+  return false;
+}
+
+// Loads stack entries [lo, hi] (ids from the global stack, rows from the ELL) into the cache.
+__device__ void v6_fill(const PeelArgs& a, V6Smem& S, int32_t lo, int32_t hi, int lane) {
+  for (int32_t idx = lane; idx < (hi - lo + 1) * 4; idx += 32) {
+    const int32_t i = lo + (idx >> 2);
+    const int32_t sv = a.gsid[i];
+    if ((idx & 3) == 0) S.sid[i & (kV6Stack - 1)] = sv;
+    S.row[i & (kV6Stack - 1)][idx & 3] = a.ell6[static_cast<int64_t>(sv & 0xffffff) * 4 + (idx & 3)];
+  }
+}
+
+__device__ __forceinline__ void v6_publish(const PeelArgs& a, int32_t p) {
+  if (a.progress) {
+    __threadfence();
+    st_release(a.progress, p);
+  }
+}
+
+__device__ void peel_warp_v6(const PeelArgs& a, V6Smem& S) {
+  const int lane = threadIdx.x & 31;
+  const long long t_start = clock64();
+  constexpr int32_t SC = kV6Stack;
+  for (int i = lane; i < (2 << kV6BucketBits); i += 32) S.ht[i] = kV6Empty;
+  for (int i = lane; i < (1 << (kV6BucketBits - 1)); i += 32) S.ovc[i] = 0;
+  int32_t top = a.nsrc - 1;
+  int32_t base = max(0, a.nsrc - SC / 2);
+  v6_fill(a, S, base, top, lane);
+  __syncwarp();
+  int32_t p = 0;
+  while (top >= 0) {
+    if (top < base) {
+      base = max(0, top + 1 - SC / 2);
+      v6_fill(a, S, base, top, lane);
+      __syncwarp();
+    }
+    const int32_t slot = top & (SC - 1);
+    const int32_t sv = S.sid[slot];
+    --top;
+    const int32_t v = sv & 0xffffff;
+    if (lane == 0) {
+      S.seqbuf[p & 31] = v;
+      a.pos_of[v] = p;
+    }
+    ++p;
+    if ((p & 31) == 0) {
+      __syncwarp();
+      a.seq[p - 32 + lane] = S.seqbuf[lane];
+      if ((p & 255) == 0 && lane == 0) v6_publish(a, p);
+    }
+    if (sv & kV6Long) {
+      // ---- CSR path: rows longer than 8
+      const int32_t rs = a.out_off[v], dg = a.out_off[v + 1] - rs;
+      int32_t nf = 0;
+      for (int32_t b0 = 0; b0 < dg; b0 += 32) {
+        const int32_t k = b0 + lane;
+        int2 cm = make_int2(-1, 0);
+        if (k < dg) cm = a.cmeta[rs + k];
+        bool fr = false;
+        if (cm.x >= 0) {
+          const int code = (cm.y >> 24) & 127;
+          if (code == 1) fr = true;
+          else if (code == 127) fr = atomicSub(a.rem_big + cm.x, 1) == 1;
+          else fr = v6_dec(S, a.gover, cm.x, code);
+        }
+        const unsigned m = __ballot_sync(FULL, fr);
+        if (fr) {
+          const int32_t at = nf + __popc(m & ((1u << lane) - 1));
+          const int64_t rec = (static_cast<int64_t>(cm.y & 0xffffff) << 32) |
+                              static_cast<uint32_t>(cm.x | (cm.y < 0 ? kV6Long : 0));
+          if (at < kV6FreedCap) S.freed[at] = rec; else a.freed_spill[at - kV6FreedCap] = rec;
+        }
+        nf += __popc(m);
+      }
+      __syncwarp();
+      if (nf > 0) {
+        if (top + nf - base >= SC - 1) {
+          for (int32_t i = base + lane; i <= top; i += 32) a.gsid[i] = S.sid[i & (SC - 1)];
+          __syncwarp();
+          base = top + 1;
+        }
+        const bool big = nf >= SC - 1;
+        for (int32_t i = lane; i < nf; i += 32) {
+          const int64_t ri = i < kV6FreedCap ? S.freed[i] : a.freed_spill[i - kV6FreedCap];
+          const int32_t rk = static_cast<int32_t>(ri >> 32);
+          int32_t cnt = 0;
+          for (int32_t j = 0; j < nf; ++j) {
+            const int64_t rj = j < kV6FreedCap ? S.freed[j] : a.freed_spill[j - kV6FreedCap];
+            cnt += static_cast<int32_t>(rj >> 32) > rk;
+          }
+          const int32_t sidv = static_cast<int32_t>(ri & 0xffffffff);
+          if (big) a.gsid[top + 1 + cnt] = sidv; else S.sid[(top + 1 + cnt) & (SC - 1)] = sidv;
+        }
+        __syncwarp();
+        if (!big) {
+          for (int32_t idx = lane; idx < nf * 4; idx += 32) {
+            const int32_t e = (top + 1 + (idx >> 2)) & (SC - 1);
+            const int32_t c = S.sid[e] & 0xffffff;
+            S.row[e][idx & 3] = a.ell6[static_cast<int64_t>(c) * 4 + (idx & 3)];
+          }
+        }
+        top += nf;
+        if (big) base = top + 1;
+        __syncwarp();
+      }
+      continue;
+    }
+    // ---- 8-slot row on chip (slots sorted by rank)
+    const int2* rowp = reinterpret_cast<const int2*>(S.row[slot]);
+    const int q = lane >> 2;
+    const int2 cq = rowp[q];
+    int4 crow = make_int4(-1, 0, -1, 0);
+    if (cq.x >= 0) crow = a.ell6[static_cast<int64_t>(cq.x) * 4 + (lane & 3)];
+    const int2 my = rowp[lane & 7];
+    bool fr = false;
+    if (lane < 8 && my.x >= 0) {
+      const int code = (my.y >> 24) & 127;
+      if (code == 1) fr = true;
+      else if (code == 127) fr = atomicSub(a.rem_big + my.x, 1) == 1;
+      else fr = v6_dec(S, a.gover, my.x, code);
+    }
+    const unsigned m = __ballot_sync(FULL, fr);
+    if (m) {
+      const int nf = __popc(m);
+      if (top + nf - base >= SC - 1) {  // spill the lower half of the cache (rows are dropped)
+        for (int32_t i = base + lane; i < base + SC / 2; i += 32) a.gsid[i] = S.sid[i & (SC - 1)];
+        __syncwarp();
+        base += SC / 2;
+      }
+      // pushed in descending rank: slot k lands above every freed slot of higher rank
+      if ((m >> q) & 1u) {
+        S.row[(top + 1 + __popc(m >> q >> 1)) & (SC - 1)][lane & 3] = crow;
+        if (crow.x >= 0) prefetch_l2(a.ell6 + static_cast<int64_t>(crow.x) * 4);
+        if (crow.z >= 0) prefetch_l2(a.ell6 + static_cast<int64_t>(crow.z) * 4);
+      }
+      if (fr) S.sid[(top + 1 + __popc(m >> lane >> 1)) & (SC - 1)] = my.x | (my.y < 0 ? kV6Long : 0);
+      top += nf;
+    }
+    __syncwarp();
+  }
+  __syncwarp();
+  if (lane < (p & 31)) a.seq[(p & ~31) + lane] = S.seqbuf[lane];
+  __syncwarp();
+  if (lane == 0) {
+    *a.emitted = p;
+    v6_publish(a, p);
+    if (a.debug) *a.debug = clock64() - t_start;
+  }
+}
+
 __device__ __forceinline__ void peel_dispatch(const PeelArgs& a, int4* smem4) {
+  if (a.v6) {
+    peel_warp_v6(a, *reinterpret_cast<V6Smem*>(smem4));
+    return;
+  }
   int64_t* sfreed = reinterpret_cast<int64_t*>(smem4 + kStackCache);
   int32_t* srow = reinterpret_cast<int32_t*>(sfreed + kFreedCap);
   int32_t* stop = srow + 32;
@@ -403,6 +635,8 @@ struct DpArgs {
   int32_t* prev_cut;        // [n+1]
   int* first_exceed;
   bool keys32;              // window values fit 32-bit keys (see peel_dp_stream)
+  bool block32;             // ... with 32 steps of drift headroom: 32-step block recurrence
+  bool v3;                  // block32 and R <= 225: multi-warp age-ordered recurrence
   long long* debug;         // optional: [total, waiting, staging] cycles of the DP warp
 };
 
@@ -427,6 +661,8 @@ struct DpSmem {
   int64_t pref[kRing];
   int32_t node[kCh];
   int32_t ioff[kCh];
+  int32_t mt[32][33];  // block recurrence: per step, per lane minimum over old candidates
+  int32_t ct[32][33];  // block recurrence: per step, placeholder key of block candidate k
 };
 
 __device__ void dp_warp(const DpArgs& a, DpSmem& S) {
@@ -454,7 +690,7 @@ __device__ void dp_warp(const DpArgs& a, DpSmem& S) {
     const long long tw0 = clock64();
     while (avail < j1 + 1) {
       avail = ld_acquire(a.progress);
-      if (avail < j1 + 1) __nanosleep(200);
+        if (avail < j1 + 1) __nanosleep(200);
     }
     wait_cycles += clock64() - tw0;
     // node, memory, out-cost, in-degree per position
@@ -550,6 +786,106 @@ __device__ void dp_warp(const DpArgs& a, DpSmem& S) {
     }
     __syncwarp();
     stage_cycles += clock64() - tw0;
+    if (a.keys32 && a.block32) {
+      // ---- 32-step blocks, 32-bit keys K = (D - off) * 256 + distance, slot of candidate
+      // i = lane (i & 31), register (i >> 5) & 7.  Per block [P, P+32):
+      //  A. lanes advance all window slots through the 32 transitions (independent work):
+      //     the minimum over the block's OLD candidates (i <= P, value known) per step goes
+      //     to S.mt[step][lane]; block candidate P+k lives in lane k's register Kn, entered
+      //     with a placeholder value 0 instead of best[P+k] (unknown yet), and its key per
+      //     step goes to S.ct[step][k].  All later updates are additive, so its real key is
+      //     placeholder + (best[P+k] - off_{P+k-1}) * 256.
+      //  B. lane t: R = min_q mt[t][q], then k = 1..31 in order: best[P+k] = lane k-1's R
+      //     (final once candidates < P+k are in), candidate key ct[t][k] + bestrel * 256.
+      //  Ties: the smaller key has the smaller distance = the larger i (fusion.cpp:152).
+      if (j0 == 0) {
+        off = S.out[0];  // candidate 0: D_1(0) = out(0)
+        if (lane == 0) K[0] = 0;
+      }
+      for (int32_t tb = 0; tb < cnt; tb += 32) {
+        const int32_t P = j0 + tb;
+        const int32_t nb = min(32, cnt - tb);
+        const int rb = (P >> 5) & (SPL - 1);
+        int32_t Kn = 0;
+        for (int32_t u = 0; u < nb; ++u) {
+          const int32_t t = tb + u, p = P + u;
+          if (p > 0) {
+#pragma unroll
+            for (int r = 0; r < SPL; ++r) K[r] += 1;
+            Kn += 1;
+            if (u == 0) {
+              if (lane == 0) {
+#pragma unroll
+                for (int r = 0; r < SPL; ++r)
+                  if (r == rb) K[r] = bvr * 256;
+              }
+            } else if (lane == u) {
+              Kn = 0;
+            }
+            const bool live_n = lane >= 1 && lane <= u;
+            const int32_t kb = S.off[t], ke = S.off[t + 1];
+            for (int32_t k = kb; k < ke; ++k) {
+              int32_t av;
+              int64_t cv;
+              if (staged) {
+                av = S.ipos[k];
+                cv = S.ic[k];
+              } else {
+                av = a.pos_of[a.in_src[S.ioff[t] - kb + k]];
+                cv = a.in_cost[S.ioff[t] - kb + k];
+              }
+              if (av <= p - W) continue;
+              const int32_t thr = p - av;
+              const int32_t sub = static_cast<int32_t>(cv) << 8;
+#pragma unroll
+              for (int r = 0; r < SPL; ++r)
+                if ((K[r] & 255) >= thr) K[r] -= sub;
+              if (live_n && (Kn & 255) >= thr) Kn -= sub;
+            }
+            off += S.out[t];
+          }
+          // minimum over the old candidates: u <= distance <= p - lo[p+1]
+          const int32_t span = p - S.lo[t] - u;
+          int32_t mk = INT32_MAX;
+          if (span >= 0) {
+#pragma unroll
+            for (int r = 0; r < SPL; ++r)
+              if (static_cast<uint32_t>((K[r] & 255) - u) <= static_cast<uint32_t>(span) && K[r] < mk) mk = K[r];
+          }
+          S.mt[u][lane] = mk;
+          if (lane >= 1 && lane <= u) S.ct[u][lane] = Kn;
+        }
+        __syncwarp();
+        int32_t R = INT32_MAX, maxd = -1;
+        if (lane < nb) {
+#pragma unroll 8
+          for (int q = 0; q < 32; ++q) R = min(R, S.mt[lane][q]);
+          maxd = P + lane - S.lo[tb + lane];
+        }
+        for (int k = 1; k < nb; ++k) {
+          const int32_t b = __shfl_sync(FULL, R, k - 1) >> 8;
+          const int32_t c = S.ct[lane][k];
+          if (lane >= k && lane - k <= maxd) R = min(R, c + b * 256);
+        }
+        if (lane < nb) a.prev_cut[P + lane + 1] = P + lane - (R & 255);
+        const int32_t bk = __shfl_up_sync(FULL, R, 1) >> 8;
+        if (lane >= 1 && lane < nb) {
+#pragma unroll
+          for (int r = 0; r < SPL; ++r)
+            if (r == rb) K[r] = Kn + bk * 256;
+        }
+        bvr = __shfl_sync(FULL, R, nb - 1) >> 8;
+        if (bvr > (1 << 20) || bvr < -(1 << 20)) {
+#pragma unroll
+          for (int r = 0; r < SPL; ++r)
+            if (K[r] < kUnfilled) K[r] -= bvr * 256;
+          off += bvr;
+          bvr = 0;
+        }
+        __syncwarp();
+      }
+      continue;
+    }
     if (a.keys32) {
       // ---- 32-bit keys: K = (D - OFFSET) * 256 + distance; argmin = one redux.sync
       if (j0 == 0) {
@@ -680,11 +1016,304 @@ __device__ void dp_warp(const DpArgs& a, DpSmem& S) {
 }
 
 
-__global__ void __launch_bounds__(32) k_peel_dp(PeelArgs pa, DpArgs da) {
+// ---------------------------------------------------------------- DP v3 (R <= 225)
+// One compute warp plus kDpProducers staging warps per DP CTA.  Producer k stages chunks
+// k, k + P, ... (256 positions each) into its own buffer — node, out-cost sum, lo[j] from a
+// local memory prefix, in-edges as (source position, cost) — so staging latency is off
+// the recurrence's path.  The compute warp keeps the window in AGE order: lane l holds
+// old candidates i = B - 224 + 32r + l (r = 0..6, B = block start) in K[r] and the block's
+// own candidate B + l in Kn; keys are (value - off) * 256 + (255 - (i - (B - 224))), so the
+// tie-break byte is fixed inside a block (no per-step increments), "i <= a" is r <= a
+// shifted by 5, and each block ends with one register rotation.  Blocks run the two-phase
+// recurrence of the block32 path (independent slot updates, then a 31-step chain over the
+// block's own candidates).
+constexpr int kDpProducers = 3;
+constexpr int kDpWarps = 1 + kDpProducers;
+constexpr int kLpMax = 256 + kCh + 1;
+constexpr int kE2Cap = 4096;
+
+struct DpBuf {
+  int32_t lo[kCh];   // lo[j] for j = j0 + t + 1 (absolute position)
+  int64_t out[kCh];
+  int32_t off[kCh + 1];   // all in-edges of position t: [off[t], off[t+1])
+  int32_t off2[kCh + 1];  // in-window in-edges of position t in e2
+  int32_t cnt2[kCh];
+  int2 e2[kE2Cap];        // {source position, cost << 8}, sources >= block start - 224
+  int32_t ioff[kCh];
+  int64_t lp[kLpMax];
+  int32_t node[kCh];
+  int32_t cnt, n2;        // n2 > kE2Cap: the compute warp reads in-edges from HBM
+};
+
+struct DpSmem3 {
+  DpBuf buf[kDpProducers];
+  int32_t mt[32][33];
+  int32_t ct[32][33];
+  int ready[kDpProducers];
+  int consumed;
+};
+
+__device__ __forceinline__ int ld_volatile_shared(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+
+__device__ void dp_stage(const DpArgs& a, DpBuf& B, int32_t j0, int32_t cnt, int lane) {
+  for (int32_t t = lane; t < cnt; t += 32) {
+    const int32_t v = a.seq[j0 + t];
+    B.node[t] = v;
+    B.out[t] = a.out_sum[v];
+  }
+  // memory prefix over positions [b0, j0 + cnt): the window of every j in the chunk
+  const int32_t b0 = max(0, j0 - a.range);
+  const int32_t L = j0 + cnt - b0;
+  int64_t carry = 0;
+  if (lane == 0) B.lp[0] = 0;
+  for (int32_t x0 = 0; x0 < L; x0 += 32) {
+    const int32_t x = x0 + lane;
+    int64_t mv = 0;
+    if (x < L) {
+      const int32_t pos = b0 + x;
+      mv = a.mem[a.seq[pos]];
+      if (pos >= j0 && mv > a.limit) atomicMin(a.first_exceed, pos);
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(FULL, mv, o);
+      if (lane >= o) mv += y;
+    }
+    if (x < L) B.lp[x + 1] = carry + mv;
+    carry += __shfl_sync(FULL, mv, 31);
+  }
+  __syncwarp();
+  for (int32_t t = lane; t < cnt; t += 32) {
+    const int32_t j = j0 + t + 1;
+    int32_t lo = max(0, j - a.range), hi = j - 1;
+    const int64_t pj = B.lp[j - b0];
+    while (lo < hi) {
+      const int32_t mid = (lo + hi) >> 1;
+      if (pj - B.lp[mid - b0] <= a.limit) hi = mid; else lo = mid + 1;
+    }
+    B.lo[t] = lo;
+  }
+  // in-edge offsets per position
+  int32_t my_in = 0;
+  for (int32_t t0 = 0; t0 < kCh; t0 += 32) {
+    const int32_t t = t0 + lane;
+    int32_t c = 0;
+    if (t < cnt) {
+      const int32_t v = B.node[t];
+      const int32_t b = a.in_off[v];
+      B.ioff[t] = b;
+      c = a.in_off[v + 1] - b;
+    }
+    if (t < kCh) B.cnt2[t] = 0;
+    int32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    if (t < kCh) B.off[t + 1] = my_in + x;
+    my_in += __shfl_sync(FULL, x, 31);
+  }
+  if (lane == 0) B.off[0] = 0;
+  __syncwarp();
+  // gather (source position, cost) of every in-edge; keep those whose source can still
+  // be a candidate in the edge's block (>= block start - 224), compacted in edge order
+  int32_t n2 = 0;
+  for (int32_t o0 = 0; o0 < my_in; o0 += 128) {
+    int32_t src[4], tt[4];
+    int64_t cc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int32_t o = o0 + u * 32 + lane;
+      src[u] = -1;
+      cc[u] = 0;
+      tt[u] = 0;
+      if (o < my_in) {
+        int32_t lo = 0, hi = cnt - 1;  // last t with off[t] <= o
+        while (lo < hi) {
+          const int32_t mid = (lo + hi + 1) >> 1;
+          if (B.off[mid] <= o) lo = mid; else hi = mid - 1;
+        }
+        const int32_t k = B.ioff[lo] + (o - B.off[lo]);
+        tt[u] = lo;
+        src[u] = a.in_src[k];
+        cc[u] = a.in_cost[k];
+      }
+    }
+    int32_t av[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) av[u] = src[u] >= 0 ? a.pos_of[src[u]] : -1;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool keep = src[u] >= 0 && av[u] >= j0 + (tt[u] & ~31) - 224;
+      const unsigned m = __ballot_sync(FULL, keep);
+      if (keep) {
+        const int32_t idx = n2 + __popc(m & ((1u << lane) - 1));
+        if (idx < kE2Cap) B.e2[idx] = make_int2(av[u], static_cast<int32_t>(cc[u]) << 8);
+        atomicAdd(&B.cnt2[tt[u]], 1);
+      }
+      n2 += __popc(m);
+    }
+  }
+  __syncwarp();
+  int32_t run = 0;
+  for (int32_t t0 = 0; t0 < kCh; t0 += 32) {
+    const int32_t t = t0 + lane;
+    int32_t x = B.cnt2[t];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    B.off2[t + 1] = run + x;
+    run += __shfl_sync(FULL, x, 31);
+  }
+  if (lane == 0) {
+    B.off2[0] = 0;
+    B.cnt = cnt;
+    B.n2 = n2;
+  }
+}
+
+__device__ void dp_producer(const DpArgs& a, DpSmem3& S, int k, int lane) {
+  int avail = 0;
+  for (int32_t c = k;; c += kDpProducers) {
+    const int32_t j0 = c * kCh;
+    if (j0 >= a.n) break;
+    const int32_t j1 = min(a.n - 1, j0 + kCh - 1);
+    while (ld_volatile_shared(&S.consumed) < c - kDpProducers + 1) __nanosleep(100);
+    while (avail < j1 + 1) {
+      avail = ld_acquire(a.progress);
+      if (avail < j1 + 1) __nanosleep(200);
+    }
+    dp_stage(a, S.buf[k], j0, j1 - j0 + 1, lane);
+    __syncwarp();
+    __threadfence_block();
+    if (lane == 0) *reinterpret_cast<volatile int*>(&S.ready[k]) = c;
+  }
+}
+
+__device__ void dp_compute_v3(const DpArgs& a, DpSmem3& S) {
+  constexpr int NR = 7;
+  const int lane = threadIdx.x & 31;
+  const int32_t n = a.n;
+  constexpr int32_t kUnfilled = 0x3f000000;
+  int32_t K[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) K[r] = kUnfilled;
+  int32_t Kn = kUnfilled;
+  int64_t off = 0;   // candidate 0 enters with best[0] = 0 relative to off = 0
+  int32_t bvr = 0;
+  long long wait_cycles = 0;
+  const long long t_start = clock64();
+  for (int32_t c = 0;; ++c) {
+    const int32_t j0 = c * kCh;
+    if (j0 >= n) break;
+    const int kb = c % kDpProducers;
+    const long long tw0 = clock64();
+    while (ld_volatile_shared(&S.ready[kb]) != c) __nanosleep(32);
+    wait_cycles += clock64() - tw0;
+    __threadfence_block();
+    const DpBuf& B = S.buf[kb];
+    const int32_t cnt = B.cnt;
+    const bool staged = B.n2 <= kE2Cap;
+    for (int32_t tb = 0; tb < cnt; tb += 32) {
+      const int32_t P = j0 + tb;
+      const int32_t nb = min(32, cnt - tb);
+      const int32_t c0 = 224 - P - lane;
+      const int32_t kn_lim = -P - lane;  // Kn (candidate P + lane) loses c iff av + kn_lim >= 0
+#pragma unroll 1
+      for (int32_t u = 0; u < nb; ++u) {
+        const int32_t t = tb + u;
+        if (lane == u) Kn = (u == 0 ? bvr * 256 : 0) + 31 - u;
+        if (staged) {
+          const int32_t eb = B.off2[t], ee = B.off2[t + 1];
+          for (int32_t e = eb; e < ee; ++e) {
+            const int2 x = B.e2[e];
+            const int32_t rmax = (x.x + c0) >> 5;
+#pragma unroll
+            for (int r = 0; r < NR; ++r) K[r] -= r <= rmax ? x.y : 0;
+            Kn -= x.x + kn_lim >= 0 ? x.y : 0;
+          }
+        } else {
+          const int32_t eb = B.off[t], ee = B.off[t + 1];
+          for (int32_t e = eb; e < ee; ++e) {
+            const int32_t k = B.ioff[t] + (e - eb);
+            const int32_t av = a.pos_of[a.in_src[k]];
+            if (av < P - 224) continue;
+            const int32_t sub = static_cast<int32_t>(a.in_cost[k]) << 8;
+            const int32_t rmax = (av + c0) >> 5;
+#pragma unroll
+            for (int r = 0; r < NR; ++r) K[r] -= r <= rmax ? sub : 0;
+            Kn -= av + kn_lim >= 0 ? sub : 0;
+          }
+        }
+        off += B.out[t];
+        // minimum over the old candidates i in [lo[p+1], P] (tree)
+        const int32_t lo = B.lo[t];
+        const int32_t rmin = (lo + c0 + 31) >> 5;
+        int32_t mv[8];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) mv[r] = r >= rmin ? K[r] : INT32_MAX;
+        mv[7] = (lane == 0 && P >= lo) ? Kn : INT32_MAX;
+        const int32_t m01 = min(mv[0], mv[1]), m23 = min(mv[2], mv[3]), m45 = min(mv[4], mv[5]),
+                      m67 = min(mv[6], mv[7]);
+        S.mt[u][lane] = min(min(m01, m23), min(m45, m67));
+        if (lane >= 1 && lane <= u) S.ct[u][lane] = Kn;
+      }
+      __syncwarp();
+      int32_t R = INT32_MAX, kmin = 0;
+      if (lane < nb) {
+        int32_t r4[4] = {INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX};
+#pragma unroll
+        for (int q = 0; q < 32; ++q) r4[q & 3] = min(r4[q & 3], S.mt[lane][q]);
+        R = min(min(r4[0], r4[1]), min(r4[2], r4[3]));
+        kmin = B.lo[tb + lane] - P;
+      }
+      for (int k = 1; k < nb; ++k) {
+        const int32_t b = __shfl_sync(FULL, R, k - 1) >> 8;
+        const int32_t cc = S.ct[lane][k];
+        if (lane >= k && k >= kmin) R = min(R, cc + b * 256);
+      }
+      if (lane < nb) a.prev_cut[P + lane + 1] = P + 31 - (R & 255);
+      const int32_t bk = __shfl_up_sync(FULL, R, 1) >> 8;
+      if (lane >= 1) Kn += bk * 256;
+#pragma unroll
+      for (int r = 0; r < NR - 1; ++r) K[r] = K[r + 1] + 32;
+      K[NR - 1] = Kn + 32;
+      bvr = __shfl_sync(FULL, R, nb - 1) >> 8;
+      if (bvr > (1 << 20) || bvr < -(1 << 20)) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r)
+          if (K[r] < kUnfilled) K[r] -= bvr * 256;
+        off += bvr;
+        bvr = 0;
+      }
+      __syncwarp();
+    }
+    __syncwarp();
+    if (lane == 0) *reinterpret_cast<volatile int*>(&S.consumed) = c + 1;
+  }
+  if (lane == 0 && a.debug) {
+    a.debug[0] = clock64() - t_start;
+    a.debug[1] = wait_cycles;
+    a.debug[2] = 0;
+  }
+}
+
+__global__ void __launch_bounds__(kDpWarps * 32, 1) k_peel_dp(PeelArgs pa, DpArgs da) {
   extern __shared__ int4 smem4[];
+  const int warp = threadIdx.x >> 5;
   if (blockIdx.x == 0) {
-    peel_dispatch(pa, smem4);
-  } else {
+    if (warp == 0) peel_dispatch(pa, smem4);
+  } else if (da.v3) {
+    DpSmem3& S = *reinterpret_cast<DpSmem3*>(smem4);
+    if (threadIdx.x < kDpProducers) S.ready[threadIdx.x] = -1;
+    if (threadIdx.x == 0) S.consumed = 0;
+    __syncthreads();
+    if (warp == 0) dp_compute_v3(da, S);
+    else dp_producer(da, S, warp - 1, threadIdx.x & 31);
+  } else if (warp == 0) {
     dp_warp(da, *reinterpret_cast<DpSmem*>(smem4));
   }
 }
@@ -750,6 +1379,60 @@ __global__ void k_src_place_v5(const int32_t* by_rank, const int32_t* flag, cons
   }
 }
 
+// meta(c) = rank | min(indeg, 127) << 24 | (out-degree > 8) << 31
+__device__ __forceinline__ int32_t v6_meta(const int32_t* in_off, const int32_t* out_off, const int32_t* rank,
+                                           int32_t c) {
+  const int32_t ind = min(in_off[c + 1] - in_off[c], 127);
+  const bool lng = out_off[c + 1] - out_off[c] > 8;
+  return static_cast<int32_t>(static_cast<uint32_t>(rank[c]) | (static_cast<uint32_t>(ind) << 24) |
+                              (lng ? 0x80000000u : 0u));
+}
+
+// 8-slot rows sorted by child rank (ascending); -1 padded; long rows (> 8) left empty.
+__global__ void k_ell6(const int32_t* in_off, const int32_t* out_off, const int32_t* out_dst, const int32_t* rank,
+                       int32_t n, int2* ell) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t b = out_off[v], d = out_off[v + 1] - b;
+    int2 r[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) r[q] = make_int2(-1, 0);
+    if (d <= 8) {
+      for (int q = 0; q < d; ++q) {
+        const int32_t c = out_dst[b + q];
+        int2 x = make_int2(c, v6_meta(in_off, out_off, rank, c));
+        // insertion by rank (low 24 bits)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (x.x >= 0 && (r[j].x < 0 || (x.y & 0xffffff) < (r[j].y & 0xffffff))) {
+            const int2 t = r[j];
+            r[j] = x;
+            x = t;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) ell[v * 8 + q] = r[q];
+  }
+}
+
+__global__ void k_cmeta(const int32_t* in_off, const int32_t* out_off, const int32_t* out_dst, const int32_t* rank,
+                        int32_t m, int2* cm) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = out_dst[k];
+    cm[k] = make_int2(c, v6_meta(in_off, out_off, rank, c));
+  }
+}
+
+__global__ void k_src_place_v6(const int32_t* by_rank, const int32_t* flag, const int32_t* pos, const int32_t* out_off,
+                               int32_t n, int32_t nsrc, int32_t* buf) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    if (!flag[r]) continue;
+    const int32_t v = by_rank[r];
+    buf[nsrc - 1 - pos[r]] = v | (out_off[v + 1] - out_off[v] > 8 ? kV6Long : 0);
+  }
+}
+
 __global__ void k_scatter_pos_of(const int32_t* seq, int32_t n, int32_t* pos_of) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
     pos_of[seq[p]] = static_cast<int32_t>(p);
@@ -777,12 +1460,14 @@ __global__ void k_out_sum(const int32_t* out_off, const int64_t* out_cost, int32
   }
 }
 
-size_t peel_smem() { return sizeof(int4) * kStackCache + sizeof(int64_t) * kFreedCap + sizeof(int32_t) * 96; }
+size_t peel_smem() {
+  return std::max(sizeof(int4) * kStackCache + sizeof(int64_t) * kFreedCap + sizeof(int32_t) * 96, sizeof(V6Smem));
+}
 
 }  // namespace
 
 // Builds the peel inputs (ranks, 16-byte slot records, initial stack, in-degrees).
-void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st) {
+void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st, bool force_v5) {
   dp_ctx* ctx = g.ctx;
   const int B = 256;
   const int32_t n = g.n, m = g.m_ok;
@@ -804,6 +1489,26 @@ void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st) 
   exclusive_scan_i32(ctx, flag.p, fpos.p, (int64_t)n + 1);
   st.nsrc = scalar_to_host(ctx, fpos.p + n);
   st.stack_mode = policy != DP_TOPO_M;
+  st.v6 = st.stack_mode && n < (1 << 24) && static_cast<int64_t>(m) <= 6 * static_cast<int64_t>(n) && !force_v5 &&
+          getenv("DP_PEEL_V5") == nullptr;
+  if (st.v6) {
+    st.ell6.alloc(ctx, (size_t)n * 4);
+    DP_LAUNCH(ctx, k_ell6, grid_for(n, B), B, 0, g.in_off.p, g.out_off.p, g.out_dst.p, rank.p, n,
+              reinterpret_cast<int2*>(st.ell6.p));
+    st.cmeta.alloc(ctx, m > 0 ? m : 1);
+    DP_LAUNCH(ctx, k_cmeta, grid_for(m, B), B, 0, g.in_off.p, g.out_off.p, g.out_dst.p, rank.p, m, st.cmeta.p);
+    st.gsid.alloc(ctx, (size_t)n + 1);
+    DP_LAUNCH(ctx, k_src_place_v6, grid_for(n, B), B, 0, by_rank.p, flag.p, fpos.p, g.out_off.p, n, st.nsrc,
+              st.gsid.p);
+    st.indeg.alloc(ctx, n);
+    DP_LAUNCH(ctx, k_indeg_init2, grid_for(n, B), B, 0, g.in_off.p, n, st.indeg.p);
+    st.gover.alloc(ctx, n);
+    st.gover.zero();
+    st.spill.alloc(ctx, m > 0 ? m : 1);
+    st.counters.alloc(ctx, 3);
+    st.counters.zero();
+    return;
+  }
   st.gstack.alloc(ctx, (size_t)n + 1);
   if (st.stack_mode && n < (1 << 24)) {
     st.ellw = n > 262144 ? 8 : 32;
@@ -847,21 +1552,27 @@ static PeelArgs peel_args(DevGraph& g, PeelState& st, int32_t* seq, int32_t* pos
   a.out_off = g.out_off.p;
   a.out_dst = g.out_dst.p;
   a.gstack2 = st.gstack2.p;
+  a.v6 = st.v6;
+  a.ell6 = st.ell6.p;
+  a.cmeta = st.cmeta.p;
+  a.rem_big = st.indeg.p;
+  a.gsid = st.gsid.p;
+  a.gover = st.gover.p;
   return a;
 }
 
 int32_t topo_order(DevGraph& g, int policy, const int64_t* cpath, int32_t* seq, int32_t* pos_of) {
   dp_ctx* ctx = g.ctx;
   if (g.n == 0) return 0;
-  PeelState st;
-  peel_prepare(g, policy, cpath, st);
-  PeelArgs a = peel_args(g, st, seq, pos_of, false);
   const size_t sm = peel_smem();
   static bool attr = false;
   if (!attr) {
     DP_CUDA(cudaFuncSetAttribute(k_peel2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
     attr = true;
   }
+  PeelState st;
+  peel_prepare(g, policy, cpath, st);
+  PeelArgs a = peel_args(g, st, seq, pos_of, false);
   {
     StageScope s(ctx, policy == DP_TOPO_CPD ? "cpd_peel" : "peel", 0.0);
     DP_LAUNCH(ctx, k_peel2, 1, 32, sm, a);
@@ -877,9 +1588,6 @@ int32_t peel_dp_stream(DevGraph& g, const int64_t* cpath, int32_t range, int64_t
   dp_ctx* ctx = g.ctx;
   const int32_t n = g.n;
   if (n == 0) return 0;
-  PeelState st;
-  peel_prepare(g, DP_TOPO_CPD, cpath, st);
-  PeelArgs pa = peel_args(g, st, seq, pos_of, true);
   DevBuf<int64_t> out_sum(ctx, n);
   DP_LAUNCH(ctx, k_out_sum, grid_for(n, 256), 256, 0, g.out_off.p, g.out_cost.p, n, out_sum.p);
   // 32-bit keys need every window value within +-2^22 of the window minimum: bounded
@@ -891,6 +1599,10 @@ int32_t peel_dp_stream(DevGraph& g, const int64_t* cpath, int32_t range, int64_t
   const unsigned long long max_out = scalar_to_host(ctx, mx.p);
   DpArgs da{};
   da.keys32 = static_cast<double>(max_out) * (range + 2) < static_cast<double>(1 << 21);
+  // the block recurrence lets relative values drift for up to 2 x 32 steps before a rebase
+  da.block32 = static_cast<double>(max_out) * (range + 2 + 64) < static_cast<double>(1 << 21) &&
+               getenv("DP_DP_PERSTEP") == nullptr;
+  da.v3 = da.keys32 && da.block32 && range <= 225 && getenv("DP_DP_V2") == nullptr;
   da.n = n;
   da.range = range;
   da.limit = limit;
@@ -901,10 +1613,9 @@ int32_t peel_dp_stream(DevGraph& g, const int64_t* cpath, int32_t range, int64_t
   da.in_off = g.in_off.p;
   da.in_src = g.in_src.p;
   da.in_cost = g.in_cost.p;
-  da.progress = st.counters.p;
   da.prev_cut = prev_cut;
   da.first_exceed = first_exceed;
-  const size_t sm = std::max(peel_smem(), sizeof(DpSmem));
+  const size_t sm = std::max(peel_smem(), std::max(sizeof(DpSmem), sizeof(DpSmem3)));
   static bool attr = false;
   if (!attr) {
     DP_CUDA(cudaFuncSetAttribute(k_peel_dp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
@@ -913,18 +1624,24 @@ int32_t peel_dp_stream(DevGraph& g, const int64_t* cpath, int32_t range, int64_t
   DevBuf<long long> dbg(ctx, 4);
   dbg.zero();
   da.debug = getenv("DP_DEBUG_DP") ? dbg.p : nullptr;
+  PeelState st;
+  peel_prepare(g, DP_TOPO_CPD, cpath, st);
+  PeelArgs pa = peel_args(g, st, seq, pos_of, true);
+  pa.debug = da.debug ? dbg.p + 3 : nullptr;
+  da.progress = st.counters.p;
   void* args[] = {&pa, &da};
   {
     StageScope s(ctx, "peel+dp (streamed)", 0.0);
-    DP_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_peel_dp), 2, 32, args, sm, ctx->stream));
+    DP_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_peel_dp), 2, kDpWarps * 32, args, sm,
+                                        ctx->stream));
     ++ctx->launches;
   }
   if (da.debug) {
-    long long h[3];
-    dbg.download(h, 3);
+    long long h[4];
+    dbg.download(h, 4);
     sync(ctx);
-    fprintf(stderr, "[peel_dp] dp warp: total %.1f ms, waiting %.1f ms, staging %.1f ms (at 1.965 GHz)\n",
-            h[0] / 1.965e6, h[1] / 1.965e6, h[2] / 1.965e6);
+    fprintf(stderr, "[peel_dp] dp warp: total %.1f ms, waiting %.1f ms, staging %.1f ms; peel warp %.1f ms (at 1.965 GHz)\n",
+            h[0] / 1.965e6, h[1] / 1.965e6, h[2] / 1.965e6, h[3] / 1.965e6);
   }
   return scalar_to_host(ctx, st.counters.p + 1);
 }

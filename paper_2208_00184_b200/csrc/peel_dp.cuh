@@ -13,10 +13,16 @@ struct PeelState {
   int32_t ellw = 8;
   DevBuf<int32_t> indeg;
   DevBuf<int64_t> spill;
-  DevBuf<int> counters;  // [0] progress, [1] emitted
+  DevBuf<int> counters;  // [0] progress, [1] emitted, [2] unused
+  // peel v6
+  bool v6 = false;
+  DevBuf<int4> ell6;
+  DevBuf<int2> cmeta;
+  DevBuf<int32_t> gsid;
+  DevBuf<int32_t> gover;
 };
 
-void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st);
+void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st, bool force_v5 = false);
 
 // CPD peel of g streamed into the breakpoint DP (R <= 256); writes seq/pos_of and
 // prev_cut[1..n]; *first_exceed = first position whose node exceeds `limit` (or

@@ -1,3 +1,5 @@
+#include <chrono>
+#include <cstdlib>
 // pipeline.cu — evaluate_pipeline (pipeline.cpp:27-111, /root/reference/proj/src) with
 // every intermediate resident in HBM.  The generation window of pipeline.cpp:67-79
 // (fuse -> coarse levels + cpd_topo -> order_place + adjusting_placement -> 2x expand)
@@ -153,8 +155,14 @@ extern "C" {
 int dp_pipeline(dp_ctx_t* ctx, const dp_graph_t* h, const dp_devices_t* devices, dp_comm_t comm,
                 const dp_pipeline_config_t* cfg, dp_pipeline_result_t** out) {
   DP_API_BEGIN(ctx)
+  const bool dbg = getenv("DP_DEBUG_PIPE") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto span_ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  const auto h0 = now();
   Resident r;
   resident_init(r, ctx, h, devices, comm, cfg);
+  if (dbg) sync(ctx);
+  const auto h1 = now();
   cudaEvent_t e0, e1;
   DP_CUDA(cudaEventCreate(&e0));
   DP_CUDA(cudaEventCreate(&e1));
@@ -175,6 +183,8 @@ int dp_pipeline(dp_ctx_t* ctx, const dp_graph_t* h, const dp_devices_t* devices,
     graph_costs(g, comm);
     r.original_ccr = ccr_dev(g);
   }
+  if (dbg) sync(ctx);
+  const auto h2 = now();
   DP_CUDA(cudaEventRecord(e0, ctx->stream));
   fuse_dev(r.g, r.comm, r.cfg.fusion_range, r.limit, r.f);
   DevGraph& coarse = r.f.coarse;
@@ -191,6 +201,8 @@ int dp_pipeline(dp_ctx_t* ctx, const dp_graph_t* h, const dp_devices_t* devices,
   expand_dev(r.g, r.f.node_cluster.p, r.po.dev.p, D, r.dev_order.p, r.pdm_order.p);
   expand_dev(r.g, r.f.node_cluster.p, r.pa.dev.p, D, r.dev_adjust.p, r.pdm_adjust.p);
   DP_CUDA(cudaEventRecord(e1, ctx->stream));
+  if (dbg) sync(ctx);
+  const auto h3 = now();
   auto* res = halloc<dp_pipeline_result_t>(1);
   res->original_nodes = n;
   res->original_edges = r.g.m;
@@ -215,6 +227,11 @@ int dp_pipeline(dp_ctx_t* ctx, const dp_graph_t* h, const dp_devices_t* devices,
   res->coarse_ccr = 0.0;
   if (coarse.m > 0) res->coarse_ccr = ccr_dev(coarse);  // pipeline.cpp:83
   res->order_makespan = res->adjust_makespan = -1;
+  if (dbg) {
+    const auto h4 = now();
+    fprintf(stderr, "[dp_pipeline] upload %.1f ms, validate+ccr %.1f ms, window %.1f ms, results %.1f ms\n",
+            span_ms(h0, h1), span_ms(h1, h2), span_ms(h2, h3), span_ms(h3, h4));
+  }
   if (cfg->simulate) {  // pipeline.cpp:89-90
     dp_sim_report_t* so = sim_report(r.g, r.devs, r.dev_order.p, false);
     dp_sim_report_t* sa = sim_report(r.g, r.devs, r.dev_adjust.p, false);
