@@ -30,13 +30,16 @@ struct StageResolver {
     if ((ctx)->timing) ::dpb::stage_reset(ctx);
 
 #define DP_API_END                                                           \
+    if (!dp_stage_resolver_.ctx->pending.empty()) ::dpb::sync(dp_stage_resolver_.ctx); \
     dp_stage_resolver_.ok = true;                                            \
   }                                                                          \
   catch (const ::dpb::DpFail& f_) {                                          \
+    if (dp_stage_resolver_.ctx) ::dpb::discard_pending(dp_stage_resolver_.ctx); \
     ::dpb::set_last_error(f_.code, f_.msg);                                  \
     return f_.code;                                                          \
   }                                                                          \
   catch (const std::bad_alloc&) {                                            \
+    if (dp_stage_resolver_.ctx) ::dpb::discard_pending(dp_stage_resolver_.ctx); \
     ::dpb::set_last_error(DP_E_OUT_OF_MEMORY, "host allocation failed");     \
     return DP_E_OUT_OF_MEMORY;                                               \
   }                                                                          \

@@ -52,6 +52,16 @@ struct dp_ctx {
   std::vector<dpb::Stage> event_pool;  // recycled events
   size_t event_next = 0;
   std::vector<double> stage_ms;        // resolved durations
+  // Device->host results are staged through a pinned arena and copied to their
+  // destination at the next dpb::sync: a D2H copy into pageable memory would block the
+  // calling thread until the stream drains (and serialise concurrent contexts).
+  struct PendingCopy {
+    void* dst;
+    size_t off, bytes;
+  };
+  char* pin = nullptr;
+  size_t pin_cap = 0, pin_off = 0;
+  std::vector<PendingCopy> pending;
 };
 
 namespace dpb {
@@ -143,29 +153,39 @@ struct DevBuf {
   void upload(const T* host, size_t count) {
     if (count) DP_CUDA(cudaMemcpyAsync(p, host, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
   }
-  void download(T* host, size_t count) const {
-    if (count) DP_CUDA(cudaMemcpyAsync(host, p, count * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
-  }
+  void download(T* host, size_t count) const;
   T* get() const { return p; }
 };
+
+// Stream-ordered D2H copy of `bytes` into `host` through the pinned arena; `host` is
+// valid after the next sync(ctx).
+void download_bytes(dp_ctx* ctx, void* host, const void* dev, size_t bytes);
+// Waits for the context stream and completes the pending D2H copies.
+void sync(dp_ctx* ctx);
+// Drops pending copies (error paths: their destinations may be gone).
+void discard_pending(dp_ctx* ctx);
+
+template <typename T>
+void DevBuf<T>::download(T* host, size_t count) const {
+  if (count) download_bytes(ctx, host, p, count * sizeof(T));
+}
 
 template <typename T>
 inline std::vector<T> to_host(dp_ctx* ctx, const T* dev, size_t count) {
   std::vector<T> h(count);
   if (count) {
-    DP_CUDA(cudaMemcpyAsync(h.data(), dev, count * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
-    DP_CUDA(cudaStreamSynchronize(ctx->stream));
+    download_bytes(ctx, h.data(), dev, count * sizeof(T));
+    sync(ctx);
   }
   return h;
 }
 template <typename T>
 inline T scalar_to_host(dp_ctx* ctx, const T* dev) {
   T v{};
-  DP_CUDA(cudaMemcpyAsync(&v, dev, sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
-  DP_CUDA(cudaStreamSynchronize(ctx->stream));
+  download_bytes(ctx, &v, dev, sizeof(T));
+  sync(ctx);
   return v;
 }
-inline void sync(dp_ctx* ctx) { DP_CUDA(cudaStreamSynchronize(ctx->stream)); }
 
 // ------------------------------------------------------------------ device helpers
 constexpr int64_t kNever = INT64_MAX;

@@ -85,9 +85,39 @@ void stage_end(dp_ctx* ctx, size_t idx) {
   DP_CUDA(cudaEventRecord(ctx->stages[idx].b, ctx->stream));
 }
 
+void download_bytes(dp_ctx* ctx, void* host, const void* dev, size_t bytes) {
+  if (!bytes) return;
+  const size_t need = (bytes + 255) & ~static_cast<size_t>(255);
+  if (ctx->pin_off + need > ctx->pin_cap) {
+    sync(ctx);  // completes (and empties) the pending copies
+    if (need > ctx->pin_cap) {
+      if (ctx->pin) cudaFreeHost(ctx->pin);
+      ctx->pin = nullptr;
+      ctx->pin_cap = 0;
+      const size_t cap = std::max<size_t>(need, std::max<size_t>(1 << 20, 2 * ctx->pin_cap));
+      DP_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->pin), cap, cudaHostAllocDefault));
+      ctx->pin_cap = cap;
+    }
+  }
+  DP_CUDA(cudaMemcpyAsync(ctx->pin + ctx->pin_off, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->pending.push_back({host, ctx->pin_off, bytes});
+  ctx->pin_off += need;
+}
+
+void sync(dp_ctx* ctx) {
+  DP_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (const auto& c : ctx->pending) std::memcpy(c.dst, ctx->pin + c.off, c.bytes);
+  ctx->pending.clear();
+  ctx->pin_off = 0;
+}
+
+void discard_pending(dp_ctx* ctx) {
+  ctx->pending.clear();
+}
+
 void stage_resolve(dp_ctx* ctx) {
   ctx->stage_ms.clear();
-  DP_CUDA(cudaStreamSynchronize(ctx->stream));
+  sync(ctx);
   for (auto& s : ctx->stages) {
     float ms = 0;
     DP_CUDA(cudaEventElapsedTime(&ms, s.a, s.b));
@@ -139,6 +169,8 @@ void dp_ctx_destroy(dp_ctx_t* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  ctx->pending.clear();
+  if (ctx->pin) cudaFreeHost(ctx->pin);
   for (auto& s : ctx->stages) ctx->event_pool.push_back(s);
   for (auto& s : ctx->event_pool) {
     cudaEventDestroy(s.a);
@@ -154,6 +186,11 @@ int dp_ctx_set_stream(dp_ctx_t* ctx, void* stream) {
 
 int dp_ctx_synchronize(dp_ctx_t* ctx) {
   cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e == cudaSuccess) {
+    for (const auto& c : ctx->pending) std::memcpy(c.dst, ctx->pin + c.off, c.bytes);
+    ctx->pending.clear();
+    ctx->pin_off = 0;
+  }
   if (e != cudaSuccess) {
     set_last_error(DP_E_CUDA, cudaGetErrorString(e));
     return DP_E_CUDA;

@@ -422,18 +422,16 @@ __device__ __forceinline__ uint32_t v6_bucket(int32_t c) {
 __device__ __forceinline__ bool v6_dec(V6Smem& S, int32_t* gover, int32_t c, int code) {
   const uint32_t b = v6_bucket(c), uc = static_cast<uint32_t>(c);
   const uint2 w = *reinterpret_cast<const uint2*>(&S.ht[2 * b]);
-  if ((w.x >> 7) == uc) {
-    const uint32_t r = (w.x & 127u) - 1;
-    S.ht[2 * b] = r ? w.x - 1 : kV6Empty;
-    return r == 0;
-  }
-  if ((w.y >> 7) == uc) {
-    const uint32_t r = (w.y & 127u) - 1;
-    S.ht[2 * b + 1] = r ? w.y - 1 : kV6Empty;
-    return r == 0;
-  }
   const uint32_t sh = (b & 1u) * 16;
-  if ((S.ovc[b >> 1] >> sh) & 0xffffu) {
+  const uint32_t ov = S.ovc[b >> 1];
+  const bool h0 = (w.x >> 7) == uc, h1 = (w.y >> 7) == uc;
+  if (h0 | h1) {
+    const uint32_t e = h0 ? w.x : w.y;
+    const bool fr = (e & 127u) == 1u;
+    S.ht[2 * b + (h0 ? 0 : 1)] = fr ? kV6Empty : e - 1;
+    return fr;
+  }
+  if ((ov >> sh) & 0xffffu) {
     const int32_t g = gover[c];
     if (g > 0) {
       gover[c] = g - 1;
@@ -485,17 +483,19 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem& S) {
     }
     const int32_t slot = top & (SC - 1);
     const int32_t sv = S.sid[slot];
+    const int2* rowp = reinterpret_cast<const int2*>(S.row[slot]);
+    const int2 cq = rowp[lane >> 2];  // child whose row this lane fetches
+    const int2 my = rowp[lane & 7];   // child this lane decrements (lanes 0..7)
     --top;
     const int32_t v = sv & 0xffffff;
     if (lane == 0) {
-      S.seqbuf[p & 31] = v;
+      a.seq[p] = v;
       a.pos_of[v] = p;
     }
     ++p;
-    if ((p & 31) == 0) {
+    if ((p & 255) == 0) {
       __syncwarp();
-      a.seq[p - 32 + lane] = S.seqbuf[lane];
-      if ((p & 255) == 0 && lane == 0) v6_publish(a, p);
+      if (lane == 0) v6_publish(a, p);
     }
     if (sv & kV6Long) {
       // ---- CSR path: rows longer than 8
@@ -555,12 +555,9 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem& S) {
       continue;
     }
     // ---- 8-slot row on chip (slots sorted by rank)
-    const int2* rowp = reinterpret_cast<const int2*>(S.row[slot]);
     const int q = lane >> 2;
-    const int2 cq = rowp[q];
     int4 crow = make_int4(-1, 0, -1, 0);
     if (cq.x >= 0) crow = a.ell6[static_cast<int64_t>(cq.x) * 4 + (lane & 3)];
-    const int2 my = rowp[lane & 7];
     bool fr = false;
     if (lane < 8 && my.x >= 0) {
       const int code = (my.y >> 24) & 127;
@@ -587,8 +584,6 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem& S) {
     }
     __syncwarp();
   }
-  __syncwarp();
-  if (lane < (p & 31)) a.seq[(p & ~31) + lane] = S.seqbuf[lane];
   __syncwarp();
   if (lane == 0) {
     *a.emitted = p;

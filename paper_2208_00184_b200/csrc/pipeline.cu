@@ -288,6 +288,7 @@ void dp_resident_destroy(dp_resident_t* r) {
   if (!r) return;
   cudaSetDevice(r->ctx->device);
   cudaStreamSynchronize(r->ctx->stream);
+  r->ctx->pending.clear();
   delete r;
 }
 
