@@ -267,6 +267,12 @@ def ours(args):
     step()
     stages = stage_times(lib, ctx)
     lib.dp_ctx_enable_stage_timing(ctx, 0)
+    # the fine graph's levels come first; the coarse graph's (pipeline.cpp:70) second
+    seen = set()
+    for i, (nm, ms_, by) in enumerate(stages):
+        if nm in seen:
+            stages[i] = ("coarse " + nm, ms_, by)
+        seen.add(nm)
     if args.stages and rank == 0:
         for nm, ms, by in stages:
             print(f"stage {nm:18s} {ms:10.3f} ms  {by / 1e6:10.1f} MB", file=sys.stderr)

@@ -87,7 +87,8 @@ void prepare_graph(DevGraph& g, dp_ctx* ctx, const dp_graph_t* h) {
 }
 
 // compute_levels (graph.cpp:217-269) on a validated device graph; cycle -> error.
-void levels_dev(DevGraph& g, dp_comm_t comm, DevBuf<int64_t>& t, DevBuf<int64_t>& b, DevBuf<int64_t>& c) {
+void levels_dev(DevGraph& g, dp_comm_t comm, DevBuf<int64_t>& t, DevBuf<int64_t>& b, DevBuf<int64_t>& c,
+                bool chainlike) {
   dp_ctx* ctx = g.ctx;
   graph_costs(g, comm);
   t.alloc(ctx, g.n > 0 ? g.n : 1);
@@ -95,7 +96,7 @@ void levels_dev(DevGraph& g, dp_comm_t comm, DevBuf<int64_t>& t, DevBuf<int64_t>
   c.alloc(ctx, g.n > 0 ? g.n : 1);
   {
     StageScope st(ctx, "levels", 40.0 * g.m_ok + 48.0 * g.n);
-    if (!graph_levels_indexorder(g, t.p, b.p)) graph_kahn(g, t.p, b.p, nullptr);
+    if (!graph_levels_indexorder(g, t.p, b.p, chainlike)) graph_kahn(g, t.p, b.p, nullptr);
   }
   if (g.processed != g.n) {
     std::vector<int64_t> wit = graph_cycle_witness(g);

@@ -20,7 +20,8 @@
 
 namespace dpb {
 
-void levels_dev(DevGraph& g, dp_comm_t comm, DevBuf<int64_t>& t, DevBuf<int64_t>& b, DevBuf<int64_t>& c);
+void levels_dev(DevGraph& g, dp_comm_t comm, DevBuf<int64_t>& t, DevBuf<int64_t>& b, DevBuf<int64_t>& c,
+                bool chainlike);
 
 namespace {
 
@@ -671,7 +672,7 @@ void fuse_dev(DevGraph& g, dp_comm_t comm, int32_t range, int64_t limit, FuseOut
     }
   }
   DevBuf<int64_t> t, b, c;
-  levels_dev(work, comm, t, b, c);
+  levels_dev(work, comm, t, b, c, false);
   const int32_t n = work.n;
   out.seq.alloc(ctx, n > 0 ? n : 1);
   out.pos_of.alloc(ctx, n > 0 ? n : 1);

@@ -329,11 +329,14 @@ __device__ __forceinline__ int64_t warp_max_nonneg(int64_t x) {
 
 // forward: tlevel[v] = max(0, max_{u->v} f[u] + c), f[u] = tlevel[u] + w[u]
 // backward (rev): blevel[v] = w[v] + max(0, max_{v->s} blevel[s] + c)
+// Values of the last kSeqMaxN sweep positions live in a shared-memory ring; older ones
+// (graphs larger than the ring) are read from `gval` in HBM/L2 with ld.global.cg (the
+// sweep writes them there too), so any n works and chain-like graphs hit the ring.
 __global__ void __launch_bounds__(1024) k_levels_seq(int32_t n, const int32_t* off, const int32_t* nbr,
                                                      const int64_t* cost, const int64_t* w, int64_t* out,
-                                                     bool rev) {
+                                                     bool rev, int64_t* gval) {
   extern __shared__ int64_t sm64[];
-  int64_t* val = sm64;                                         // [n]: f (fwd) or blevel (bwd)
+  int64_t* val = sm64;                                         // ring [kSeqMaxN]: f (fwd) or blevel (bwd)
   int64_t* ec = val + kSeqMaxN;                                // [kSeqTile]
   int64_t* wt = ec + kSeqTile;                                 // [kSeqTileN]
   int32_t* en = reinterpret_cast<int32_t*>(wt + kSeqTileN);    // [kSeqTile]
@@ -383,13 +386,16 @@ __global__ void __launch_bounds__(1024) k_levels_seq(int32_t n, const int32_t* o
         for (int32_t k = b + lane; k < e; k += 32) {
           const int32_t u = fits ? en[k - e0] : nbr[k];
           const int64_t c = fits ? ec[k - e0] : cost[k];
-          mx = max(mx, val[u] + c);
+          const int32_t pu = rev ? n - 1 - u : u;  // sweep position of u (< i)
+          const int64_t fu = i - pu <= kSeqMaxN ? val[pu % kSeqMaxN] : __ldcg(gval + u);
+          mx = max(mx, fu + c);
         }
         mx = warp_max_nonneg(mx);
         if (lane == 0) {
-          const int64_t wv = wt[i - done];
-          val[v] = rev ? mx + wv : mx + wv;  // f[v] = tlevel + w (fwd); blevel (bwd)
-          out[v] = rev ? mx + wv : mx;
+          const int64_t vv = mx + wt[i - done];  // f[v] = tlevel + w (fwd); blevel (bwd)
+          val[i % kSeqMaxN] = vv;
+          if (gval) __stcg(gval + v, vv);
+          out[v] = rev ? vv : mx;
         }
         __syncwarp();
       }
@@ -690,10 +696,13 @@ void graph_costs(DevGraph& g, dp_comm_t comm) {
 
 // Levels by an index-order sweep when the node index order is topological and the graph
 // is small enough for on-chip values; returns false otherwise (caller uses graph_kahn).
-bool graph_levels_indexorder(DevGraph& g, int64_t* tlevel, int64_t* blevel) {
+bool graph_levels_indexorder(DevGraph& g, int64_t* tlevel, int64_t* blevel, bool chainlike) {
   dp_ctx* ctx = g.ctx;
   const int32_t n = g.n;
-  if (n == 0 || n > kSeqMaxN || getenv("DP_LEVELS_KAHN")) return false;
+  if (n == 0 || getenv("DP_LEVELS_KAHN")) return false;
+  // the sweep pays one warp step per node: taken for small graphs, and for graphs the
+  // caller knows to be chain-like (the coarse graph of fuse) at any size
+  if (n > kSeqMaxN && !chainlike) return false;
   DevBuf<int> ok(ctx, 1);
   int one = 1;
   ok.upload(&one, 1);
@@ -705,8 +714,10 @@ bool graph_levels_indexorder(DevGraph& g, int64_t* tlevel, int64_t* blevel) {
     DP_CUDA(cudaFuncSetAttribute(k_levels_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
     attr = true;
   }
-  DP_LAUNCH(ctx, k_levels_seq, 1, 1024, sm, n, g.in_off.p, g.in_src.p, g.in_cost.p, g.w.p, tlevel, false);
-  DP_LAUNCH(ctx, k_levels_seq, 1, 1024, sm, n, g.out_off.p, g.out_dst.p, g.out_cost.p, g.w.p, blevel, true);
+  DevBuf<int64_t> gval;
+  if (n > kSeqMaxN) gval.alloc(ctx, n);
+  DP_LAUNCH(ctx, k_levels_seq, 1, 1024, sm, n, g.in_off.p, g.in_src.p, g.in_cost.p, g.w.p, tlevel, false, gval.p);
+  DP_LAUNCH(ctx, k_levels_seq, 1, 1024, sm, n, g.out_off.p, g.out_dst.p, g.out_cost.p, g.w.p, blevel, true, gval.p);
   g.processed = n;
   return true;
 }

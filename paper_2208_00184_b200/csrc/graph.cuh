@@ -63,7 +63,7 @@ void graph_costs(DevGraph& g, dp_comm_t comm);
 Validation graph_validate(DevGraph& g, const dp_graph_t* h, bool all, bool cycle_check = true);
 // Kahn frontier (level-synchronous, persistent cooperative kernel): fills order /
 // level_off / processed, and when requested tlevel / blevel (graph.cpp:228-261).
-bool graph_levels_indexorder(DevGraph& g, int64_t* tlevel, int64_t* blevel);
+bool graph_levels_indexorder(DevGraph& g, int64_t* tlevel, int64_t* blevel, bool chainlike);
 void graph_kahn(DevGraph& g, int64_t* tlevel, int64_t* blevel, int32_t* level_of);
 // CycleDetected witness after an incomplete Kahn pass (graph.cpp:71-94).
 std::vector<int64_t> graph_cycle_witness(DevGraph& g);

@@ -474,7 +474,10 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem& S) {
   int32_t base = max(0, a.nsrc - SC / 2);
   v6_fill(a, S, base, top, lane);
   __syncwarp();
-  int32_t p = 0;
+  int32_t p = 0, held = 0;
+  int32_t* const seq = a.seq;
+  int32_t* const pos_of = a.pos_of;
+  const int4* const ell6 = a.ell6;
   while (top >= 0) {
     if (top < base) {
       base = max(0, top + 1 - SC / 2);
@@ -488,14 +491,15 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem& S) {
     const int2 my = rowp[lane & 7];   // child this lane decrements (lanes 0..7)
     --top;
     const int32_t v = sv & 0xffffff;
-    if (lane == 0) {
-      a.seq[p] = v;
-      a.pos_of[v] = p;
-    }
+    if (lane == (p & 31)) held = v;  // lane k holds the node of position 32i + k
     ++p;
-    if ((p & 255) == 0) {
-      __syncwarp();
-      if (lane == 0) v6_publish(a, p);
+    if ((p & 31) == 0) {
+      seq[p - 32 + lane] = held;
+      pos_of[held] = p - 32 + lane;
+      if ((p & 255) == 0) {
+        __syncwarp();
+        if (lane == 0) v6_publish(a, p);
+      }
     }
     if (sv & kV6Long) {
       // ---- CSR path: rows longer than 8
@@ -557,13 +561,34 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem& S) {
     // ---- 8-slot row on chip (slots sorted by rank)
     const int q = lane >> 2;
     int4 crow = make_int4(-1, 0, -1, 0);
-    if (cq.x >= 0) crow = a.ell6[static_cast<int64_t>(cq.x) * 4 + (lane & 3)];
+    if (cq.x >= 0) crow = ell6[static_cast<int64_t>(cq.x) * 4 + (lane & 3)];
     bool fr = false;
     if (lane < 8 && my.x >= 0) {
-      const int code = (my.y >> 24) & 127;
-      if (code == 1) fr = true;
-      else if (code == 127) fr = atomicSub(a.rem_big + my.x, 1) == 1;
-      else fr = v6_dec(S, a.gover, my.x, code);
+      // branch-light table step: one bucket load; remaining = table value on a hit, the
+      // initial in-degree on a first touch (code == 1 frees without touching the table)
+      const uint32_t code = (static_cast<uint32_t>(my.y) >> 24) & 127u, uc = static_cast<uint32_t>(my.x);
+      const uint32_t b = v6_bucket(my.x), sh = (b & 1u) * 16;
+      const uint2 w = *reinterpret_cast<const uint2*>(&S.ht[2 * b]);
+      const uint32_t ov = (S.ovc[b >> 1] >> sh) & 0xffffu;
+      const bool h0 = (w.x >> 7) == uc, h1 = (w.y >> 7) == uc, hit = h0 | h1;
+      const uint32_t e = h0 ? w.x : w.y;
+      if (code == 127u || (!hit && ov != 0u)) {
+        fr = code == 127u ? atomicSub(a.rem_big + my.x, 1) == 1 : v6_dec(S, a.gover, my.x, static_cast<int>(code));
+      } else {
+        const uint32_t rem = hit ? (e & 127u) : code;
+        fr = rem == 1u;
+        if (hit) {
+          S.ht[2 * b + (h0 ? 0 : 1)] = fr ? kV6Empty : e - 1;
+        } else if (!fr) {  // first touch: insert (ways taken by concurrent lanes -> spill)
+          const uint32_t nv = (uc << 7) | (code - 1);
+          bool ok = w.x == kV6Empty && atomicCAS(&S.ht[2 * b], kV6Empty, nv) == kV6Empty;
+          if (!ok) ok = w.y == kV6Empty && atomicCAS(&S.ht[2 * b + 1], kV6Empty, nv) == kV6Empty;
+          if (!ok) {
+            a.gover[my.x] = static_cast<int32_t>(code - 1);
+            atomicAdd(&S.ovc[b >> 1], 1u << sh);
+          }
+        }
+      }
     }
     const unsigned m = __ballot_sync(FULL, fr);
     if (m) {
@@ -576,13 +601,18 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem& S) {
       // pushed in descending rank: slot k lands above every freed slot of higher rank
       if ((m >> q) & 1u) {
         S.row[(top + 1 + __popc(m >> q >> 1)) & (SC - 1)][lane & 3] = crow;
-        if (crow.x >= 0) prefetch_l2(a.ell6 + static_cast<int64_t>(crow.x) * 4);
-        if (crow.z >= 0) prefetch_l2(a.ell6 + static_cast<int64_t>(crow.z) * 4);
+        if (crow.x >= 0) prefetch_l2(ell6 + static_cast<int64_t>(crow.x) * 4);
+        if (crow.z >= 0) prefetch_l2(ell6 + static_cast<int64_t>(crow.z) * 4);
       }
       if (fr) S.sid[(top + 1 + __popc(m >> lane >> 1)) & (SC - 1)] = my.x | (my.y < 0 ? kV6Long : 0);
       top += nf;
     }
     __syncwarp();
+  }
+  __syncwarp();
+  if (lane < (p & 31)) {
+    seq[(p & ~31) + lane] = held;
+    pos_of[held] = (p & ~31) + lane;
   }
   __syncwarp();
   if (lane == 0) {
@@ -1033,7 +1063,7 @@ struct DpBuf {
   int32_t off[kCh + 1];   // all in-edges of position t: [off[t], off[t+1])
   int32_t off2[kCh + 1];  // in-window in-edges of position t in e2
   int32_t cnt2[kCh];
-  int2 e2[kE2Cap];        // {source position, cost << 8}, sources >= block start - 224
+  int2 e2[kE2Cap + 2];    // {source position, cost << 8}, sources >= block start - 224
   int32_t ioff[kCh];
   int64_t lp[kLpMax];
   int32_t node[kCh];
@@ -1222,8 +1252,16 @@ __device__ void dp_compute_v3(const DpArgs& a, DpSmem3& S) {
         const int32_t t = tb + u;
         if (lane == u) Kn = (u == 0 ? bvr * 256 : 0) + 31 - u;
         if (staged) {
+          // most steps have at most two in-window in-edges: apply two unconditionally
+          // (masked to zero past the step's range), loop over the rest
           const int32_t eb = B.off2[t], ee = B.off2[t + 1];
-          for (int32_t e = eb; e < ee; ++e) {
+          const int2 x0 = B.e2[eb], x1 = B.e2[eb + 1];
+          const int32_t s0 = eb < ee ? x0.y : 0, s1 = eb + 1 < ee ? x1.y : 0;
+          const int32_t r0 = (x0.x + c0) >> 5, r1 = (x1.x + c0) >> 5;
+#pragma unroll
+          for (int r = 0; r < NR; ++r) K[r] -= (r <= r0 ? s0 : 0) + (r <= r1 ? s1 : 0);
+          Kn -= (x0.x + kn_lim >= 0 ? s0 : 0) + (x1.x + kn_lim >= 0 ? s1 : 0);
+          for (int32_t e = eb + 2; e < ee; ++e) {
             const int2 x = B.e2[e];
             const int32_t rmax = (x.x + c0) >> 5;
 #pragma unroll

@@ -91,7 +91,7 @@ void resident_generate(Resident& r, bool with_ccr) {
   if (with_ccr) r.original_ccr = ccr_dev(g);
   fuse_dev(g, r.comm, r.cfg.fusion_range, r.limit, r.f);
   DevGraph& coarse = r.f.coarse;
-  levels_dev(coarse, r.comm, r.ct, r.cb, r.cc);
+  levels_dev(coarse, r.comm, r.ct, r.cb, r.cc, true);  // clusters are runs of a topological order
   const int32_t k = coarse.n;
   r.cseq.alloc(ctx, k > 0 ? k : 1);
   r.cpos.alloc(ctx, k > 0 ? k : 1);
@@ -188,7 +188,7 @@ int dp_pipeline(dp_ctx_t* ctx, const dp_graph_t* h, const dp_devices_t* devices,
   DP_CUDA(cudaEventRecord(e0, ctx->stream));
   fuse_dev(r.g, r.comm, r.cfg.fusion_range, r.limit, r.f);
   DevGraph& coarse = r.f.coarse;
-  levels_dev(coarse, r.comm, r.ct, r.cb, r.cc);
+  levels_dev(coarse, r.comm, r.ct, r.cb, r.cc, true);  // clusters are runs of a topological order
   const int32_t k = coarse.n, n = r.g.n, D = r.devs.D;
   r.cseq.alloc(ctx, k > 0 ? k : 1);
   r.cpos.alloc(ctx, k > 0 ? k : 1);

@@ -1,0 +1,116 @@
+"""GPU parity for the special paths of the sequential kernels (peel_dp.cu, graph.cu):
+each case is built to force one code path and is compared bit-exactly with the oracle
+restatement (oracle/dp_oracle.c).
+
+  peel v6        in-degree >= 127 (global counters), out-degree > 8 (CSR rows), full
+                 hash buckets (global spill counters), DFS as well as CPD ranks
+  streamed DP    v3 (R <= 225), 32-step blocks (226..256), per-step 32-bit keys (cost
+                 bound), 64-bit keys (large costs), R = 1 / 32 / 33 block edges
+  levels         index-order sweep (n <= 12288, index order topological) vs the Kahn
+                 frontier (shuffled ids, n just above the sweep limit)
+"""
+import numpy as np
+import pytest
+
+from compare import same, same_graph, same_map
+from graphs import layered, shuffled
+from paper_2208_00184_b200._abi import Graph
+
+pytestmark = pytest.mark.gpu
+
+GEN = (0.001, 10.0)
+
+
+def _fanin_hub(seed=5, hubs=3, preds=200, n=2000):
+    """Nodes with in-degree `preds` (>= 127) among an otherwise layered DAG."""
+    rng = np.random.default_rng(seed)
+    g = layered(seed, n, 40)
+    src, dst = list(g.edge_src), list(g.edge_dst)
+    for h in range(hubs):
+        v = n - 1 - h
+        layer_lo = (v // 40 - 1) * 40
+        cand = np.setdiff1d(np.arange(0, layer_lo), np.array(src)[np.array(dst) == v])
+        for u in rng.choice(cand, preds, replace=False):
+            src.append(int(u))
+            dst.append(v)
+    o = np.lexsort((dst, src))
+    s, d = np.array(src)[o], np.array(dst)[o]
+    return Graph(g.node_id, g.compute_us, g.memory_bytes, s, d, rng.integers(1 << 15, 3 << 15, len(s)))
+
+
+def _orders(gpu, oracle, g):
+    t, b, c = oracle.compute_levels(g, GEN)
+    same(gpu.cpd_topo(g, c), oracle.cpd_topo(g, c), "cpd")
+    same(gpu.dfs_topo(g), oracle.dfs_topo(g), "dfs")
+    a = gpu.compute_levels(g, GEN)
+    for x, y, nm in zip(a, (t, b, c), "tbc"):
+        same(x, y, nm)
+
+
+def test_peel_high_indegree(gpu, oracle):
+    _orders(gpu, oracle, _fanin_hub())
+
+
+def test_peel_long_rows(gpu, oracle):
+    # fan-out up to 30 from the previous layer: many rows longer than 8
+    g = layered(9, 6000, 60, fan_lo=6, fan_hi=30)
+    _orders(gpu, oracle, g)
+
+
+def test_peel_bucket_spill(gpu, oracle):
+    # a 40k-wide layer keeps tens of thousands of nodes open: buckets overflow to HBM
+    g = layered(13, 120000, 40000, fan_lo=2, fan_hi=5)
+    _orders(gpu, oracle, g)
+
+
+@pytest.mark.parametrize("r", [1, 2, 31, 32, 33, 200, 224, 225, 226, 256])
+def test_streamed_dp_ranges(gpu, oracle, r):
+    g = layered(17, 12000, 48)
+    total = int(g.memory_bytes.sum())
+    for limit in (total // 4, total // 300):
+        ca, ma = gpu.fuse(g, GEN, r, limit)
+        cb, mb = oracle.fuse(g, GEN, r, limit)
+        same_graph(ca, cb, f"r{r}")
+        same_map(ma, mb, f"r{r}")
+
+
+@pytest.mark.parametrize("scale", [1 << 20, 1 << 26, 1 << 40])
+def test_streamed_dp_cost_widths(gpu, oracle, scale):
+    """Costs sized to select the per-step 32-bit path (block bound fails) and the 64-bit
+    path (32-bit keys cannot hold the window)."""
+    g = layered(23, 6000, 32, nbytes=(scale, 2 * scale))
+    total = int(g.memory_bytes.sum())
+    for r in (20, 200):
+        ca, ma = gpu.fuse(g, GEN, r, total // 6)
+        cb, mb = oracle.fuse(g, GEN, r, total // 6)
+        same_graph(ca, cb, f"s{scale} r{r}")
+        same_map(ma, mb, f"s{scale} r{r}")
+
+
+@pytest.mark.parametrize("n", [12287, 12288, 12289])
+def test_levels_indexorder_limit(gpu, oracle, n):
+    g = layered(29, n, 3, fan_lo=1, fan_hi=3)
+    a = gpu.compute_levels(g, GEN)
+    b = oracle.compute_levels(g, GEN)
+    for x, y, nm in zip(a, b, "tbc"):
+        same(x, y, nm)
+    h = shuffled(g, 3, relabel=True)  # index order no longer topological: Kahn path
+    a = gpu.compute_levels(h, GEN)
+    b = oracle.compute_levels(h, GEN)
+    for x, y, nm in zip(a, b, "tbc"):
+        same(x, y, nm)
+
+
+def test_levels_indexorder_long_row(gpu, oracle):
+    # one node with more in-edges than a staged tile (6144): the sweep reads it from HBM
+    n = 9000
+    rng = np.random.default_rng(2)
+    src = list(range(7000)) + list(rng.integers(0, 8000, 3000))
+    dst = [8999] * 7000 + [int(x) + 1 + int(rng.integers(0, 999)) for x in rng.integers(0, 8000, 3000)]
+    pairs = sorted({(s, d) for s, d in zip(src, dst) if s < d < n})
+    g = Graph(np.arange(n), rng.integers(1, 100, n), np.ones(n, np.int64), [p[0] for p in pairs],
+              [p[1] for p in pairs], rng.integers(0, 1 << 20, len(pairs)))
+    a = gpu.compute_levels(g, GEN)
+    b = oracle.compute_levels(g, GEN)
+    for x, y, nm in zip(a, b, "tbc"):
+        same(x, y, nm)
