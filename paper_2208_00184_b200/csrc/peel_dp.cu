@@ -478,29 +478,17 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem& S) {
   int32_t* const seq = a.seq;
   int32_t* const pos_of = a.pos_of;
   const int4* const ell6 = a.ell6;
-  // When the previous step pushed children, the new top's row is already in registers
-  // (it arrived as `crow`): the next pop needs no shared-memory round trip.
-  bool have_next = false;
-  int32_t nsv = 0;
-  int2 nmy = make_int2(-1, 0);
   while (top >= 0) {
-    int32_t sv;
-    int2 my;  // slot (lane & 7) of the popped node's row
-    if (have_next) {
-      sv = nsv;
-      my = nmy;
-    } else {
-      if (top < base) {
-        base = max(0, top + 1 - SC / 2);
-        v6_fill(a, S, base, top, lane);
-        __syncwarp();
-      }
-      const int32_t slot = top & (SC - 1);
-      sv = S.sid[slot];
-      my = reinterpret_cast<const int2*>(S.row[slot])[lane & 7];
+    if (top < base) {
+      base = max(0, top + 1 - SC / 2);
+      v6_fill(a, S, base, top, lane);
+      __syncwarp();
     }
-    // child whose row this lane fetches: slot lane >> 2
-    const int2 cq = make_int2(__shfl_sync(FULL, my.x, lane >> 2), __shfl_sync(FULL, my.y, lane >> 2));
+    const int32_t slot = top & (SC - 1);
+    const int32_t sv = S.sid[slot];
+    const int2* rowp = reinterpret_cast<const int2*>(S.row[slot]);
+    const int2 cq = rowp[lane >> 2];  // child whose row this lane fetches
+    const int2 my = rowp[lane & 7];   // child this lane decrements (lanes 0..7)
     --top;
     const int32_t v = sv & 0xffffff;
     if (lane == (p & 31)) held = v;  // lane k holds the node of position 32i + k
@@ -515,7 +503,6 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem& S) {
     }
     if (sv & kV6Long) {
       // ---- CSR path: rows longer than 8
-      have_next = false;
       const int32_t rs = a.out_off[v], dg = a.out_off[v + 1] - rs;
       int32_t nf = 0;
       for (int32_t b0 = 0; b0 < dg; b0 += 32) {
@@ -604,7 +591,6 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem& S) {
       }
     }
     const unsigned m = __ballot_sync(FULL, fr);
-    have_next = m != 0u;
     if (m) {
       const int nf = __popc(m);
       if (top + nf - base >= SC - 1) {  // spill the lower half of the cache (rows are dropped)
@@ -612,23 +598,13 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem& S) {
         __syncwarp();
         base += SC / 2;
       }
-      // pushed in descending rank: slot k lands above every freed slot of higher rank;
-      // the lowest freed slot (the new top) is handed over in registers instead
-      const int j = __ffs(m) - 1;
-      if (((m >> q) & 1u) && q != j) {
-        S.row[(top + 1 + __popc(m >> q >> 1)) & (SC - 1)][lane & 3] = crow;
-      }
+      // pushed in descending rank: slot k lands above every freed slot of higher rank
       if ((m >> q) & 1u) {
+        S.row[(top + 1 + __popc(m >> q >> 1)) & (SC - 1)][lane & 3] = crow;
         if (crow.x >= 0) prefetch_l2(ell6 + static_cast<int64_t>(crow.x) * 4);
         if (crow.z >= 0) prefetch_l2(ell6 + static_cast<int64_t>(crow.z) * 4);
       }
-      const int32_t mysid = my.x | (my.y < 0 ? kV6Long : 0);
-      if (fr && lane != j) S.sid[(top + 1 + __popc(m >> lane >> 1)) & (SC - 1)] = mysid;
-      const int src = 4 * j + ((lane & 7) >> 1);
-      const int4 t4 = make_int4(__shfl_sync(FULL, crow.x, src), __shfl_sync(FULL, crow.y, src),
-                                __shfl_sync(FULL, crow.z, src), __shfl_sync(FULL, crow.w, src));
-      nmy = (lane & 1) ? make_int2(t4.z, t4.w) : make_int2(t4.x, t4.y);
-      nsv = __shfl_sync(FULL, mysid, j);
+      if (fr) S.sid[(top + 1 + __popc(m >> lane >> 1)) & (SC - 1)] = my.x | (my.y < 0 ? kV6Long : 0);
       top += nf;
     }
     __syncwarp();
