@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--stages", action="store_true", help="print per-stage device times to stderr")
+    p.add_argument("--stages-under-load", action="store_true",
+                   help="print replica 0's per-stage device times during the throughput steps")
     p.add_argument("--replicas", type=int, default=32,
                    help="independent graphs generated concurrently per GPU (one stream + host thread each)")
     return p.parse_args()
@@ -252,6 +254,8 @@ def ours(args):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     l0 = sum(lib.dp_ctx_launch_count(rb.ctx) for _, rb, _ in reps)
+    if args.stages_under_load:
+        lib.dp_ctx_enable_stage_timing(reps[0][1].ctx, 1)
     with Clocks(local) as clocks:
         t0 = time.perf_counter()
         for i in range(args.steps):
@@ -271,6 +275,10 @@ def ours(args):
         wall = time.perf_counter() - t0
     if world > 1:
         torch.distributed.barrier()
+    if args.stages_under_load and rank == 0:
+        for nm, ms_, _ in stage_times(lib, reps[0][1].ctx):
+            print(f"under load (R={R}): stage {nm:18s} {ms_:10.3f} ms", file=sys.stderr)
+        lib.dp_ctx_enable_stage_timing(reps[0][1].ctx, 0)
     launches = sum(lib.dp_ctx_launch_count(rb.ctx) for _, rb, _ in reps) - l0
     step_ms = [a.elapsed_time(b) for a, b in evs]
     mean_ms = float(np.mean(step_ms))
