@@ -62,6 +62,9 @@ struct dp_ctx {
   char* pin = nullptr;
   size_t pin_cap = 0, pin_off = 0;
   std::vector<PendingCopy> pending;
+  // Host waits block on this event (cudaEventBlockingSync) instead of spinning: many
+  // contexts driven by more host threads than cores must not burn the cores they share.
+  cudaEvent_t sync_ev = nullptr;
 };
 
 namespace dpb {

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // context.cu — dp_ctx lifecycle, thread-local last error, stage timing.
 #include <cstring>
 
@@ -105,7 +106,12 @@ void download_bytes(dp_ctx* ctx, void* host, const void* dev, size_t bytes) {
 }
 
 void sync(dp_ctx* ctx) {
-  DP_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ctx->sync_ev) {
+    DP_CUDA(cudaEventRecord(ctx->sync_ev, ctx->stream));
+    DP_CUDA(cudaEventSynchronize(ctx->sync_ev));
+  } else {
+    DP_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
   for (const auto& c : ctx->pending) std::memcpy(c.dst, ctx->pin + c.off, c.bytes);
   ctx->pending.clear();
   ctx->pin_off = 0;
@@ -152,6 +158,8 @@ int dp_ctx_create(int device, void* stream, dp_ctx_t** out) {
     ctx->device = device;
     ctx->stream = static_cast<cudaStream_t>(stream);
     ctx->num_sms = prop.multiProcessorCount;
+    if (getenv("DP_SPIN_SYNC") == nullptr)
+      DP_CUDA(cudaEventCreateWithFlags(&ctx->sync_ev, cudaEventBlockingSync | cudaEventDisableTiming));
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
       uint64_t threshold = UINT64_MAX;
@@ -171,6 +179,7 @@ void dp_ctx_destroy(dp_ctx_t* ctx) {
   cudaStreamSynchronize(ctx->stream);
   ctx->pending.clear();
   if (ctx->pin) cudaFreeHost(ctx->pin);
+  if (ctx->sync_ev) cudaEventDestroy(ctx->sync_ev);
   for (auto& s : ctx->stages) ctx->event_pool.push_back(s);
   for (auto& s : ctx->event_pool) {
     cudaEventDestroy(s.a);
