@@ -330,6 +330,18 @@ int dp_pipeline(dp_ctx_t* ctx, const dp_graph_t* g, const dp_devices_t* devices,
                 const dp_pipeline_config_t* cfg, dp_pipeline_result_t** out);
 void dp_pipeline_result_free(dp_pipeline_result_t* r);
 
+/* Graph / device documents parsed straight into SoA arrays (host code,
+ * json_load.cu): replaces graph_from_json (json_io.cpp:43-74) + the AoS
+ * ComputationGraph, so a document feeds dp_* calls directly (the result casts to the
+ * dp_graph_t view: same field order).  colocation_group strings become labels in
+ * first-appearance order (-1 = none); node names are not kept.  Errors: DP_E_PARSE_ERROR
+ * with the reference's message for schema errors; syntax errors (which json::parse
+ * rejects) are "invalid JSON: <what>".  Free with dp_graph_out_free. */
+int dp_graph_from_json(const char* text, int64_t len, dp_graph_out_t** out);
+/* devices_from_json (json_io.cpp:93-117): writes min(count, capacity) devices. */
+int dp_devices_from_json(const char* text, int64_t len, int32_t* count, int32_t* ids, int64_t* memory_bytes,
+                         int32_t capacity, dp_comm_t* comm);
+
 /* Device-resident variant for throughput measurement: upload once, then run the
  * generation window (pipeline.cpp:67-79) with every intermediate kept in HBM.
  * dp_resident_generate writes only device buffers; dp_resident_fetch copies the two

@@ -18,6 +18,7 @@
 #include "dagplace/generator.hpp"
 #include "dagplace/graph.hpp"
 #include "dagplace/graph_index.hpp"
+#include "dagplace/json_io.hpp"
 #include "dagplace/ordering.hpp"
 #include "dagplace/pipeline.hpp"
 #include "dagplace/placement.hpp"
@@ -202,6 +203,68 @@ extern "C" {
 DPR_DEFINE_FREES(dpr_)
 
 const char* dpr_last_error_message(void) { return g_err.c_str(); }
+
+// graph_from_json (json_io.cpp:43-74) over json::parse of the text; colocation_group
+// strings become labels in first-appearance order.  json::exception -> ParseError.
+int dpr_graph_from_json(const char* text, int64_t len, dp_graph_out_t** out) {
+  try {
+    nlohmann::json j;
+    try {
+      j = nlohmann::json::parse(std::string(text, static_cast<size_t>(len)));
+    } catch (const nlohmann::json::exception& e) {
+      g_err = std::string("ParseError: invalid JSON: ") + e.what();
+      return 1 + static_cast<int>(ErrorKind::ParseError);
+    }
+    const ComputationGraph g = graph_from_json(j);
+    dp_graph_out_t* o = dpr_graph_out_new(static_cast<int64_t>(g.nodes.size()), static_cast<int64_t>(g.edges.size()));
+    std::map<std::string, int32_t> labels;
+    for (size_t i = 0; i < g.nodes.size(); ++i) {
+      o->node_id[i] = g.nodes[i].id;
+      o->compute_us[i] = g.nodes[i].compute_us;
+      o->memory_bytes[i] = g.nodes[i].memory_bytes;
+      int32_t lab = -1;
+      if (g.nodes[i].colocation_group) {
+        auto it = labels.emplace(*g.nodes[i].colocation_group, static_cast<int32_t>(labels.size())).first;
+        lab = it->second;
+      }
+      o->group[i] = lab;
+    }
+    for (size_t e = 0; e < g.edges.size(); ++e) {
+      o->edge_src[e] = g.edges[e].src;
+      o->edge_dst[e] = g.edges[e].dst;
+      o->edge_bytes[e] = g.edges[e].tensor_bytes;
+    }
+    *out = o;
+    return 0;
+  } catch (const DagError& e) {
+    return fail(e);
+  }
+}
+
+// devices_from_json (json_io.cpp:93-117).
+int dpr_devices_from_json(const char* text, int64_t len, int32_t* count, int32_t* ids, int64_t* memory_bytes,
+                          int32_t capacity, dp_comm_t* comm) {
+  try {
+    nlohmann::json j;
+    try {
+      j = nlohmann::json::parse(std::string(text, static_cast<size_t>(len)));
+    } catch (const nlohmann::json::exception& e) {
+      g_err = std::string("ParseError: invalid JSON: ") + e.what();
+      return 1 + static_cast<int>(ErrorKind::ParseError);
+    }
+    const DeviceFile f = devices_from_json(j);
+    *count = static_cast<int32_t>(f.devices.size());
+    for (size_t i = 0; i < f.devices.size() && static_cast<int32_t>(i) < capacity; ++i) {
+      ids[i] = f.devices[i].id;
+      memory_bytes[i] = f.devices[i].memory_bytes;
+    }
+    comm->k_us_per_byte = f.comm.k_us_per_byte;
+    comm->b_us = f.comm.b_us;
+    return 0;
+  } catch (const DagError& e) {
+    return fail(e);
+  }
+}
 
 int dpr_comm_time(int64_t bytes, dp_comm_t comm, int64_t* out) {
   try {  // graph.cpp:200-204

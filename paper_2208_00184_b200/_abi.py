@@ -586,3 +586,51 @@ class Backend:
                              int(r.order_makespan), int(r.adjust_makespan), float(r.generation_ms))
         self._free["pipeline"](p)
         return rep
+
+
+def graph_from_json(lib: C.CDLL, text, prefix: str = "dp_") -> Graph:
+    """graph_from_json (json_io.cpp:43-74) through `prefix`graph_from_json: the product's
+    SoA loader (dp_, host code, no GPU needed) or the reference shim (dpr_, tests only)."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    f = getattr(lib, prefix + "graph_from_json")
+    f.restype = C.c_int
+    f.argtypes = [C.c_char_p, C.c_int64, C.POINTER(C.POINTER(GraphOutC))]
+    out = C.POINTER(GraphOutC)()
+    rc = f(data, len(data), C.byref(out))
+    err = getattr(lib, prefix + "last_error_message")
+    err.restype = C.c_char_p
+    if rc:
+        raise DagError(rc, (err() or b"").decode())
+    o = out.contents
+    n, m = o.n_nodes, o.n_edges
+
+    def arr(ptr, k, dt):
+        return np.ctypeslib.as_array(ptr, shape=(k,)).astype(dt, copy=True) if k else np.zeros(0, dt)
+    g = Graph(arr(o.node_id, n, np.int64), arr(o.compute_us, n, np.int64), arr(o.memory_bytes, n, np.int64),
+              arr(o.edge_src, m, np.int64), arr(o.edge_dst, m, np.int64), arr(o.edge_bytes, m, np.int64),
+              arr(o.group, n, np.int32))
+    free = getattr(lib, "dp_graph_out_free" if prefix == "dp_" else prefix + "free_graph_out")
+    free.restype = None
+    free.argtypes = [C.POINTER(GraphOutC)]
+    free(out)
+    return g
+
+
+def devices_from_json(lib: C.CDLL, text, prefix: str = "dp_"):
+    """devices_from_json (json_io.cpp:93-117) -> ([(id, memory_bytes)], (k, b))."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    f = getattr(lib, prefix + "devices_from_json")
+    f.restype = C.c_int
+    f.argtypes = [C.c_char_p, C.c_int64, I32P, I32P, I64P, C.c_int32, C.POINTER(CommC)]
+    cap = 4096
+    ids = np.zeros(cap, np.int32)
+    mem = np.zeros(cap, np.int64)
+    cnt = C.c_int32()
+    comm = CommC()
+    rc = f(data, len(data), C.byref(cnt), ids.ctypes.data_as(I32P), mem.ctypes.data_as(I64P), cap, C.byref(comm))
+    err = getattr(lib, prefix + "last_error_message")
+    err.restype = C.c_char_p
+    if rc:
+        raise DagError(rc, (err() or b"").decode())
+    k = min(cnt.value, cap)
+    return [(int(ids[i]), int(mem[i])) for i in range(k)], (comm.k_us_per_byte, comm.b_us)
