@@ -600,7 +600,7 @@ def graph_from_json(lib: C.CDLL, text, prefix: str = "dp_") -> Graph:
     err = getattr(lib, prefix + "last_error_message")
     err.restype = C.c_char_p
     if rc:
-        raise DagError(rc, (err() or b"").decode())
+        raise DagError(rc, (err() or b"").decode(errors="replace"))
     o = out.contents
     n, m = o.n_nodes, o.n_edges
 
@@ -631,6 +631,6 @@ def devices_from_json(lib: C.CDLL, text, prefix: str = "dp_"):
     err = getattr(lib, prefix + "last_error_message")
     err.restype = C.c_char_p
     if rc:
-        raise DagError(rc, (err() or b"").decode())
+        raise DagError(rc, (err() or b"").decode(errors="replace"))
     k = min(cnt.value, cap)
     return [(int(ids[i]), int(mem[i])) for i in range(k)], (comm.k_us_per_byte, comm.b_us)

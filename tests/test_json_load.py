@@ -35,7 +35,7 @@ def _outcome(fn, lib, text, prefix):
 
 
 def _same(a, b, text, syntax_kind_only=False):
-    assert a[0] == b[0], (text[:200], a, b)  # noqa
+    assert a[0] == b[0], (text[:200], a, b)
     if a[0] == "err":
         assert a[1][0] == b[1][0], (text[:200], a[1], b[1])
         if not syntax_kind_only and "invalid JSON" not in b[1][1]:
