@@ -309,8 +309,8 @@ __device__ __forceinline__ void kahn_pull_warp(const KahnArgs& a, int32_t v) {
 // rows (CSC for tlevel, CSR backwards for blevel) into shared memory, then warp 0 walks
 // the tile with the running finish/blevel values in shared memory: per node one gather
 // per in-edge and a two-step 64-bit max (redux.sync on high then low words).
-constexpr int kSeqMaxN = 12288;
-constexpr int kSeqTile = 6144;   // edges staged per tile
+constexpr int kSeqMaxN = 16384;  // power of two: the value ring is indexed with a mask
+constexpr int kSeqTile = 4096;   // edges staged per tile
 constexpr int kSeqTileN = 2048;  // nodes staged per tile
 
 __global__ void k_index_topo(const int32_t* in_off, const int32_t* in_src, int32_t n, int* ok) {
@@ -387,13 +387,13 @@ __global__ void __launch_bounds__(1024) k_levels_seq(int32_t n, const int32_t* o
           const int32_t u = fits ? en[k - e0] : nbr[k];
           const int64_t c = fits ? ec[k - e0] : cost[k];
           const int32_t pu = rev ? n - 1 - u : u;  // sweep position of u (< i)
-          const int64_t fu = i - pu <= kSeqMaxN ? val[pu % kSeqMaxN] : __ldcg(gval + u);
+          const int64_t fu = i - pu <= kSeqMaxN ? val[pu & (kSeqMaxN - 1)] : __ldcg(gval + u);
           mx = max(mx, fu + c);
         }
         mx = warp_max_nonneg(mx);
         if (lane == 0) {
           const int64_t vv = mx + wt[i - done];  // f[v] = tlevel + w (fwd); blevel (bwd)
-          val[i % kSeqMaxN] = vv;
+          val[i & (kSeqMaxN - 1)] = vv;
           if (gval) __stcg(gval + v, vv);
           out[v] = rev ? vv : mx;
         }

@@ -6,7 +6,7 @@ restatement (oracle/dp_oracle.c).
                  hash buckets (global spill counters), DFS as well as CPD ranks
   streamed DP    v3 (R <= 225), 32-step blocks (226..256), per-step 32-bit keys (cost
                  bound), 64-bit keys (large costs), R = 1 / 32 / 33 block edges
-  levels         index-order sweep (n <= 12288, index order topological) vs the Kahn
+  levels         index-order sweep (n <= 16384, index order topological) vs the Kahn
                  frontier (shuffled ids, n just above the sweep limit)
 """
 import numpy as np
@@ -87,7 +87,7 @@ def test_streamed_dp_cost_widths(gpu, oracle, scale):
         same_map(ma, mb, f"s{scale} r{r}")
 
 
-@pytest.mark.parametrize("n", [12287, 12288, 12289])
+@pytest.mark.parametrize("n", [16383, 16384, 16385])
 def test_levels_indexorder_limit(gpu, oracle, n):
     g = layered(29, n, 3, fan_lo=1, fan_hi=3)
     a = gpu.compute_levels(g, GEN)
