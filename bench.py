@@ -229,22 +229,33 @@ def ours(args):
         reps.append((st, rbe, rres))
     torch.cuda.synchronize()
 
-    def run_all():
-        errs = []
+    # one persistent host thread per replica (created once), released together each step
+    errs = []
+    go = threading.Barrier(R + 1)
+    done = threading.Barrier(R + 1)
+    stop = [False]
 
-        def work(rres):
+    def worker(rres):
+        while True:
+            go.wait()
+            if stop[0]:
+                return
             rc = lib.dp_resident_generate(rres)
             if rc:
                 errs.append(lib.dp_last_error_message().decode())
-        ths = [threading.Thread(target=work, args=(rr,)) for _, _, rr in reps]
-        for t_ in ths:
-            t_.start()
-        for t_ in ths:
-            t_.join()
+            done.wait()
+
+    pool = [threading.Thread(target=worker, args=(rr,), daemon=True) for _, _, rr in reps]
+    for t_ in pool:
+        t_.start()
+
+    def run_all():
+        go.wait()
+        done.wait()
         if errs:
             raise RuntimeError(errs[0])
 
-    for _ in range(max(1, args.warmup // 2)):
+    for _ in range(max(2, args.warmup)):
         flush_l2(flush)
         run_all()
     torch.cuda.synchronize()
@@ -280,6 +291,10 @@ def ours(args):
             print(f"under load (R={R}): stage {nm:18s} {ms_:10.3f} ms", file=sys.stderr)
         lib.dp_ctx_enable_stage_timing(reps[0][1].ctx, 0)
     launches = sum(lib.dp_ctx_launch_count(rb.ctx) for _, rb, _ in reps) - l0
+    stop[0] = True
+    go.wait()
+    for t_ in pool:
+        t_.join()
     step_ms = [a.elapsed_time(b) for a, b in evs]
     mean_ms = float(np.mean(step_ms))
     t = torch.tensor([mean_ms], device="cuda")

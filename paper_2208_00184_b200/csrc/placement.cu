@@ -28,16 +28,35 @@ namespace {
 constexpr int kMaxD = 256;
 constexpr unsigned FULL = 0xffffffffu;
 
+// Blocked device timeline (DeviceTimeline, placement.cpp:13-32).  Intervals sorted by
+// start (upper_bound insert) live in blocks of 32 (one lane per entry); blocks are kept
+// in sequence by POSITION with per-position meta: physical id, count, max end, end
+// prefix max over all blocks up to here (pmEnd), first entry, and an upper bound of the
+// gaps inside the block (computed with the block-local end prefix max; the true prefix
+// max can only be larger, so the true gaps only smaller: false positives are re-checked).
+// An insert touches one block (split in halves when full) instead of shifting the whole
+// timeline; pmEnd changes propagate forward only while they change (rarely past one).
+// Semantics are the reference's exactly: with PM[k] = max(E[0..k]) the scan stops at the
+// first interval with PM > earliest if its start leaves room, else at the first later
+// interval k with E[k] > PM[k-1] and S[k] - PM[k-1] >= dur, returning PM[k-1]; else the
+// overall max end (zero-length intervals included).
+constexpr int kTB = 32;
+
 struct TLView {
-  int64_t *S, *E, *PM, *GQ, *BG;
+  int64_t *S, *E;                                 // [maxb][kTB] by physical block id
+  int32_t *id, *cnt;                              // [maxb] by position
+  int64_t *maxE, *pmEnd, *fS, *fE, *gub;          // [maxb] by position
+  int32_t* nb;                                    // blocks in use (shared memory)
 };
 
 struct TLArrays {
-  int64_t *S, *E, *PM, *GQ, *BG;
-  int32_t cap, nb;
+  int64_t *S, *E, *maxE, *pmEnd, *fS, *fE, *gub;
+  int32_t *id, *cnt;
+  int32_t maxb;
+  int32_t* nb;  // shared memory, set by the kernel
   __device__ TLView view(int d) const {
-    return TLView{S + (int64_t)d * cap, E + (int64_t)d * cap, PM + (int64_t)d * cap, GQ + (int64_t)d * cap,
-                  BG + (int64_t)d * nb};
+    const int64_t eo = (int64_t)d * maxb * kTB, mo = (int64_t)d * maxb;
+    return TLView{S + eo, E + eo, id + mo, cnt + mo, maxE + mo, pmEnd + mo, fS + mo, fE + mo, gub + mo, nb + d};
   }
 };
 
@@ -63,121 +82,213 @@ __device__ __forceinline__ int32_t warp_first_true(int32_t lo, int32_t hi, Pred 
   return lo + __ffs(b) - 1;
 }
 
+__device__ __forceinline__ int64_t warp_incl_max(int64_t v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v = y > v ? y : v;
+  }
+  return v;
+}
+
+struct BlockLoad {
+  int64_t s, e, pm, pmprev;  // this lane's entry, PM at it, PM before it (with carry)
+  int32_t c;
+};
+
+// Loads block at position pos (lane = entry) with the PM carried in from earlier blocks.
+__device__ __forceinline__ BlockLoad tl_load(const TLView t, int32_t pos) {
+  const int lane = threadIdx.x & 31;
+  BlockLoad r;
+  const int32_t b = t.id[pos];
+  r.c = t.cnt[pos];
+  const int64_t carry = pos > 0 ? t.pmEnd[pos - 1] : INT64_MIN;
+  r.s = lane < r.c ? t.S[(int64_t)b * kTB + lane] : INT64_MAX;
+  r.e = lane < r.c ? t.E[(int64_t)b * kTB + lane] : INT64_MIN;
+  const int64_t inc = warp_incl_max(r.e);
+  r.pm = inc > carry ? inc : carry;
+  const int64_t up = __shfl_up_sync(FULL, r.pm, 1);
+  r.pmprev = lane == 0 ? carry : up;
+  return r;
+}
+
 // DeviceTimeline::find_slot(earliest, dur) (placement.cpp:13-21); warp-collective.
 __device__ int64_t tl_query(const TLView t, int32_t K, int64_t gmax, int64_t last, int64_t earliest, int64_t dur) {
   const int lane = threadIdx.x & 31;
   if (K == 0 || last <= earliest) return earliest;
-  const int32_t k0 = warp_first_true(0, K - 1, [&](int32_t q) { return t.PM[q] > earliest; });
-  const int64_t sk = t.S[k0];
-  if (sk >= earliest && sk - earliest >= dur) return earliest;
+  const int32_t nb = *t.nb;
+  // first interval with PM > earliest: its block is the first position with pmEnd > earliest
+  const int32_t j = warp_first_true(0, nb - 1, [&](int32_t q) { return t.pmEnd[q] > earliest; });
+  BlockLoad L = tl_load(t, j);
+  const int k0 = __ffs(__ballot_sync(FULL, lane < L.c && L.pm > earliest)) - 1;
+  const int64_t s0 = __shfl_sync(FULL, L.s, k0);
+  if (s0 >= earliest && s0 - earliest >= dur) return earliest;
   if (gmax < dur) return last;
-  const int32_t k = k0 + 1;
-  if (k >= K) return last;
-  const int32_t blk = k >> 5;
   {
-    const int32_t idx = (blk << 5) + lane;
-    const unsigned b = __ballot_sync(FULL, idx >= k && idx < K && t.GQ[idx] >= dur);
-    if (b) return t.PM[(blk << 5) + __ffs(b) - 2];
+    const bool fit = lane > k0 && lane < L.c && L.e > L.pmprev && L.s - L.pmprev >= dur;
+    const unsigned bal = __ballot_sync(FULL, fit);
+    if (bal) return __shfl_sync(FULL, L.pmprev, __ffs(bal) - 1);
   }
-  const int32_t nblk = (K + 31) >> 5;
-  for (int32_t b0 = blk + 1; b0 < nblk; b0 += 32) {
-    const int32_t bb = b0 + lane;
-    const unsigned bal = __ballot_sync(FULL, bb < nblk && t.BG[bb] >= dur);
-    if (bal) {
-      const int32_t fb = b0 + __ffs(bal) - 1;
-      const int32_t idx = (fb << 5) + lane;
-      const unsigned b2 = __ballot_sync(FULL, idx < K && t.GQ[idx] >= dur);
-      return t.PM[(fb << 5) + __ffs(b2) - 2];
+  for (int32_t p0 = j + 1; p0 < nb; p0 += 32) {
+    const int32_t p = p0 + lane;
+    bool cand = false;
+    if (p < nb) {
+      const int64_t pe = t.pmEnd[p - 1];
+      cand = t.gub[p] >= dur || (t.fE[p] > pe && t.fS[p] - pe >= dur);
+    }
+    unsigned bal = __ballot_sync(FULL, cand);
+    while (bal) {
+      const int32_t pos = p0 + __ffs(bal) - 1;
+      bal &= bal - 1;
+      L = tl_load(t, pos);
+      const bool fit = lane < L.c && L.e > L.pmprev && L.s - L.pmprev >= dur;
+      const unsigned b2 = __ballot_sync(FULL, fit);
+      if (b2) return __shfl_sync(FULL, L.pmprev, __ffs(b2) - 1);
     }
   }
   return last;
+}
+
+// Recomputes the meta of the block at position pos from its entries (warp-collective)
+// and propagates pmEnd forward while it changes.  Returns the block's gap upper bound.
+__device__ int64_t tl_meta(const TLView t, int32_t pos, int32_t nb, bool propagate = true) {
+  const int lane = threadIdx.x & 31;
+  const int32_t b = t.id[pos], c = t.cnt[pos];
+  const int64_t s = lane < c ? t.S[(int64_t)b * kTB + lane] : INT64_MAX;
+  const int64_t e = lane < c ? t.E[(int64_t)b * kTB + lane] : INT64_MIN;
+  const int64_t inc = warp_incl_max(e);
+  const int64_t prev = __shfl_up_sync(FULL, inc, 1);
+  int64_t g = (lane >= 1 && lane < c && e > prev) ? s - prev : -1;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const int64_t y = __shfl_xor_sync(FULL, g, o);
+    g = y > g ? y : g;
+  }
+  const int64_t mx = __shfl_sync(FULL, inc, 31);
+  const int64_t fs = __shfl_sync(FULL, s, 0), fe = __shfl_sync(FULL, e, 0);
+  if (lane == 0) {
+    t.maxE[pos] = mx;
+    t.fS[pos] = fs;
+    t.fE[pos] = fe;
+    t.gub[pos] = g;
+    int64_t pm = pos > 0 && t.pmEnd[pos - 1] > mx ? t.pmEnd[pos - 1] : mx;
+    t.pmEnd[pos] = pm;
+    for (int32_t q = pos + 1; propagate && q < nb; ++q) {  // forward while it changes
+      const int64_t np = t.maxE[q] > pm ? t.maxE[q] : pm;
+      if (np == t.pmEnd[q]) break;
+      t.pmEnd[q] = np;
+      pm = np;
+    }
+  }
+  __syncwarp();
+  return g;
 }
 
 // DeviceTimeline::reserve(start, dur) (placement.cpp:23-32): upper_bound insert.
 __device__ void tl_insert(const TLView t, int32_t* Kp, int64_t* gmaxp, int64_t* lastp, int64_t s, int64_t dur) {
   const int lane = threadIdx.x & 31;
   const int64_t e = s + dur;
-  const int32_t K = *Kp;
+  int32_t nb = *t.nb;
   const int64_t last = *lastp;
-  int32_t q;
-  if (K == 0 || t.S[K - 1] <= s) {
-    q = K;
-  } else {
-    q = warp_first_true(0, K - 1, [&](int32_t x) { return t.S[x] > s; });
-  }
-  if (q == K) {
+  int64_t gnew = -1;  // gaps this insert may create (upper bound bookkeeping)
+  if (nb == 0) {
     if (lane == 0) {
-      t.S[q] = s;
-      t.E[q] = e;
-      const int64_t pm = K ? (last > e ? last : e) : e;
-      t.PM[q] = pm;
-      const int64_t gq = (K == 0) ? -1 : (e > last ? s - last : -1);
-      t.GQ[q] = gq;
-      const int32_t b = q >> 5;
-      t.BG[b] = (q & 31) == 0 ? gq : (t.BG[b] > gq ? t.BG[b] : gq);
-      if (gq > *gmaxp) *gmaxp = gq;
-      *lastp = pm;
-      *Kp = K + 1;
+      t.id[0] = 0;
+      t.cnt[0] = 1;
+      t.S[0] = s;
+      t.E[0] = e;
+      t.maxE[0] = e;
+      t.pmEnd[0] = e;
+      t.fS[0] = s;
+      t.fE[0] = e;
+      t.gub[0] = -1;
+      *t.nb = 1;
+      *Kp = 1;
+      *lastp = e;
     }
     __syncwarp();
     return;
   }
-  for (int32_t top = K; top > q; top -= 32) {
-    const int32_t base = max(q, top - 32);
-    const int32_t idx = base + lane;
-    const bool act = idx < top;
-    int64_t vs = 0, ve = 0, vp = 0, vg = 0;
-    if (act) {
-      vs = t.S[idx];
-      ve = t.E[idx];
-      vp = t.PM[idx];
-      vg = t.GQ[idx];
+  // target block: the last position whose first start <= s (entries with S <= s precede)
+  int32_t j;
+  if (t.fS[nb - 1] <= s) {
+    j = nb - 1;
+  } else {
+    j = warp_first_true(0, nb - 1, [&](int32_t q) { return t.fS[q] > s; }) - 1;
+    if (j < 0) j = 0;
+  }
+  if (t.cnt[j] == kTB) {  // split in halves: the upper half moves to a new block after j
+    const int32_t nbid = nb;  // ids are allocated densely: the next free id is nb
+    const int32_t b = t.id[j];
+    if (lane >= kTB / 2) {
+      t.S[(int64_t)nbid * kTB + lane - kTB / 2] = t.S[(int64_t)b * kTB + lane];
+      t.E[(int64_t)nbid * kTB + lane - kTB / 2] = t.E[(int64_t)b * kTB + lane];
+    }
+    // shift positions j+1 .. nb-1 up by one (from the top, 32 at a time)
+    for (int32_t top = nb; top > j + 1; top -= 32) {
+      const int32_t lo = max(j + 1, top - 32);
+      const int32_t q = lo + lane;
+      int32_t vi = 0, vc = 0;
+      int64_t m1 = 0, m2 = 0, m3 = 0, m4 = 0, m5 = 0;
+      const bool act = q < top;
+      if (act) {
+        vi = t.id[q]; vc = t.cnt[q]; m1 = t.maxE[q]; m2 = t.pmEnd[q]; m3 = t.fS[q]; m4 = t.fE[q]; m5 = t.gub[q];
+      }
+      __syncwarp();
+      if (act) {
+        t.id[q + 1] = vi; t.cnt[q + 1] = vc; t.maxE[q + 1] = m1; t.pmEnd[q + 1] = m2; t.fS[q + 1] = m3;
+        t.fE[q + 1] = m4; t.gub[q + 1] = m5;
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      t.id[j + 1] = nbid;
+      t.cnt[j + 1] = kTB / 2;
+      t.cnt[j] = kTB / 2;
+      t.pmEnd[j + 1] = t.pmEnd[j];  // placeholder until tl_meta below
+      *t.nb = ++nb;
     }
     __syncwarp();
-    if (act) {
-      t.S[idx + 1] = vs;
-      t.E[idx + 1] = ve;
-      t.PM[idx + 1] = vp;
-      t.GQ[idx + 1] = vg;
+    tl_meta(t, j, nb, false);  // position j + 1 is not valid yet: no propagation
+    tl_meta(t, j + 1, nb);
+    if (t.fS[j + 1] <= s) ++j;
+  }
+  // insert into block j at the upper_bound position
+  const int32_t b = t.id[j], c = t.cnt[j];
+  const int64_t vs = lane < c ? t.S[(int64_t)b * kTB + lane] : INT64_MAX;
+  const int64_t ve = lane < c ? t.E[(int64_t)b * kTB + lane] : 0;
+  const int q = __popc(__ballot_sync(FULL, lane < c && vs <= s));
+  __syncwarp();
+  if (lane >= q && lane < c) {
+    t.S[(int64_t)b * kTB + lane + 1] = vs;
+    t.E[(int64_t)b * kTB + lane + 1] = ve;
+  }
+  if (lane == q) {
+    t.S[(int64_t)b * kTB + lane] = s;
+    t.E[(int64_t)b * kTB + lane] = e;
+  }
+  if (lane == 0) t.cnt[j] = c + 1;
+  __syncwarp();
+  gnew = tl_meta(t, j, nb);
+  // the next block's first gap may have changed (its carry in); count it in the bound
+  if (j + 1 < nb) {
+    const int64_t pe = t.pmEnd[j];
+    const int64_t g1 = t.fE[j + 1] > pe ? t.fS[j + 1] - pe : -1;
+    gnew = g1 > gnew ? g1 : gnew;
+  }
+  // the first gap of block j itself (against its carry)
+  {
+    const int64_t pe = j > 0 ? t.pmEnd[j - 1] : INT64_MIN;
+    if (j > 0 && t.fE[j] > pe) {
+      const int64_t g0 = t.fS[j] - pe;
+      gnew = g0 > gnew ? g0 : gnew;
     }
-    __syncwarp();
   }
-  const int32_t Kn = K + 1;
   if (lane == 0) {
-    t.S[q] = s;
-    t.E[q] = e;
-    const int64_t prev = q ? t.PM[q - 1] : INT64_MIN;
-    t.PM[q] = prev > e ? prev : e;
-  }
-  __syncwarp();
-  for (int32_t idx = q + 1 + lane; idx < Kn; idx += 32) {
-    const int64_t pm = t.PM[idx];
-    if (pm < e) t.PM[idx] = e;
-  }
-  __syncwarp();
-  for (int32_t idx = max(q, 1) + lane; idx < Kn; idx += 32) {
-    const int64_t pp = t.PM[idx - 1];
-    const int64_t ev = t.E[idx];
-    t.GQ[idx] = ev > pp ? t.S[idx] - pp : -1;
-  }
-  if (q == 0 && lane == 0) t.GQ[0] = -1;
-  __syncwarp();
-  const int32_t lastb = (Kn - 1) >> 5;
-  for (int32_t b = (q >> 5) + lane; b <= lastb; b += 32) {
-    int64_t mx = INT64_MIN;
-    const int32_t hi = min((b << 5) + 31, Kn - 1);
-    for (int32_t i = b << 5; i <= hi; ++i) mx = max(mx, t.GQ[i]);
-    t.BG[b] = mx;
-  }
-  __syncwarp();
-  int64_t mx = -1;
-  for (int32_t b = lane; b <= lastb; b += 32) mx = max(mx, t.BG[b]);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL, mx, o));
-  if (lane == 0) {
-    *gmaxp = mx;
+    if (gnew > *gmaxp) *gmaxp = gnew;
     *lastp = last > e ? last : e;
-    *Kp = Kn;
+    *Kp = *Kp + 1;
   }
   __syncwarp();
 }
@@ -212,7 +323,7 @@ __device__ int32_t most_free(const int64_t* avail, int32_t D) {  // placement.cp
 }
 
 __global__ void __launch_bounds__(256) k_place(PlaceArgs a) {
-  __shared__ int32_t sK[kMaxD];
+  __shared__ int32_t sK[kMaxD], snb[kMaxD];
   __shared__ int64_t sg[kMaxD], sl[kMaxD], savail[kMaxD], spdm[kMaxD];
   __shared__ long long sA[kMaxD], sB[kMaxD];
   __shared__ int64_t sest[kMaxD], spre[kMaxD];
@@ -222,9 +333,11 @@ __global__ void __launch_bounds__(256) k_place(PlaceArgs a) {
   if (!a.run[which]) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int32_t D = a.D;
-  const TLArrays tl = a.tl[which];
+  TLArrays tl = a.tl[which];
+  tl.nb = snb;
   for (int d = tid; d < D; d += blockDim.x) {
     sK[d] = 0;
+    snb[d] = 0;
     sg[d] = -1;
     sl[d] = 0;
     savail[d] = a.cap[d];
@@ -384,17 +497,23 @@ __global__ void k_expand(const int32_t* cl, const int32_t* cdev, const int64_t* 
     if (sm[d]) atomicAdd(reinterpret_cast<unsigned long long*>(&pdm[d]), sm[d]);
 }
 
-void alloc_tl(dp_ctx* ctx, int32_t D, int32_t cap, DevBuf<int64_t>& store, TLArrays& t) {
-  const int64_t nb = cap / 32 + 2;
-  const int64_t per = (int64_t)D * cap;
-  store.alloc(ctx, static_cast<size_t>(4 * per + (int64_t)D * nb));
+void alloc_tl(dp_ctx* ctx, int32_t D, int32_t n, DevBuf<int64_t>& store, DevBuf<int32_t>& store32, TLArrays& t) {
+  // a device holding K intervals uses at most K/16 + 1 blocks (splits leave halves of 16)
+  const int64_t maxb = n / (kTB / 2) + 2;
+  const int64_t ent = (int64_t)D * maxb * kTB, meta = (int64_t)D * maxb;
+  store.alloc(ctx, static_cast<size_t>(2 * ent + 5 * meta));
+  store32.alloc(ctx, static_cast<size_t>(2 * meta));
   t.S = store.p;
-  t.E = store.p + per;
-  t.PM = store.p + 2 * per;
-  t.GQ = store.p + 3 * per;
-  t.BG = store.p + 4 * per;
-  t.cap = cap;
-  t.nb = static_cast<int32_t>(nb);
+  t.E = store.p + ent;
+  t.maxE = store.p + 2 * ent;
+  t.pmEnd = t.maxE + meta;
+  t.fS = t.pmEnd + meta;
+  t.fE = t.fS + meta;
+  t.gub = t.fE + meta;
+  t.id = store32.p;
+  t.cnt = store32.p + meta;
+  t.maxb = static_cast<int32_t>(maxb);
+  t.nb = nullptr;
 }
 
 }  // namespace
@@ -436,11 +555,12 @@ void place_dev(DevGraph& g, const int32_t* seq, const Devices& devs, PlaceOut* o
   a.cap = cap.p;
   a.finish = finish.p;
   DevBuf<int64_t> store[2];
+  DevBuf<int32_t> store32[2];
   PlaceOut* outs[2] = {order_out, adjust_out};
   for (int w = 0; w < 2; ++w) {
     a.run[w] = outs[w] != nullptr;
     if (!outs[w]) continue;
-    alloc_tl(ctx, D, n > 0 ? n : 1, store[w], a.tl[w]);
+    alloc_tl(ctx, D, n > 0 ? n : 1, store[w], store32[w], a.tl[w]);
     outs[w]->dev.alloc(ctx, n > 0 ? n : 1);
     outs[w]->per_dev_mem.alloc(ctx, D);
     outs[w]->flags.alloc(ctx, 1);
