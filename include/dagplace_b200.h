@@ -330,6 +330,55 @@ int dp_pipeline(dp_ctx_t* ctx, const dp_graph_t* g, const dp_devices_t* devices,
                 const dp_pipeline_config_t* cfg, dp_pipeline_result_t** out);
 void dp_pipeline_result_free(dp_pipeline_result_t* r);
 
+/* ---------------------------------------------------------------- Standard Evaluation
+ * (estimation.cpp, estimation.hpp:13-86), bit-exact fp64 on the GPU (estimation.cu). */
+/* ProfileSet (estimation.hpp:25-28): batch b's samples are [node_off[b], node_off[b+1]). */
+typedef struct dp_profiles {
+  int32_t n_batches;
+  const int64_t* batch_size;    /* [n_batches] */
+  const int64_t* node_off;      /* [n_batches + 1] */
+  const int64_t* node_id;
+  const int64_t* memory_bytes;
+  const int64_t* compute_us;
+} dp_profiles_t;
+/* NodeCostModel (estimation.hpp:37-40), ascending id; fit[6k..6k+5] = memory {slope,
+ * intercept, residual_norm}, compute {slope, intercept, residual_norm} (LinearFit). */
+typedef struct dp_node_models {
+  int64_t n;
+  int64_t* node_id;
+  double* fit;
+} dp_node_models_t;
+/* DeviationReport (estimation.hpp:44-53): maps as ascending-id arrays. */
+typedef struct dp_deviation {
+  int64_t n_memory;
+  int64_t* memory_id;
+  double* memory_dev;
+  int64_t n_time;
+  int64_t* time_id;
+  double* time_dev;
+  double mean_memory, mean_time;
+  int64_t n_zero_memory;
+  int64_t* zero_memory;
+  int64_t n_zero_time;
+  int64_t* zero_time;
+} dp_deviation_t;
+/* fit_node_models (estimation.cpp:67-88).  A batch listing a node twice (not
+ * representable in the reference's unordered_map) is DP_E_INVALID_VALUE; a missing node
+ * is reported as the smallest missing id (the reference names the first in hash order). */
+int dp_fit_node_models(dp_ctx_t* ctx, const dp_profiles_t* profiles, dp_node_models_t** out);
+void dp_node_models_free(dp_node_models_t* m);
+/* estimate_graph (estimation.cpp:90-119): EdgeScaling as reference_batch + overrides
+ * (src, dst, factor); the last of repeated override pairs wins. */
+int dp_estimate_graph(dp_ctx_t* ctx, const dp_graph_t* base, const dp_node_models_t* models, int64_t target_batch,
+                      int64_t reference_batch, int64_t n_override, const int64_t* ov_src, const int64_t* ov_dst,
+                      const double* ov_factor, dp_graph_out_t** out);
+/* fit_comm_model (estimation.cpp:121-140). */
+int dp_fit_comm_model(dp_ctx_t* ctx, int64_t n, const int64_t* bytes, const double* us, dp_comm_t* out);
+/* deviation_report (estimation.cpp:148-192). */
+int dp_deviation_report(dp_ctx_t* ctx, const dp_graph_t* estimated, const dp_graph_t* measured,
+                        dp_deviation_t** out);
+void dp_deviation_free(dp_deviation_t* d);
+
 /* Graph / device documents parsed straight into SoA arrays (host code,
  * json_load.cu): replaces graph_from_json (json_io.cpp:43-74) + the AoS
  * ComputationGraph, so a document feeds dp_* calls directly (the result casts to the

@@ -14,6 +14,7 @@
 #include <thread>
 #include <vector>
 
+#include "dagplace/estimation.hpp"
 #include "dagplace/fusion.hpp"
 #include "dagplace/generator.hpp"
 #include "dagplace/graph.hpp"
@@ -264,6 +265,113 @@ int dpr_devices_from_json(const char* text, int64_t len, int32_t* count, int32_t
   } catch (const DagError& e) {
     return fail(e);
   }
+}
+
+// ---- Standard Evaluation (estimation.cpp) over the flat structs of dagplace_b200.h
+ProfileSet dpr_to_profiles(const dp_profiles_t* p) {
+  ProfileSet ps;
+  for (int32_t b = 0; b < p->n_batches; ++b) {
+    BatchProfile bp;
+    bp.batch_size = p->batch_size[b];
+    for (int64_t i = p->node_off[b]; i < p->node_off[b + 1]; ++i)
+      bp.nodes[p->node_id[i]] = NodeSample{p->memory_bytes[i], p->compute_us[i]};
+    ps.batches.push_back(std::move(bp));
+  }
+  return ps;
+}
+
+// fit_node_models (estimation.cpp:67-88); output sorted by id.
+int dpr_fit_node_models(const dp_profiles_t* p, dp_node_models_t** out) {
+  try {
+    const NodeCostModel m = fit_node_models(dpr_to_profiles(p));
+    std::vector<NodeId> ids;
+    for (const auto& kv : m.memory_fit) ids.push_back(kv.first);
+    std::sort(ids.begin(), ids.end());
+    auto* r = static_cast<dp_node_models_t*>(calloc(1, sizeof(dp_node_models_t)));
+    r->n = static_cast<int64_t>(ids.size());
+    r->node_id = static_cast<int64_t*>(calloc(ids.size() + 1, sizeof(int64_t)));
+    r->fit = static_cast<double*>(calloc(6 * ids.size() + 1, sizeof(double)));
+    for (size_t i = 0; i < ids.size(); ++i) {
+      const LinearFit& a = m.memory_fit.at(ids[i]);
+      const LinearFit& b = m.time_fit.at(ids[i]);
+      r->node_id[i] = ids[i];
+      double* f = r->fit + 6 * i;
+      f[0] = a.slope; f[1] = a.intercept; f[2] = a.residual_norm;
+      f[3] = b.slope; f[4] = b.intercept; f[5] = b.residual_norm;
+    }
+    *out = r;
+    return 0;
+  } catch (const DagError& e) { return fail(e); }
+}
+
+void dpr_node_models_free(dp_node_models_t* m) {
+  if (!m) return;
+  free(m->node_id); free(m->fit); free(m);
+}
+
+// estimate_graph (estimation.cpp:90-119).
+int dpr_estimate_graph(const dp_graph_t* base, const dp_node_models_t* models, int64_t target_batch,
+                       int64_t reference_batch, int64_t n_override, const int64_t* ov_src, const int64_t* ov_dst,
+                       const double* ov_factor, dp_graph_out_t** out) {
+  try {
+    NodeCostModel m;
+    for (int64_t i = 0; i < models->n; ++i) {
+      const double* f = models->fit + 6 * i;
+      m.memory_fit[models->node_id[i]] = LinearFit{f[0], f[1], f[2]};
+      m.time_fit[models->node_id[i]] = LinearFit{f[3], f[4], f[5]};
+    }
+    EdgeScaling sc;
+    sc.reference_batch = reference_batch;
+    for (int64_t i = 0; i < n_override; ++i) sc.scale_override[{ov_src[i], ov_dst[i]}] = ov_factor[i];
+    *out = flatten_graph(estimate_graph(to_graph(base), m, target_batch, sc));
+    return 0;
+  } catch (const DagError& e) { return fail(e); }
+}
+
+// fit_comm_model (estimation.cpp:121-140).
+int dpr_fit_comm_model(int64_t n, const int64_t* bytes, const double* us, dp_comm_t* out) {
+  try {
+    std::vector<std::pair<Bytes, double>> s;
+    for (int64_t i = 0; i < n; ++i) s.emplace_back(bytes[i], us[i]);
+    const CommModel c = fit_comm_model(s);
+    out->k_us_per_byte = c.k_us_per_byte;
+    out->b_us = c.b_us;
+    return 0;
+  } catch (const DagError& e) { return fail(e); }
+}
+
+// deviation_report (estimation.cpp:148-192).
+int dpr_deviation_report(const dp_graph_t* est, const dp_graph_t* meas, dp_deviation_t** out) {
+  try {
+    const DeviationReport d = deviation_report(to_graph(est), to_graph(meas));
+    auto* r = static_cast<dp_deviation_t*>(calloc(1, sizeof(dp_deviation_t)));
+    auto fill = [](const std::map<NodeId, double>& mp, int64_t* n, int64_t** ids, double** vals) {
+      *n = static_cast<int64_t>(mp.size());
+      *ids = static_cast<int64_t*>(calloc(mp.size() + 1, sizeof(int64_t)));
+      *vals = static_cast<double*>(calloc(mp.size() + 1, sizeof(double)));
+      int64_t k = 0;
+      for (const auto& kv : mp) { (*ids)[k] = kv.first; (*vals)[k] = kv.second; ++k; }
+    };
+    fill(d.memory_deviation, &r->n_memory, &r->memory_id, &r->memory_dev);
+    fill(d.time_deviation, &r->n_time, &r->time_id, &r->time_dev);
+    r->mean_memory = d.mean_memory_deviation;
+    r->mean_time = d.mean_time_deviation;
+    auto lst = [](const std::vector<NodeId>& v, int64_t* n, int64_t** ids) {
+      *n = static_cast<int64_t>(v.size());
+      *ids = static_cast<int64_t*>(calloc(v.size() + 1, sizeof(int64_t)));
+      for (size_t i = 0; i < v.size(); ++i) (*ids)[i] = v[i];
+    };
+    lst(d.zero_memory_nodes, &r->n_zero_memory, &r->zero_memory);
+    lst(d.zero_time_nodes, &r->n_zero_time, &r->zero_time);
+    *out = r;
+    return 0;
+  } catch (const DagError& e) { return fail(e); }
+}
+
+void dpr_deviation_free(dp_deviation_t* d) {
+  if (!d) return;
+  free(d->memory_id); free(d->memory_dev); free(d->time_id); free(d->time_dev);
+  free(d->zero_memory); free(d->zero_time); free(d);
 }
 
 int dpr_comm_time(int64_t bytes, dp_comm_t comm, int64_t* out) {

@@ -634,3 +634,131 @@ def devices_from_json(lib: C.CDLL, text, prefix: str = "dp_"):
         raise DagError(rc, (err() or b"").decode(errors="replace"))
     k = min(cnt.value, cap)
     return [(int(ids[i]), int(mem[i])) for i in range(k)], (comm.k_us_per_byte, comm.b_us)
+
+
+# ---------------------------------------------------------------- Standard Evaluation
+class ProfilesC(C.Structure):
+    _fields_ = [("n_batches", C.c_int32), ("batch_size", I64P), ("node_off", I64P), ("node_id", I64P),
+                ("memory_bytes", I64P), ("compute_us", I64P)]
+
+
+class NodeModelsC(C.Structure):
+    _fields_ = [("n", C.c_int64), ("node_id", I64P), ("fit", C.POINTER(C.c_double))]
+
+
+class DeviationC(C.Structure):
+    _fields_ = [("n_memory", C.c_int64), ("memory_id", I64P), ("memory_dev", C.POINTER(C.c_double)),
+                ("n_time", C.c_int64), ("time_id", I64P), ("time_dev", C.POINTER(C.c_double)),
+                ("mean_memory", C.c_double), ("mean_time", C.c_double),
+                ("n_zero_memory", C.c_int64), ("zero_memory", I64P),
+                ("n_zero_time", C.c_int64), ("zero_time", I64P)]
+
+
+@dataclass
+class Profiles:
+    """ProfileSet (estimation.hpp:25-28): batches of (node_id, memory_bytes, compute_us)."""
+    batch_size: np.ndarray
+    node_off: np.ndarray
+    node_id: np.ndarray
+    memory_bytes: np.ndarray
+    compute_us: np.ndarray
+
+    def c(self) -> ProfilesC:
+        for f in ("batch_size", "node_off", "node_id", "memory_bytes", "compute_us"):
+            setattr(self, f, np.ascontiguousarray(getattr(self, f), dtype=np.int64))
+        return ProfilesC(len(self.batch_size), self.batch_size.ctypes.data_as(I64P),
+                         self.node_off.ctypes.data_as(I64P), self.node_id.ctypes.data_as(I64P),
+                         self.memory_bytes.ctypes.data_as(I64P), self.compute_us.ctypes.data_as(I64P))
+
+
+class Estimation:
+    """Standard Evaluation entry points of one library: the product (dp_, GPU context
+    required) or the reference shim (dpr_, tests only)."""
+
+    def __init__(self, lib: C.CDLL, prefix: str, ctx=None):
+        self.lib, self.prefix, self.ctx = lib, prefix, ctx
+        pre = (C.c_void_p,) if ctx is not None else ()
+        self.f_fit = self._f("fit_node_models", pre + (C.POINTER(ProfilesC), C.POINTER(C.POINTER(NodeModelsC))))
+        self.f_est = self._f("estimate_graph", pre + (C.POINTER(GraphC), C.POINTER(NodeModelsC), C.c_int64, C.c_int64,
+                                                      C.c_int64, I64P, I64P, C.POINTER(C.c_double),
+                                                      C.POINTER(C.POINTER(GraphOutC))))
+        self.f_comm = self._f("fit_comm_model", pre + (C.c_int64, I64P, C.POINTER(C.c_double), C.POINTER(CommC)))
+        self.f_dev = self._f("deviation_report", pre + (C.POINTER(GraphC), C.POINTER(GraphC),
+                                                        C.POINTER(C.POINTER(DeviationC))))
+        self.f_free_models = getattr(lib, prefix + "node_models_free")
+        self.f_free_dev = getattr(lib, prefix + "deviation_free")
+        self.f_free_graph = getattr(lib, "dp_graph_out_free" if prefix == "dp_" else prefix + "free_graph_out")
+        for f in (self.f_free_models, self.f_free_dev, self.f_free_graph):
+            f.restype = None
+        err = getattr(lib, prefix + "last_error_message")
+        err.restype = C.c_char_p
+        self._err = err
+
+    def _f(self, name, argt):
+        f = getattr(self.lib, self.prefix + name)
+        f.restype = C.c_int
+        f.argtypes = list(argt)
+        return f
+
+    def _call(self, f, *a):
+        rc = f(self.ctx, *a) if self.ctx is not None else f(*a)
+        if rc:
+            raise DagError(rc, (self._err() or b"").decode(errors="replace"))
+
+    def fit_node_models(self, prof: Profiles):
+        """-> (node_id ascending, fit[n, 6])"""
+        out = C.POINTER(NodeModelsC)()
+        pc = prof.c()
+        self._call(self.f_fit, C.byref(pc), C.byref(out))
+        o = out.contents
+        ids = np.ctypeslib.as_array(o.node_id, shape=(o.n,)).copy() if o.n else np.zeros(0, np.int64)
+        fit = np.ctypeslib.as_array(o.fit, shape=(o.n * 6,)).reshape(o.n, 6).copy() if o.n else np.zeros((0, 6))
+        self.f_free_models(out)
+        return ids, fit
+
+    def estimate_graph(self, g: Graph, models, target_batch: int, reference_batch: int, overrides=()) -> Graph:
+        ids, fit = models
+        ids = np.ascontiguousarray(ids, np.int64)
+        fit = np.ascontiguousarray(fit, np.float64).reshape(-1)
+        mc = NodeModelsC(len(ids), ids.ctypes.data_as(I64P), fit.ctypes.data_as(C.POINTER(C.c_double)))
+        osrc = np.array([o[0] for o in overrides], np.int64)
+        odst = np.array([o[1] for o in overrides], np.int64)
+        ofac = np.array([o[2] for o in overrides], np.float64)
+        out = C.POINTER(GraphOutC)()
+        gc = g.c()
+        self._call(self.f_est, C.byref(gc), C.byref(mc), target_batch, reference_batch, len(osrc),
+                   osrc.ctypes.data_as(I64P), odst.ctypes.data_as(I64P), ofac.ctypes.data_as(C.POINTER(C.c_double)),
+                   C.byref(out))
+        o = out.contents
+        n, m = o.n_nodes, o.n_edges
+
+        def arr(ptr, k, dt):
+            return np.ctypeslib.as_array(ptr, shape=(k,)).astype(dt, copy=True) if k else np.zeros(0, dt)
+        r = Graph(arr(o.node_id, n, np.int64), arr(o.compute_us, n, np.int64), arr(o.memory_bytes, n, np.int64),
+                  arr(o.edge_src, m, np.int64), arr(o.edge_dst, m, np.int64), arr(o.edge_bytes, m, np.int64))
+        self.f_free_graph(out)
+        return r
+
+    def fit_comm_model(self, samples):
+        b = np.array([x[0] for x in samples], np.int64)
+        u = np.array([x[1] for x in samples], np.float64)
+        out = CommC()
+        self._call(self.f_comm, len(b), b.ctypes.data_as(I64P), u.ctypes.data_as(C.POINTER(C.c_double)),
+                   C.byref(out))
+        return out.k_us_per_byte, out.b_us
+
+    def deviation_report(self, est: Graph, meas: Graph):
+        out = C.POINTER(DeviationC)()
+        a, b = est.c(), meas.c()
+        self._call(self.f_dev, C.byref(a), C.byref(b), C.byref(out))
+        o = out.contents
+
+        def arr(ptr, k, dt):
+            return np.ctypeslib.as_array(ptr, shape=(k,)).astype(dt, copy=True) if k else np.zeros(0, dt)
+        r = dict(memory=(arr(o.memory_id, o.n_memory, np.int64), arr(o.memory_dev, o.n_memory, np.float64)),
+                 time=(arr(o.time_id, o.n_time, np.int64), arr(o.time_dev, o.n_time, np.float64)),
+                 mean_memory=o.mean_memory, mean_time=o.mean_time,
+                 zero_memory=arr(o.zero_memory, o.n_zero_memory, np.int64),
+                 zero_time=arr(o.zero_time, o.n_zero_time, np.int64))
+        self.f_free_dev(out)
+        return r

@@ -23,6 +23,9 @@ HEADER_SYMBOLS = [
     "dp_brute_force_optimal", "dp_pipeline", "dp_pipeline_result_free", "dp_resident_create",
     "dp_resident_generate", "dp_resident_fetch", "dp_resident_destroy", "dp_gen_layered",
     "dp_gen_candidates", "dp_gen_gnmt", "dp_gen_bert",
+    "dp_graph_from_json", "dp_devices_from_json",
+    "dp_fit_node_models", "dp_node_models_free", "dp_estimate_graph", "dp_fit_comm_model",
+    "dp_deviation_report", "dp_deviation_free",
 ]
 
 
