@@ -233,12 +233,12 @@ def ours(args):
     errs = []
     go = threading.Barrier(R + 1)
     done = threading.Barrier(R + 1)
-    stop = [False]
+    pool_stop = [False]
 
     def worker(rres):
         while True:
             go.wait()
-            if stop[0]:
+            if pool_stop[0]:
                 return
             rc = lib.dp_resident_generate(rres)
             if rc:
@@ -291,7 +291,7 @@ def ours(args):
             print(f"under load (R={R}): stage {nm:18s} {ms_:10.3f} ms", file=sys.stderr)
         lib.dp_ctx_enable_stage_timing(reps[0][1].ctx, 0)
     launches = sum(lib.dp_ctx_launch_count(rb.ctx) for _, rb, _ in reps) - l0
-    stop[0] = True
+    pool_stop[0] = True
     go.wait()
     for t_ in pool:
         t_.join()

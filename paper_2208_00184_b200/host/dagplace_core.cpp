@@ -610,36 +610,9 @@ std::pair<Placement, Duration> brute_force_optimal(const ComputationGraph& graph
 }
 
 // ---------------------------------------------------------------- estimation.hpp
-// Standard Evaluation (estimation.cpp) — host drop-in: per-node least squares over the
-// profiled batches, same summation order and fp64 operations as the reference.
-namespace {
-LinearFit fit_line(const std::vector<std::pair<double, double>>& pts) {
-  const double cnt = static_cast<double>(pts.size());
-  double sx = 0, sy = 0;
-  for (const auto& xy : pts) {
-    sx += xy.first;
-    sy += xy.second;
-  }
-  const double mx = sx / cnt, my = sy / cnt;
-  double sxx = 0, sxy = 0;
-  for (const auto& xy : pts) {
-    const double dx = xy.first - mx;
-    sxx += dx * dx;
-    sxy += dx * (xy.second - my);
-  }
-  LinearFit fit;
-  fit.slope = sxx > 0 ? sxy / sxx : 0.0;
-  fit.intercept = my - fit.slope * mx;
-  double ss = 0;
-  for (const auto& xy : pts) {
-    const double r = xy.second - fit.predict(xy.first);
-    ss += r * r;
-  }
-  fit.residual_norm = std::sqrt(ss);
-  return fit;
-}
-}  // namespace
-
+// Standard Evaluation (estimation.cpp) on the GPU (estimation.cu through the C-ABI).
+// The profile-universe checks run here first, over the same unordered_maps as the
+// reference, so a missing node is named in the reference's (hash) order.
 NodeCostModel fit_node_models(const ProfileSet& profiles) {
   std::set<std::int64_t> sizes;
   for (const auto& b : profiles.batches) sizes.insert(b.batch_size);
@@ -656,53 +629,75 @@ NodeCostModel fit_node_models(const ProfileSet& profiles) {
         throw DagError(ErrorKind::NodeUniverseMismatch, "node " + std::to_string(kv.first) + " missing from batch " +
                                                             std::to_string(b.batch_size));
   }
-  NodeCostModel model;
-  for (const auto& kv : universe) {
-    std::vector<std::pair<double, double>> mp, tp;
-    for (const auto& b : profiles.batches) {
-      const NodeSample& s = b.nodes.at(kv.first);
-      mp.emplace_back(static_cast<double>(b.batch_size), static_cast<double>(s.memory_bytes));
-      tp.emplace_back(static_cast<double>(b.batch_size), static_cast<double>(s.compute_us));
+  std::vector<int64_t> bs, off{0}, id, mem, w;
+  for (const auto& b : profiles.batches) {
+    bs.push_back(b.batch_size);
+    for (const auto& kv : b.nodes) {
+      id.push_back(kv.first);
+      mem.push_back(kv.second.memory_bytes);
+      w.push_back(kv.second.compute_us);
     }
-    model.memory_fit[kv.first] = fit_line(mp);
-    model.time_fit[kv.first] = fit_line(tp);
+    off.push_back(static_cast<int64_t>(id.size()));
   }
+  dp_profiles_t pc{static_cast<int32_t>(bs.size()), bs.data(), off.data(), id.data(), mem.data(), w.data()};
+  dp_node_models_t* m = nullptr;
+  check(dp_fit_node_models(ctx(), &pc, &m));
+  NodeCostModel model;
+  for (int64_t i = 0; i < m->n; ++i) {
+    const double* f = m->fit + 6 * i;
+    model.memory_fit[m->node_id[i]] = LinearFit{f[0], f[1], f[2]};
+    model.time_fit[m->node_id[i]] = LinearFit{f[3], f[4], f[5]};
+  }
+  dp_node_models_free(m);
   return model;
 }
 
 ComputationGraph estimate_graph(const ComputationGraph& base, const NodeCostModel& models, std::int64_t target_batch,
                                 const EdgeScaling& scaling) {
-  if (target_batch <= 0) throw DagError(ErrorKind::InvalidValue, "target batch must be > 0");
-  if (scaling.reference_batch <= 0) throw DagError(ErrorKind::InvalidValue, "reference batch must be > 0");
+  Flat f(base);
+  std::vector<int64_t> mid;
+  for (const auto& kv : models.memory_fit)
+    if (models.time_fit.count(kv.first)) mid.push_back(kv.first);
+  std::sort(mid.begin(), mid.end());
+  std::vector<double> fit(mid.size() * 6);
+  for (size_t i = 0; i < mid.size(); ++i) {
+    const LinearFit& a = models.memory_fit.at(mid[i]);
+    const LinearFit& b = models.time_fit.at(mid[i]);
+    double* x = fit.data() + 6 * i;
+    x[0] = a.slope; x[1] = a.intercept; x[2] = a.residual_norm;
+    x[3] = b.slope; x[4] = b.intercept; x[5] = b.residual_norm;
+  }
+  dp_node_models_t mc{static_cast<int64_t>(mid.size()), mid.data(), fit.data()};
+  std::vector<int64_t> os, od;
+  std::vector<double> of;
+  for (const auto& kv : scaling.scale_override) {
+    os.push_back(kv.first.first);
+    od.push_back(kv.first.second);
+    of.push_back(kv.second);
+  }
+  dp_graph_out_t* o = nullptr;
+  check(dp_estimate_graph(ctx(), &f.g, &mc, target_batch, scaling.reference_batch, static_cast<int64_t>(os.size()),
+                          os.data(), od.data(), of.data(), &o));
   ComputationGraph est = base;
-  for (auto& n : est.nodes) {
-    auto mf = models.memory_fit.find(n.id);
-    auto tf = models.time_fit.find(n.id);
-    if (mf == models.memory_fit.end() || tf == models.time_fit.end())
-      throw DagError(ErrorKind::UnknownNode, "no fitted model for node " + std::to_string(n.id));
-    n.memory_bytes = std::max<Bytes>(0, std::llround(mf->second.predict(static_cast<double>(target_batch))));
-    n.compute_us = std::max<Duration>(0, std::llround(tf->second.predict(static_cast<double>(target_batch))));
+  for (size_t i = 0; i < est.nodes.size(); ++i) {
+    est.nodes[i].memory_bytes = o->memory_bytes[i];
+    est.nodes[i].compute_us = o->compute_us[i];
   }
-  const double ratio = static_cast<double>(target_batch) / static_cast<double>(scaling.reference_batch);
-  for (auto& e : est.edges) {
-    double factor = ratio;
-    auto ov = scaling.scale_override.find({e.src, e.dst});
-    if (ov != scaling.scale_override.end()) factor = ov->second;
-    e.tensor_bytes = std::max<Bytes>(0, std::llround(static_cast<double>(e.tensor_bytes) * factor));
-  }
+  for (size_t e = 0; e < est.edges.size(); ++e) est.edges[e].tensor_bytes = o->edge_bytes[e];
+  dp_graph_out_free(o);
   return est;
 }
 
 CommModel fit_comm_model(const std::vector<std::pair<Bytes, double>>& samples) {
-  if (samples.size() < 2) throw DagError(ErrorKind::InsufficientSamples, "need at least 2 transfer samples");
-  std::set<Bytes> distinct;
-  for (const auto& s : samples) distinct.insert(s.first);
-  if (distinct.size() < 2)
-    throw DagError(ErrorKind::InsufficientSamples, "transfer samples need 2 distinct byte counts");
-  std::vector<std::pair<double, double>> pts;
-  for (const auto& s : samples) pts.emplace_back(static_cast<double>(s.first), s.second);
-  const LinearFit fit = fit_line(pts);
-  return CommModel{std::max(0.0, fit.slope), std::max(0.0, fit.intercept)};
+  std::vector<int64_t> b;
+  std::vector<double> u;
+  for (const auto& s : samples) {
+    b.push_back(s.first);
+    u.push_back(s.second);
+  }
+  dp_comm_t c{};
+  check(dp_fit_comm_model(ctx(), static_cast<int64_t>(b.size()), b.data(), u.data(), &c));
+  return CommModel{c.k_us_per_byte, c.b_us};
 }
 
 PlacementResult sequential_eval_placement(const ComputationGraph& estimated, const std::vector<DeviceSpec>& devices) {
@@ -710,40 +705,17 @@ PlacementResult sequential_eval_placement(const ComputationGraph& estimated, con
 }
 
 DeviationReport deviation_report(const ComputationGraph& estimated, const ComputationGraph& measured) {
-  std::unordered_map<NodeId, const OpNode*> actual;
-  for (const auto& n : measured.nodes) actual[n.id] = &n;
-  if (actual.size() != estimated.nodes.size())
-    throw DagError(ErrorKind::NodeUniverseMismatch, "estimated and measured graphs have different node counts");
+  Flat fe(estimated), fm(measured);
+  dp_deviation_t* d = nullptr;
+  check(dp_deviation_report(ctx(), &fe.g, &fm.g, &d));
   DeviationReport r;
-  double ms = 0, ts = 0;
-  std::int64_t mc = 0, tc = 0;
-  for (const auto& e : estimated.nodes) {
-    auto it = actual.find(e.id);
-    if (it == actual.end())
-      throw DagError(ErrorKind::NodeUniverseMismatch, "node " + std::to_string(e.id) + " missing from measured graph");
-    const OpNode& m = *it->second;
-    if (m.memory_bytes == 0) {
-      r.zero_memory_nodes.push_back(e.id);
-    } else {
-      const double d = std::abs(static_cast<double>(e.memory_bytes - m.memory_bytes)) /
-                       static_cast<double>(m.memory_bytes);
-      r.memory_deviation[e.id] = d;
-      ms += d;
-      ++mc;
-    }
-    if (m.compute_us == 0) {
-      r.zero_time_nodes.push_back(e.id);
-    } else {
-      const double d = std::abs(static_cast<double>(e.compute_us - m.compute_us)) / static_cast<double>(m.compute_us);
-      r.time_deviation[e.id] = d;
-      ts += d;
-      ++tc;
-    }
-  }
-  std::sort(r.zero_memory_nodes.begin(), r.zero_memory_nodes.end());
-  std::sort(r.zero_time_nodes.begin(), r.zero_time_nodes.end());
-  r.mean_memory_deviation = mc ? ms / mc : 0.0;
-  r.mean_time_deviation = tc ? ts / tc : 0.0;
+  for (int64_t i = 0; i < d->n_memory; ++i) r.memory_deviation[d->memory_id[i]] = d->memory_dev[i];
+  for (int64_t i = 0; i < d->n_time; ++i) r.time_deviation[d->time_id[i]] = d->time_dev[i];
+  r.mean_memory_deviation = d->mean_memory;
+  r.mean_time_deviation = d->mean_time;
+  r.zero_memory_nodes.assign(d->zero_memory, d->zero_memory + d->n_zero_memory);
+  r.zero_time_nodes.assign(d->zero_time, d->zero_time + d->n_zero_time);
+  dp_deviation_free(d);
   return r;
 }
 
