@@ -478,11 +478,7 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem& S) {
   int32_t* const seq = a.seq;
   int32_t* const pos_of = a.pos_of;
   const int4* const ell6 = a.ell6;
-  // The loop is unrolled by two with a separate register set for the children's rows
-  // of each half, kept live across the other half: an unconsumed row load (no child
-  // freed) is never overwritten while in flight, so no step waits on the previous one's.
-  int4 crowA = make_int4(-1, 0, -1, 0), crowB = crowA;
-  auto step = [&](int4& crow) {
+  while (top >= 0) {
     if (top < base) {
       base = max(0, top + 1 - SC / 2);
       v6_fill(a, S, base, top, lane);
@@ -560,11 +556,11 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem& S) {
         if (big) base = top + 1;
         __syncwarp();
       }
-      return;
+      continue;
     }
     // ---- 8-slot row on chip (slots sorted by rank)
     const int q = lane >> 2;
-    crow = make_int4(-1, 0, -1, 0);
+    int4 crow = make_int4(-1, 0, -1, 0);
     if (cq.x >= 0) crow = ell6[static_cast<int64_t>(cq.x) * 4 + (lane & 3)];
     bool fr = false;
     if (lane < 8 && my.x >= 0) {
@@ -612,13 +608,6 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem& S) {
       top += nf;
     }
     __syncwarp();
-  };
-  while (top >= 0) {
-    step(crowA);
-    asm volatile("" ::"r"(crowB.x), "r"(crowB.y), "r"(crowB.z), "r"(crowB.w));
-    if (top < 0) break;
-    step(crowB);
-    asm volatile("" ::"r"(crowA.x), "r"(crowA.y), "r"(crowA.z), "r"(crowA.w));
   }
   __syncwarp();
   if (lane < (p & 31)) {

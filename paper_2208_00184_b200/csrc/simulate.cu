@@ -267,10 +267,12 @@ void run_sim(DevGraph& g, const SimInput& in, SimOutput& out, int32_t Q, int64_t
   const int32_t n = g.n, m = g.m, D = in.D, E = 3 * D;
   if (E > 32) fail(DP_E_UNSUPPORTED, "simulate supports at most 10 devices per placement (got %d)", D);
   if (n == 0 || count == 0) return;
-  int64_t warps = std::min<int64_t>(count, static_cast<int64_t>(ctx->num_sms) * 8);
-  // bound the ring workspace to ~4 GiB
+  // Each warp's event loop is latency-bound (dependent HBM/L2 accesses per event), so
+  // throughput comes from concurrency: up to 32 resident warps per SM.
+  int64_t warps = std::min<int64_t>(count, static_cast<int64_t>(ctx->num_sms) * 32);
+  // bound the per-warp workspace (rings + dependency counters) to ~16 GiB of HBM
   const int64_t per_warp = static_cast<int64_t>(E) * Q * sizeof(QE) + 5ll * n;
-  while (warps > 1 && warps * per_warp > (4ll << 30)) warps /= 2;
+  while (warps > 1 && warps * per_warp > (16ll << 30)) warps /= 2;
   const int64_t blocks = (warps + kWarpsPerBlock - 1) / kWarpsPerBlock;
   warps = blocks * kWarpsPerBlock;
   DevBuf<int32_t> indeg(ctx, n), deps(ctx, (size_t)warps * n);
