@@ -18,6 +18,7 @@
 // reference loop breaks at k0 (first PM[k] > earliest) when S[k0] - earliest >= dur,
 // otherwise at the first k > k0 with GQ[k] >= dur, returning PM[k-1] — else PM[K-1].
 #include <algorithm>
+#include <cstdlib>
 
 #include "placement.cuh"
 
@@ -304,6 +305,8 @@ struct PlaceArgs {
   const int64_t* back;  // max out-edge cost per node (>= 0)
   const int64_t* cap;   // [D] sorted by id
   TLArrays tl[2];
+  bool meta_smem;  // timeline block meta in dynamic shared memory (small coarse graphs)
+  long long* debug;  // optional: cycles of each CTA
   int64_t* finish;      // [n] (adjust)
   int32_t* dev[2];      // [n] device position by node index (order, adjust)
   int64_t* pdm[2];      // [D]
@@ -330,11 +333,23 @@ __global__ void __launch_bounds__(256) k_place(PlaceArgs a) {
   __shared__ int32_t s_chosen, s_be;
   __shared__ int64_t s_start;
   const int which = blockIdx.x;  // 0 order_place, 1 adjusting_placement
+  const long long t0 = clock64();
   if (!a.run[which]) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int32_t D = a.D;
   TLArrays tl = a.tl[which];
   tl.nb = snb;
+  if (a.meta_smem) {  // same layout as the global meta, carved from dynamic shared memory
+    extern __shared__ int64_t dyn[];
+    const int64_t mc = static_cast<int64_t>(D) * tl.maxb;
+    tl.maxE = dyn;
+    tl.pmEnd = dyn + mc;
+    tl.fS = dyn + 2 * mc;
+    tl.fE = dyn + 3 * mc;
+    tl.gub = dyn + 4 * mc;
+    tl.id = reinterpret_cast<int32_t*>(dyn + 5 * mc);
+    tl.cnt = tl.id + mc;
+  }
   for (int d = tid; d < D; d += blockDim.x) {
     sK[d] = 0;
     snb[d] = 0;
@@ -380,6 +395,7 @@ __global__ void __launch_bounds__(256) k_place(PlaceArgs a) {
     }
     for (int d = lane; d < D; d += 32) a.pdm[0][d] = spdm[d];
     if (lane == 0) a.flags[0][0] = oom ? 1 : 0;
+    if (lane == 0 && a.debug) a.debug[0] = clock64() - t0;
     return;
   }
   // adjusting_placement (placement.cpp:172-216)
@@ -471,6 +487,7 @@ __global__ void __launch_bounds__(256) k_place(PlaceArgs a) {
   }
   for (int d = tid; d < D; d += blockDim.x) a.pdm[1][d] = spdm[d];
   if (tid == 0) a.flags[1][0] = oom ? 1 : 0;
+  if (tid == 0 && a.debug) a.debug[1] = clock64() - t0;
 }
 
 __global__ void k_back_cost(const int32_t* out_off, const int64_t* out_cost, int32_t n, int64_t* back) {
@@ -584,7 +601,28 @@ void place_dev(DevGraph& g, const int32_t* seq, const Devices& devs, PlaceOut* o
     a.dec_be = adjust_out->dec_be.p;
   }
   StageScope st(ctx, "placement", 0.0);
-  DP_LAUNCH(ctx, k_place, 2, 256, 0, a);
+  // block meta on chip when it fits: (5 x 8 + 2 x 4) bytes per block slot
+  const size_t meta_bytes = static_cast<size_t>(48) * D * std::max(a.tl[0].maxb, a.tl[1].maxb);
+  a.meta_smem = meta_bytes <= 190 * 1024 && getenv("DP_PLACE_GLOBAL_META") == nullptr;
+  const size_t dyn = a.meta_smem ? meta_bytes : 0;
+  if (dyn) {
+    static size_t attr = 0;
+    if (dyn > attr) {
+      DP_CUDA(cudaFuncSetAttribute(k_place, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
+      attr = dyn;
+    }
+  }
+  DevBuf<long long> dbg(ctx, 2);
+  a.debug = getenv("DP_DEBUG_PLACE") ? dbg.p : nullptr;
+  if (a.debug) dbg.zero();
+  DP_LAUNCH(ctx, k_place, 2, 256, dyn, a);
+  if (a.debug) {
+    long long h[2];
+    dbg.download(h, 2);
+    sync(ctx);
+    fprintf(stderr, "[place] order_place %.2f ms, adjusting %.2f ms (n=%d, D=%d, meta %s)\n", h[0] / 1.965e6,
+            h[1] / 1.965e6, n, D, a.meta_smem ? "smem" : "global");
+  }
 }
 
 void expand_dev(DevGraph& g, const int32_t* node_cluster, const int32_t* coarse_dev, int32_t D, int32_t* dev_node,
