@@ -55,6 +55,8 @@ def parse():
     p.add_argument("--stages", action="store_true", help="print per-stage device times to stderr")
     p.add_argument("--stages-under-load", action="store_true",
                    help="print replica 0's per-stage device times during the throughput steps")
+    p.add_argument("--ref-sample", type=int, default=250_000,
+                   help="ops per reference copy in --impl reference / cpu_baseline (bounded CPU sample)")
     p.add_argument("--replicas", type=int, default=32,
                    help="independent graphs generated concurrently per GPU (one stream + host thread each)")
     return p.parse_args()
@@ -416,7 +418,7 @@ def ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args)
+        cpu = cpu_baseline(args, sample_nodes=args.ref_sample)
 
     if rank == 0:
         line = {
@@ -520,7 +522,7 @@ def reference_arm(args):
     import torch  # noqa: F401
     steps = []
     for i in range(args.warmup + args.steps):
-        r = cpu_baseline(args, sample_nodes=50_000 if i < args.warmup else 250_000)
+        r = cpu_baseline(args, sample_nodes=min(50_000, args.ref_sample) if i < args.warmup else args.ref_sample)
         if i >= args.warmup:
             steps.append(r)
     value = float(np.mean([s["value"] for s in steps]))
