@@ -65,6 +65,10 @@ struct dp_ctx {
   // Host waits block on this event (cudaEventBlockingSync) instead of spinning: many
   // contexts driven by more host threads than cores must not burn the cores they share.
   cudaEvent_t sync_ev = nullptr;
+  // A private stream-ordered pool per context: with the device's shared default pool, a
+  // block freed on one context's stream could be handed to another context's stream
+  // with an inserted cross-stream dependency, coupling independent replicas.
+  cudaMemPool_t pool = nullptr;
 };
 
 namespace dpb {
@@ -131,7 +135,9 @@ struct DevBuf {
     ctx = c;
     n = count;
     if (count) {
-      cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), c->stream);
+      cudaError_t e = c->pool ? cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p), count * sizeof(T), c->pool,
+                                                        c->stream)
+                              : cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), c->stream);
       if (e != cudaSuccess) {
         p = nullptr;
         fail(DP_E_OUT_OF_MEMORY, "device allocation of %zu bytes failed: %s", count * sizeof(T),

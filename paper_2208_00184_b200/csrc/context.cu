@@ -160,10 +160,18 @@ int dp_ctx_create(int device, void* stream, dp_ctx_t** out) {
     ctx->num_sms = prop.multiProcessorCount;
     if (getenv("DP_SPIN_SYNC") == nullptr)
       DP_CUDA(cudaEventCreateWithFlags(&ctx->sync_ev, cudaEventBlockingSync | cudaEventDisableTiming));
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      uint64_t threshold = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+    {
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = device;
+      if (cudaMemPoolCreate(&ctx->pool, &props) == cudaSuccess) {
+        uint64_t threshold = UINT64_MAX;  // keep freed blocks cached for the next call
+        cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+      } else {
+        ctx->pool = nullptr;
+        cudaGetLastError();
+      }
     }
     *out = ctx;
     return DP_OK;
@@ -180,6 +188,7 @@ void dp_ctx_destroy(dp_ctx_t* ctx) {
   ctx->pending.clear();
   if (ctx->pin) cudaFreeHost(ctx->pin);
   if (ctx->sync_ev) cudaEventDestroy(ctx->sync_ev);
+  if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
   for (auto& s : ctx->stages) ctx->event_pool.push_back(s);
   for (auto& s : ctx->event_pool) {
     cudaEventDestroy(s.a);

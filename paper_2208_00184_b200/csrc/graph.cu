@@ -234,11 +234,40 @@ __device__ __forceinline__ void kahn_relax_warp(const KahnArgs& a, int32_t u, in
   const bool small = u >= 0 && ke - kb <= 8;
   int32_t fv[8];
   bool ff[8];
+  // Phases (all loads, then all relaxations, then all in-degree decrements, then the
+  // checks) so the up-to-8 independent atomics of a row are in flight together instead
+  // of one round trip each.
+  int64_t cv[8];
+  int32_t old[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    ff[q] = false;
-    if (small && kb + q < ke) kahn_relax_edge(a, kb + q, t, &ff[q], &fv[q]);
+    const bool act = small && kb + q < ke;
+    fv[q] = act ? a.out_dst[kb + q] : 0;
+    cv[q] = act && a.tlevel ? a.out_cost[kb + q] : 0;
   }
+  // predicated PTX atomics: no branch around each one, so all issue back to back
+  if (a.tlevel) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int on = small && kb + q < ke;
+      asm volatile("{ .reg .pred p; setp.ne.b32 p, %2, 0; @p red.global.max.s64 [%0], %1; }" ::"l"(
+                       a.tlevel + fv[q]),
+                   "l"(t + cv[q]), "r"(on)
+                   : "memory");
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int on = small && kb + q < ke;
+    int r = 0;
+    asm volatile("{ .reg .pred p; setp.ne.b32 p, %2, 0; @p atom.global.add.s32 %0, [%1], -1; }"
+                 : "+r"(r)
+                 : "l"(a.indeg + fv[q]), "r"(on)
+                 : "memory");
+    old[q] = r;
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) ff[q] = old[q] == 1;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const int slot = warp_append(tail, ff[q]);
@@ -271,14 +300,19 @@ __device__ __forceinline__ void kahn_pull_warp(const KahnArgs& a, int32_t v) {
   }
   const bool small = v >= 0 && ke - kb <= 8;
   if (small) {
-    int64_t best = 0;
+    int32_t x[8];
+    int64_t c[8], bl[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      if (kb + q < ke) {
-        const int64_t c = a.blevel[a.out_dst[kb + q]] + a.out_cost[kb + q];
-        best = c > best ? c : best;
-      }
+      x[q] = kb + q < ke ? a.out_dst[kb + q] : -1;
+      c[q] = kb + q < ke ? a.out_cost[kb + q] : 0;
     }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) bl[q] = x[q] >= 0 ? a.blevel[x[q]] : 0;
+    int64_t best = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (x[q] >= 0) best = bl[q] + c[q] > best ? bl[q] + c[q] : best;
     a.blevel[v] = best + a.w[v];
   }
   unsigned big = __ballot_sync(0xffffffffu, v >= 0 && !small);
