@@ -143,24 +143,28 @@ def _new_ctx(lib, device, stream):
     return ctx
 
 
-def ncu_traffic(kernel: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` (bytes per launch) from the
-    newest committed `ncu --set full` summary under profiles/ (tools/summarize_profiles.py),
-    with the file it came from; (None, None) when no capture of that kernel exists."""
+def ncu_traffic(kernel: str, launches: int = 1):
+    """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` summed over its first
+    `launches` launches, from the newest committed `ncu --set full` summary under profiles/
+    (tools/summarize_profiles.py), with the file it came from; (None, None) when no capture
+    of that kernel exists."""
     import glob
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_full.txt")), reverse=True):
-        cur, got = None, {}
+        per, cur = [], None
         for line in open(path):
             if line.startswith("## "):
-                cur = line
+                cur = {} if kernel in line else None
+                if cur is not None:
+                    per.append(cur)
                 continue
-            if cur and kernel in cur:
-                parts = line.split()
-                if parts and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum") and len(parts) >= 3:
-                    got[parts[0]] = float(parts[1]) * scale.get(parts[2], 1)
-        if len(got) == 2:
-            return got["dram__bytes_read.sum"] + got["dram__bytes_write.sum"], os.path.relpath(path, ROOT)
+            parts = line.split()
+            if cur is not None and parts and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum") \
+                    and len(parts) >= 3:
+                cur[parts[0]] = float(parts[1]) * scale.get(parts[2], 1)
+        per = [d for d in per if len(d) == 2][:launches]
+        if len(per) == launches:
+            return sum(d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in per), os.path.relpath(path, ROOT)
     return None, None
 
 
@@ -354,11 +358,8 @@ def ours(args):
     roofline["traffic"], roofline["traffic_source"] = ncu_traffic("k_peel_dp")
     roofline["ns_per_node"] = round(dom[1] * 1e6 / g.n, 2)
     levels_roof = roof("levels", lv[0], lv[1]) if lv else None
-    if levels_roof:  # the stage is the forward + backward frontier kernels of the fine graph
-        tf, src = ncu_traffic("k_kahn_fwd_narrow")
-        tb, _ = ncu_traffic("k_kahn_bwd_narrow")
-        levels_roof["traffic"] = tf + tb if tf is not None and tb is not None else None
-        levels_roof["traffic_source"] = src
+    if levels_roof:  # the stage is the forward + backward dataflow kernels of the fine graph
+        levels_roof["traffic"], levels_roof["traffic_source"] = ncu_traffic("k_levels_flow", 2)
 
     # e2e through the public C-ABI (dp_pipeline): pinned H2D + generation + D2H of the report
     e2e = None

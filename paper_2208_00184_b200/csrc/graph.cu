@@ -347,10 +347,19 @@ constexpr int kSeqMaxN = 16384;  // power of two: the value ring is indexed with
 constexpr int kSeqTile = 4096;   // edges staged per tile
 constexpr int kSeqTileN = 2048;  // nodes staged per tile
 
-__global__ void k_index_topo(const int32_t* in_off, const int32_t* in_src, int32_t n, int* ok) {
+// ok = 0 unless every edge u->v has u < v; span += sum of (v - u) (how far ahead of a node
+// its inputs lie in index order, sizing the dataflow kernel's lookahead)
+__global__ void k_index_topo(const int32_t* in_off, const int32_t* in_src, int32_t n, int* ok,
+                             unsigned long long* span) {
+  unsigned long long s = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
-    for (int32_t k = in_off[v]; k < in_off[v + 1]; ++k)
-      if (in_src[k] >= v) atomicExch(ok, 0);
+    for (int32_t k = in_off[v]; k < in_off[v + 1]; ++k) {
+      const int32_t u = in_src[k];
+      if (u >= v) atomicExch(ok, 0);
+      else s += static_cast<unsigned long long>(v - u);
+    }
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(span, s);
 }
 
 __device__ __forceinline__ int64_t warp_max_nonneg(int64_t x) {
@@ -436,6 +445,108 @@ __global__ void __launch_bounds__(1024) k_levels_seq(int32_t n, const int32_t* o
     }
     __syncthreads();
     done = hi;
+  }
+}
+
+// ---- dataflow levels (graphs whose index order is topological, any width).  No level
+// barriers: warps take 32-node chunks in sweep order from a ticket counter, and a node's
+// value is published in HBM/L2 as soon as its last input is known (-1 = not yet), so the
+// critical path is the DAG's depth x one L2 round trip instead of depth x (frontier
+// kernel step + barrier).  A chunk waits only on lower tickets, which are held by running
+// warps, so there is no deadlock; a second counter (chunks finished) keeps the ticket
+// holders within `ahead` chunks of the finished ones, which bounds the number of warps
+// polling at once (the wavefront of a deep graph is narrow).  Each lane keeps up to 8 of
+// its in-edges in flight; the warp loop is uniform, so lanes of one warp may depend on
+// each other.
+__device__ __forceinline__ int64_t ld_relaxed_i64(const int64_t* p) {
+  int64_t x;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(x) : "l"(p) : "memory");
+  return x;
+}
+__device__ __forceinline__ void st_relaxed_i64(int64_t* p, int64_t x) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(x) : "memory");
+}
+__device__ __forceinline__ int ld_relaxed_i32(const int* p) {
+  int x;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(x) : "l"(p) : "memory");
+  return x;
+}
+
+// forward (rev = false): in-CSC rows, val = tlevel + w, out = tlevel
+// backward (rev = true): out-CSR rows, val = out = blevel
+__global__ void __launch_bounds__(128) k_levels_flow(int32_t n, const int32_t* off, const int32_t* nbr,
+                                                    const int64_t* cost, const int64_t* w, int64_t* val,
+                                                    int64_t* out, bool rev, int* ctr, int32_t ahead,
+                                                    unsigned sleep_cap) {
+  const int lane = threadIdx.x & 31;
+  const int32_t nchunks = (n + 31) >> 5;
+  for (;;) {
+    int c = 0;
+    if (lane == 0) {
+      c = atomicAdd(&ctr[0], 1);
+      if (c < nchunks)
+        while (ld_relaxed_i32(&ctr[1]) < c - ahead) __nanosleep(128);
+    }
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= nchunks) break;
+    const int32_t i = c * 32 + lane;
+    const bool valid = i < n;
+    const int32_t v = valid ? (rev ? n - 1 - i : i) : 0;
+    int32_t k = 0, e = 0;
+    int64_t wv = 0;
+    if (valid) {
+      k = off[v];
+      e = off[v + 1];
+      wv = w[v];
+    }
+    int64_t mx = 0;
+    bool done = !valid;
+    unsigned pend = 0;
+    int32_t u[8];
+    int64_t cc[8];
+    unsigned sleep_ns = 0;
+    for (;;) {
+      bool progress = false;
+      if (!done) {
+        if (pend == 0 && k < e) {
+          const int cnt = min(8, e - k);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            u[q] = q < cnt ? nbr[k + q] : 0;
+            cc[q] = q < cnt ? cost[k + q] : 0;
+          }
+          pend = (1u << cnt) - 1u;
+          k += cnt;
+        }
+        if (pend) {
+          int64_t x[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) x[q] = (pend >> q) & 1u ? ld_relaxed_i64(val + u[q]) : -1;
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (x[q] >= 0) {
+              mx = max(mx, x[q] + cc[q]);
+              pend &= ~(1u << q);
+              progress = true;
+            }
+        }
+        if (pend == 0 && k == e) {
+          const int64_t vv = mx + wv;
+          st_relaxed_i64(val + v, vv);
+          out[v] = rev ? vv : mx;
+          done = true;
+          progress = true;
+        }
+      }
+      if (__all_sync(0xffffffffu, done)) break;
+      if (__any_sync(0xffffffffu, progress)) {
+        sleep_ns = 0;
+      } else {
+        sleep_ns = sleep_ns ? min(sleep_ns * 2, sleep_cap) : 32u;
+        if (sleep_cap) __nanosleep(sleep_ns);
+      }
+    }
+    if (lane == 0) atomicAdd(&ctr[1], 1);
   }
 }
 
@@ -728,30 +839,57 @@ void graph_costs(DevGraph& g, dp_comm_t comm) {
   g.cb = comm.b_us;
 }
 
-// Levels by an index-order sweep when the node index order is topological and the graph
-// is small enough for on-chip values; returns false otherwise (caller uses graph_kahn).
+// Levels when the node index order is topological (every edge u->v has u < v): the
+// one-CTA sweep for small or chain-like graphs (the coarse graph of fuse), the dataflow
+// kernel otherwise.  Returns false when the index order is not topological (caller uses
+// graph_kahn).
 bool graph_levels_indexorder(DevGraph& g, int64_t* tlevel, int64_t* blevel, bool chainlike) {
   dp_ctx* ctx = g.ctx;
   const int32_t n = g.n;
   if (n == 0 || getenv("DP_LEVELS_KAHN")) return false;
-  // the sweep pays one warp step per node: taken for small graphs, and for graphs the
-  // caller knows to be chain-like (the coarse graph of fuse) at any size
-  if (n > kSeqMaxN && !chainlike) return false;
-  DevBuf<int> ok(ctx, 1);
-  int one = 1;
-  ok.upload(&one, 1);
-  DP_LAUNCH(ctx, k_index_topo, grid_for(n, 256), 256, 0, g.in_off.p, g.in_src.p, n, ok.p);
-  if (scalar_to_host(ctx, ok.p) != 1) return false;
-  const size_t sm = sizeof(int64_t) * (kSeqMaxN + kSeqTile + kSeqTileN) + sizeof(int32_t) * (kSeqTile + kSeqTileN + 1);
-  static bool attr = false;
-  if (!attr) {
-    DP_CUDA(cudaFuncSetAttribute(k_levels_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-    attr = true;
+  DevBuf<unsigned long long> chk(ctx, 2);  // [0] ok flag, [1] span sum
+  const unsigned long long init[2] = {1ull, 0ull};
+  chk.upload(init, 2);
+  DP_LAUNCH(ctx, k_index_topo, grid_for(n, 256), 256, 0, g.in_off.p, g.in_src.p, n, reinterpret_cast<int*>(chk.p),
+            chk.p + 1);
+  unsigned long long h[2];
+  chk.download(h, 2);
+  sync(ctx);
+  if (static_cast<int>(h[0]) != 1) return false;
+  const bool sweep = (n <= kSeqMaxN || chainlike) && getenv("DP_LEVELS_FLOW") == nullptr;
+  if (sweep) {
+    const size_t sm =
+        sizeof(int64_t) * (kSeqMaxN + kSeqTile + kSeqTileN) + sizeof(int32_t) * (kSeqTile + kSeqTileN + 1);
+    static bool attr = false;
+    if (!attr) {
+      DP_CUDA(cudaFuncSetAttribute(k_levels_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+      attr = true;
+    }
+    DevBuf<int64_t> gval;
+    if (n > kSeqMaxN) gval.alloc(ctx, n);
+    DP_LAUNCH(ctx, k_levels_seq, 1, 1024, sm, n, g.in_off.p, g.in_src.p, g.in_cost.p, g.w.p, tlevel, false, gval.p);
+    DP_LAUNCH(ctx, k_levels_seq, 1, 1024, sm, n, g.out_off.p, g.out_dst.p, g.out_cost.p, g.w.p, blevel, true, gval.p);
+    g.processed = n;
+    return true;
   }
-  DevBuf<int64_t> gval;
-  if (n > kSeqMaxN) gval.alloc(ctx, n);
-  DP_LAUNCH(ctx, k_levels_seq, 1, 1024, sm, n, g.in_off.p, g.in_src.p, g.in_cost.p, g.w.p, tlevel, false, gval.p);
-  DP_LAUNCH(ctx, k_levels_seq, 1, 1024, sm, n, g.out_off.p, g.out_dst.p, g.out_cost.p, g.w.p, blevel, true, gval.p);
+  // lookahead: four mean edge spans, in 32-node chunks, at least 256 chunks
+  const double mean_span = g.m_ok > 0 ? static_cast<double>(h[1]) / g.m_ok : 32.0;
+  int32_t ahead = static_cast<int32_t>(std::min(1.0e6, std::max(256.0, 4.0 * mean_span / 32.0)));
+  if (const char* s = getenv("DP_FLOW_AHEAD")) ahead = atoi(s);
+  unsigned sleep_cap = 256;
+  if (const char* s = getenv("DP_FLOW_SLEEP")) sleep_cap = static_cast<unsigned>(atoi(s));
+  const int32_t nchunks = (n + 31) / 32;
+  const int32_t warps = std::max(1, std::min({nchunks, ahead + 32, ctx->num_sms * 32}));
+  const int blocks = (warps + 3) / 4;
+  DevBuf<int64_t> f(ctx, n);
+  DevBuf<int> ctr(ctx, 4);
+  f.fill_bytes(0xff);
+  ctr.zero();
+  DP_LAUNCH(ctx, k_levels_flow, blocks, 128, 0, n, g.in_off.p, g.in_src.p, g.in_cost.p, g.w.p, f.p, tlevel, false,
+            ctr.p, ahead, sleep_cap);
+  DP_CUDA(cudaMemsetAsync(blevel, 0xff, sizeof(int64_t) * n, ctx->stream));
+  DP_LAUNCH(ctx, k_levels_flow, blocks, 128, 0, n, g.out_off.p, g.out_dst.p, g.out_cost.p, g.w.p, blevel, blevel,
+            true, ctr.p + 2, ahead, sleep_cap);
   g.processed = n;
   return true;
 }

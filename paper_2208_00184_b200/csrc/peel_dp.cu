@@ -1607,7 +1607,7 @@ int32_t topo_order(DevGraph& g, int policy, const int64_t* cpath, int32_t* seq, 
   peel_prepare(g, policy, cpath, st);
   PeelArgs a = peel_args(g, st, seq, pos_of, false);
   {
-    StageScope s(ctx, policy == DP_TOPO_CPD ? "cpd_peel" : "peel", 0.0);
+    StageScope s(ctx, policy == DP_TOPO_CPD ? "cpd_peel" : "peel", 72.0 * g.n + 8.0 * g.m_ok);
     DP_LAUNCH(ctx, k_peel2, 1, 32, sm, a);
   }
   const int32_t emitted = scalar_to_host(ctx, st.counters.p + 1);
@@ -1664,7 +1664,9 @@ int32_t peel_dp_stream(DevGraph& g, const int64_t* cpath, int32_t range, int64_t
   da.progress = st.counters.p;
   void* args[] = {&pa, &da};
   {
-    StageScope s(ctx, "peel+dp (streamed)", 0.0);
+    // algorithmic bytes: peel 64 B row + 8 B seq/pos_of per node; DP 4+8+8+4 B per position
+    // (node, memory, out-cost sum, cut) + 12 B per in-edge (source position, cost)
+    StageScope s(ctx, "peel+dp (streamed)", 92.0 * n + 12.0 * g.m_ok);
     DP_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_peel_dp), 2, kDpWarps * 32, args, sm,
                                         ctx->stream));
     ++ctx->launches;

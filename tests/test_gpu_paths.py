@@ -114,3 +114,29 @@ def test_levels_indexorder_long_row(gpu, oracle):
     b = oracle.compute_levels(g, GEN)
     for x, y, nm in zip(a, b, "tbc"):
         same(x, y, nm)
+
+
+def _levels_same(gpu, oracle, g):
+    a = gpu.compute_levels(g, GEN)
+    b = oracle.compute_levels(g, GEN)
+    for x, y, nm in zip(a, b, "tbc"):
+        same(x, y, nm)
+
+
+@pytest.mark.parametrize("shape", ["deep", "wide", "chain", "hub", "long_rows"])
+def test_levels_dataflow(gpu, oracle, shape):
+    """Index-topological graphs above the sweep limit take the dataflow kernel
+    (k_levels_flow): deep and wide layers, a near-chain, in-degree hubs, rows > 8."""
+    g = {"deep": lambda: layered(31, 60000, 500),
+         "wide": lambda: layered(32, 80000, 20000),
+         "chain": lambda: layered(33, 20000, 2, fan_lo=1, fan_hi=2),
+         "hub": lambda: _fanin_hub(7, hubs=4, preds=300, n=20000),
+         "long_rows": lambda: layered(34, 30000, 100, fan_lo=8, fan_hi=30)}[shape]()
+    _levels_same(gpu, oracle, g)
+
+
+@pytest.mark.parametrize("ahead", ["1", "3", "100000"])
+def test_levels_dataflow_lookahead(gpu, oracle, monkeypatch, ahead):
+    # the lookahead only throttles ticket holders: any value must give the same levels
+    monkeypatch.setenv("DP_FLOW_AHEAD", ahead)
+    _levels_same(gpu, oracle, layered(35, 40000, 700))
