@@ -328,6 +328,14 @@ int dp_brute_force_optimal(dp_ctx_t* ctx, const dp_graph_t* g, const dp_devices_
  * the H2D upload and D2H result copies are part of the call. */
 int dp_pipeline(dp_ctx_t* ctx, const dp_graph_t* g, const dp_devices_t* devices, dp_comm_t comm,
                 const dp_pipeline_config_t* cfg, dp_pipeline_result_t** out);
+/* evaluate_pipeline over `count` independent graphs with the same devices and config
+ * (out[i] for graphs[i], each freed with dp_pipeline_result_free).  The graphs share one
+ * stream; their sequential peel + DP cores run in one launch (4 graphs per launch), so a
+ * caller with many graphs keeps more of the GPU busy per stream.  generation_ms is the
+ * window of the whole call.  New surface: the reference evaluates one graph per call. */
+int dp_pipeline_batch(dp_ctx_t* ctx, int32_t count, const dp_graph_t* const* graphs,
+                      const dp_devices_t* devices, dp_comm_t comm, const dp_pipeline_config_t* cfg,
+                      dp_pipeline_result_t** out);
 void dp_pipeline_result_free(dp_pipeline_result_t* r);
 
 /* ---------------------------------------------------------------- Standard Evaluation
@@ -399,6 +407,8 @@ typedef struct dp_resident dp_resident_t;
 int dp_resident_create(dp_ctx_t* ctx, const dp_graph_t* g, const dp_devices_t* devices,
                        dp_comm_t comm, const dp_pipeline_config_t* cfg, dp_resident_t** out);
 int dp_resident_generate(dp_resident_t* r);
+/* The windows of `count` residents of ONE context, peel + DP cores in one launch. */
+int dp_resident_generate_batch(dp_resident_t* const* rs, int32_t count);
 int dp_resident_fetch(dp_resident_t* r, int32_t* order_device, int32_t* adjust_device,
                       int64_t* coarse_nodes, int64_t* coarse_edges);
 void dp_resident_destroy(dp_resident_t* r);

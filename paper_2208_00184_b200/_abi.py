@@ -573,6 +573,29 @@ class Backend:
         p = C.POINTER(PipelineC)()
         self._call("pipeline", C.byref(g.c()), C.byref(devices_c(devices)), comm_c(comm), C.byref(cfg),
                    C.byref(p))
+        return self._report(p)
+
+    def evaluate_pipeline_batch(self, graphs, devices, comm, fusion_range=200, cluster_mem_fraction=0.25,
+                                strategy=1, simulate=True) -> list:
+        """evaluate_pipeline over independent graphs in one call (dp_pipeline_batch; the
+        product only: the reference evaluates one graph per call)."""
+        if self.prefix != "dp_":
+            return [self.evaluate_pipeline(g, devices, comm, fusion_range, cluster_mem_fraction, strategy, simulate)
+                    for g in graphs]
+        cfg = PipelineCfgC(fusion_range, cluster_mem_fraction, strategy, int(simulate))
+        gcs = [g.c() for g in graphs]
+        arr = (C.POINTER(GraphC) * max(1, len(gcs)))(*[C.pointer(x) for x in gcs])
+        outs = (C.POINTER(PipelineC) * max(1, len(gcs)))()
+        f = self.lib.dp_pipeline_batch
+        f.restype = C.c_int
+        f.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.POINTER(GraphC)), C.POINTER(DevicesC), CommC,
+                      C.POINTER(PipelineCfgC), C.POINTER(C.POINTER(PipelineC))]
+        rc = f(self.ctx, len(gcs), arr, C.byref(devices_c(devices)), comm_c(comm), C.byref(cfg), outs)
+        if rc != 0:
+            raise DagError(rc, (self._err() or b"").decode(errors="replace"))
+        return [self._report(outs[i]) for i in range(len(gcs))]
+
+    def _report(self, p) -> PipelineReport:
         r = p.contents
         rep = PipelineReport(int(r.original_nodes), int(r.original_edges), float(r.original_ccr),
                              int(r.coarse_nodes), int(r.coarse_edges), float(r.coarse_ccr),

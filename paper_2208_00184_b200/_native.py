@@ -20,8 +20,8 @@ HEADER_SYMBOLS = [
     "dp_graph_out_free", "dp_contract_colocation_groups", "dp_contraction_free", "dp_fuse",
     "dp_fusion_result_free", "dp_order_place", "dp_adjusting_placement", "dp_expand_placement",
     "dp_placement_result_free", "dp_simulate", "dp_sim_report_free", "dp_simulate_candidates",
-    "dp_brute_force_optimal", "dp_pipeline", "dp_pipeline_result_free", "dp_resident_create",
-    "dp_resident_generate", "dp_resident_fetch", "dp_resident_destroy", "dp_gen_layered",
+    "dp_brute_force_optimal", "dp_pipeline", "dp_pipeline_batch", "dp_pipeline_result_free",
+    "dp_resident_create", "dp_resident_generate", "dp_resident_generate_batch", "dp_resident_fetch", "dp_resident_destroy", "dp_gen_layered",
     "dp_gen_candidates", "dp_gen_gnmt", "dp_gen_bert",
     "dp_graph_from_json", "dp_devices_from_json",
     "dp_fit_node_models", "dp_node_models_free", "dp_estimate_graph", "dp_fit_comm_model",
@@ -54,6 +54,8 @@ def declare(lib: C.CDLL) -> None:
                                        C.POINTER(PipelineCfgC), C.POINTER(C.c_void_p)]
     lib.dp_resident_generate.restype = C.c_int
     lib.dp_resident_generate.argtypes = [C.c_void_p]
+    lib.dp_resident_generate_batch.restype = C.c_int
+    lib.dp_resident_generate_batch.argtypes = [C.POINTER(C.c_void_p), C.c_int32]
     lib.dp_resident_fetch.restype = C.c_int
     lib.dp_resident_fetch.argtypes = [C.c_void_p, I32P, I32P, I64P, I64P]
     lib.dp_resident_destroy.restype = None

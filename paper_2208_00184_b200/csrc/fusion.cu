@@ -648,9 +648,10 @@ void contract_dev(DevGraph& g, Contraction& c, bool materialize_identity) {
   graph_adjacency(w);
 }
 
-void fuse_dev(DevGraph& g, dp_comm_t comm, int32_t range, int64_t limit, FuseOut& out) {
+void fuse_begin(DevGraph& g, dp_comm_t comm, int32_t range, int64_t limit, FuseOut& out, FuseStage& fs) {
   dp_ctx* ctx = g.ctx;
   const int B = 256;
+  fs.limit = limit;
   contract_dev(g, out.con, false);
   DevGraph& work = out.con.identity ? g : out.con.work;
   if (!out.con.identity) {
@@ -671,31 +672,40 @@ void fuse_dev(DevGraph& g, dp_comm_t comm, int32_t range, int64_t limit, FuseOut
            (long long)limit);
     }
   }
-  DevBuf<int64_t> t, b, c;
-  levels_dev(work, comm, t, b, c, false);
+  levels_dev(work, comm, fs.t, fs.b, fs.c, false);
   const int32_t n = work.n;
   out.seq.alloc(ctx, n > 0 ? n : 1);
   out.pos_of.alloc(ctx, n > 0 ? n : 1);
-  if (range >= 1 && range <= 256 && limit > 0 && n > 0) {
-    // cpd_topo streamed into optimal_breakpoints (peel_dp.cu)
-    DevBuf<int32_t> prev_cut(ctx, (size_t)n + 1);
-    DevBuf<int> first(ctx, 1);
+  fs.streamed = range >= 1 && range <= 256 && limit > 0 && n > 0;
+  if (fs.streamed) {
+    // cpd_topo streamed into optimal_breakpoints (peel_dp.cu); launched by the caller
+    fs.prev_cut.alloc(ctx, (size_t)n + 1);
+    fs.first.alloc(ctx, 1);
     int big = INT32_MAX;
-    first.upload(&big, 1);
-    peel_dp_stream(work, c.p, range, limit, out.seq.p, out.pos_of.p, prev_cut.p, first.p);
-    const int fe = scalar_to_host(ctx, first.p);
+    fs.first.upload(&big, 1);
+    fs.job.j = peel_dp_prepare(work, fs.c.p, range, limit, out.seq.p, out.pos_of.p, fs.prev_cut.p, fs.first.p);
+  } else {
+    topo_order(work, DP_TOPO_CPD, fs.c.p, out.seq.p, out.pos_of.p);
+    if (range < 1) fail(DP_E_INVALID_VALUE, "exploration range must be >= 1");
+    if (limit <= 0) fail(DP_E_INVALID_VALUE, "cluster memory limit must be > 0");
+    breakpoints_dev(work, out.seq.p, out.pos_of.p, range, limit, out.cl);
+  }
+}
+
+void fuse_end(DevGraph& g, FuseOut& out, FuseStage& fs) {
+  dp_ctx* ctx = g.ctx;
+  const int B = 256;
+  DevGraph& work = out.con.identity ? g : out.con.work;
+  const int32_t n = work.n;
+  if (fs.streamed) {
+    const int fe = scalar_to_host(ctx, fs.first.p);
     if (fe != INT32_MAX) {  // fusion.cpp:110-115, first position in sequence order
       const int32_t v = scalar_to_host(ctx, out.seq.p + fe);
       fail(DP_E_NODE_EXCEEDS_CLUSTER_LIMIT, "node %lld needs %lld bytes, cluster limit is %lld",
            (long long)scalar_to_host(ctx, work.id.p + v), (long long)scalar_to_host(ctx, work.mem.p + v),
-           (long long)limit);
+           (long long)fs.limit);
     }
-    clusters_from_prev_cut(work, out.seq.p, prev_cut.p, out.cl);
-  } else {
-    topo_order(work, DP_TOPO_CPD, c.p, out.seq.p, out.pos_of.p);
-    if (range < 1) fail(DP_E_INVALID_VALUE, "exploration range must be >= 1");
-    if (limit <= 0) fail(DP_E_INVALID_VALUE, "cluster memory limit must be > 0");
-    breakpoints_dev(work, out.seq.p, out.pos_of.p, range, limit, out.cl);
+    clusters_from_prev_cut(work, out.seq.p, fs.prev_cut.p, out.cl);
   }
   DevBuf<int32_t> cl_work(ctx, n > 0 ? n : 1);
   DP_LAUNCH(ctx, k_cl_of_node, grid_for(n, B), B, 0, out.cl.cl_of_pos.p, out.pos_of.p, n, cl_work.p);
@@ -703,6 +713,13 @@ void fuse_dev(DevGraph& g, dp_comm_t comm, int32_t range, int64_t limit, FuseOut
   out.node_cluster.alloc(ctx, g.n > 0 ? g.n : 1);
   DP_LAUNCH(ctx, k_node_cluster_orig, grid_for(g.n, B), B, 0, out.con.identity ? nullptr : out.con.cidx_of.p,
             cl_work.p, g.n, out.node_cluster.p);
+}
+
+void fuse_dev(DevGraph& g, dp_comm_t comm, int32_t range, int64_t limit, FuseOut& out) {
+  FuseStage fs;
+  fuse_begin(g, comm, range, limit, out, fs);
+  if (fs.streamed) peel_dp_launch(g.ctx, &fs.job.j, 1);
+  fuse_end(g, out, fs);
 }
 
 dp_cluster_map_t* fuse_map_to_host(DevGraph& g, FuseOut& f) {

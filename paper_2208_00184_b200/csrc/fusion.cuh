@@ -3,6 +3,7 @@
 #pragma once
 
 #include "graph.cuh"
+#include "peel_dp.cuh"
 
 namespace dpb {
 
@@ -50,6 +51,21 @@ struct FuseOut {
   DevGraph coarse;
 };
 void fuse_dev(DevGraph& g, dp_comm_t comm, int32_t range, int64_t limit, FuseOut& out);
+
+// fuse_dev split around the streamed peel + DP launch, so that several independent graphs
+// can share it: fuse_begin (contraction, levels, job preparation — or, off the streamed
+// path, the whole peel and DP), peel_dp_launch over the jobs, fuse_end (limit check,
+// traceback, coarse graph).
+struct FuseStage {
+  DevBuf<int64_t> t, b, c;
+  DevBuf<int32_t> prev_cut;
+  DevBuf<int> first;
+  PeelDpHandle job;
+  bool streamed = false;
+  int64_t limit = 0;
+};
+void fuse_begin(DevGraph& g, dp_comm_t comm, int32_t range, int64_t limit, FuseOut& out, FuseStage& fs);
+void fuse_end(DevGraph& g, FuseOut& out, FuseStage& fs);
 
 // ClusterMap re-expressed over original ids (fusion.cpp:317-333) into host buffers.
 dp_cluster_map_t* fuse_map_to_host(DevGraph& g, FuseOut& f);

@@ -1334,10 +1334,21 @@ __device__ void dp_compute_v3(const DpArgs& a, DpSmem3& S) {
   }
 }
 
-__global__ void __launch_bounds__(kDpWarps * 32, 1) k_peel_dp(PeelArgs pa, DpArgs da) {
+// Up to kPeelDpBatch independent graphs per launch: CTA 2j peels graph j, CTA 2j + 1 runs
+// its DP (independent graphs of one caller share one launch, so one stream keeps several
+// graphs' sequential cores in flight).
+constexpr int kPeelDpBatch = 4;
+struct PeelDpBatch {
+  PeelArgs pa[kPeelDpBatch];
+  DpArgs da[kPeelDpBatch];
+};
+
+__global__ void __launch_bounds__(kDpWarps * 32, 1) k_peel_dp(const __grid_constant__ PeelDpBatch b) {
   extern __shared__ int4 smem4[];
   const int warp = threadIdx.x >> 5;
-  if (blockIdx.x == 0) {
+  const PeelArgs& pa = b.pa[blockIdx.x >> 1];
+  const DpArgs& da = b.da[blockIdx.x >> 1];
+  if ((blockIdx.x & 1) == 0) {
     if (warp == 0) peel_dispatch(pa, smem4);
   } else if (da.v3) {
     DpSmem3& S = *reinterpret_cast<DpSmem3*>(smem4);
@@ -1616,21 +1627,34 @@ int32_t topo_order(DevGraph& g, int policy, const int64_t* cpath, int32_t* seq, 
   return emitted;
 }
 
-int32_t peel_dp_stream(DevGraph& g, const int64_t* cpath, int32_t range, int64_t limit, int32_t* seq, int32_t* pos_of,
-                       int32_t* prev_cut, int* first_exceed) {
+struct PeelDpJob {
+  dp_ctx* ctx = nullptr;
+  PeelState st;
+  DevBuf<int64_t> out_sum;
+  DevBuf<unsigned long long> mx;
+  DevBuf<long long> dbg;
+  PeelArgs pa{};
+  DpArgs da{};
+  double bytes = 0.0;  // algorithmic bytes (stage timing)
+};
+
+PeelDpJob* peel_dp_prepare(DevGraph& g, const int64_t* cpath, int32_t range, int64_t limit, int32_t* seq,
+                           int32_t* pos_of, int32_t* prev_cut, int* first_exceed) {
   dp_ctx* ctx = g.ctx;
   const int32_t n = g.n;
-  if (n == 0) return 0;
-  DevBuf<int64_t> out_sum(ctx, n);
-  DP_LAUNCH(ctx, k_out_sum, grid_for(n, 256), 256, 0, g.out_off.p, g.out_cost.p, n, out_sum.p);
+  auto* j = new PeelDpJob;
+  PeelDpHandle guard(j);
+  j->ctx = ctx;
+  j->out_sum.alloc(ctx, n);
+  DP_LAUNCH(ctx, k_out_sum, grid_for(n, 256), 256, 0, g.out_off.p, g.out_cost.p, n, j->out_sum.p);
   // 32-bit keys need every window value within +-2^22 of the window minimum: bounded
   // by R x (largest out-cost sum of a position) + largest single cost.
-  DevBuf<unsigned long long> mx(ctx, 1);
-  mx.zero();
-  DP_LAUNCH(ctx, k_max_abs, grid_for(n, 256), 256, 0, out_sum.p, n, mx.p);
-  DP_LAUNCH(ctx, k_max_abs, grid_for(g.m_ok, 256), 256, 0, g.out_cost.p, g.m_ok, mx.p);
-  const unsigned long long max_out = scalar_to_host(ctx, mx.p);
-  DpArgs da{};
+  j->mx.alloc(ctx, 1);
+  j->mx.zero();
+  DP_LAUNCH(ctx, k_max_abs, grid_for(n, 256), 256, 0, j->out_sum.p, n, j->mx.p);
+  DP_LAUNCH(ctx, k_max_abs, grid_for(g.m_ok, 256), 256, 0, g.out_cost.p, g.m_ok, j->mx.p);
+  const unsigned long long max_out = scalar_to_host(ctx, j->mx.p);
+  DpArgs& da = j->da;
   da.keys32 = static_cast<double>(max_out) * (range + 2) < static_cast<double>(1 << 21);
   // the block recurrence lets relative values drift for up to 2 x 32 steps before a rebase
   da.block32 = static_cast<double>(max_out) * (range + 2 + 64) < static_cast<double>(1 << 21) &&
@@ -1642,43 +1666,69 @@ int32_t peel_dp_stream(DevGraph& g, const int64_t* cpath, int32_t range, int64_t
   da.seq = seq;
   da.pos_of = pos_of;
   da.mem = g.mem.p;
-  da.out_sum = out_sum.p;
+  da.out_sum = j->out_sum.p;
   da.in_off = g.in_off.p;
   da.in_src = g.in_src.p;
   da.in_cost = g.in_cost.p;
   da.prev_cut = prev_cut;
   da.first_exceed = first_exceed;
+  j->dbg.alloc(ctx, 4);
+  j->dbg.zero();
+  da.debug = getenv("DP_DEBUG_DP") ? j->dbg.p : nullptr;
+  peel_prepare(g, DP_TOPO_CPD, cpath, j->st);
+  j->pa = peel_args(g, j->st, seq, pos_of, true);
+  j->pa.debug = da.debug ? j->dbg.p + 3 : nullptr;
+  da.progress = j->st.counters.p;
+  // algorithmic bytes: peel 64 B row + 8 B seq/pos_of per node; DP 4+8+8+4 B per position
+  // (node, memory, out-cost sum, cut) + 12 B per in-edge (source position, cost)
+  j->bytes = 92.0 * n + 12.0 * g.m_ok;
+  guard.j = nullptr;
+  return j;
+}
+
+void peel_dp_launch(dp_ctx* ctx, PeelDpJob* const* jobs, int count) {
   const size_t sm = std::max(peel_smem(), std::max(sizeof(DpSmem), sizeof(DpSmem3)));
   static bool attr = false;
   if (!attr) {
     DP_CUDA(cudaFuncSetAttribute(k_peel_dp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
     attr = true;
   }
-  DevBuf<long long> dbg(ctx, 4);
-  dbg.zero();
-  da.debug = getenv("DP_DEBUG_DP") ? dbg.p : nullptr;
-  PeelState st;
-  peel_prepare(g, DP_TOPO_CPD, cpath, st);
-  PeelArgs pa = peel_args(g, st, seq, pos_of, true);
-  pa.debug = da.debug ? dbg.p + 3 : nullptr;
-  da.progress = st.counters.p;
-  void* args[] = {&pa, &da};
-  {
-    // algorithmic bytes: peel 64 B row + 8 B seq/pos_of per node; DP 4+8+8+4 B per position
-    // (node, memory, out-cost sum, cut) + 12 B per in-edge (source position, cost)
-    StageScope s(ctx, "peel+dp (streamed)", 92.0 * n + 12.0 * g.m_ok);
-    DP_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_peel_dp), 2, kDpWarps * 32, args, sm,
+  for (int b0 = 0; b0 < count; b0 += kPeelDpBatch) {
+    const int k = std::min(kPeelDpBatch, count - b0);
+    PeelDpBatch batch{};
+    double bytes = 0.0;
+    for (int q = 0; q < k; ++q) {
+      batch.pa[q] = jobs[b0 + q]->pa;
+      batch.da[q] = jobs[b0 + q]->da;
+      bytes += jobs[b0 + q]->bytes;
+    }
+    void* args[] = {&batch};
+    StageScope s(ctx, "peel+dp (streamed)", bytes);
+    DP_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_peel_dp), 2 * k, kDpWarps * 32, args, sm,
                                         ctx->stream));
     ++ctx->launches;
   }
-  if (da.debug) {
-    long long h[4];
-    dbg.download(h, 4);
-    sync(ctx);
-    fprintf(stderr, "[peel_dp] dp warp: total %.1f ms, waiting %.1f ms, staging %.1f ms; peel warp %.1f ms (at 1.965 GHz)\n",
-            h[0] / 1.965e6, h[1] / 1.965e6, h[2] / 1.965e6, h[3] / 1.965e6);
+  for (int q = 0; q < count; ++q) {
+    PeelDpJob* j = jobs[q];
+    if (j->da.debug) {
+      long long h[4];
+      j->dbg.download(h, 4);
+      sync(ctx);
+      fprintf(stderr,
+              "[peel_dp] dp warp: total %.1f ms, waiting %.1f ms, staging %.1f ms; peel warp %.1f ms (at 1.965 GHz)\n",
+              h[0] / 1.965e6, h[1] / 1.965e6, h[2] / 1.965e6, h[3] / 1.965e6);
+    }
   }
-  return scalar_to_host(ctx, st.counters.p + 1);
+}
+
+void peel_dp_release(PeelDpJob* j) { delete j; }
+
+int32_t peel_dp_stream(DevGraph& g, const int64_t* cpath, int32_t range, int64_t limit, int32_t* seq, int32_t* pos_of,
+                       int32_t* prev_cut, int* first_exceed) {
+  if (g.n == 0) return 0;
+  PeelDpHandle h(peel_dp_prepare(g, cpath, range, limit, seq, pos_of, prev_cut, first_exceed));
+  peel_dp_launch(g.ctx, &h.j, 1);
+  return scalar_to_host(g.ctx, h.j->st.counters.p + 1);
 }
 
 }  // namespace dpb

@@ -30,4 +30,21 @@ void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st, 
 int32_t peel_dp_stream(DevGraph& g, const int64_t* cpath, int32_t range, int64_t limit, int32_t* seq, int32_t* pos_of,
                        int32_t* prev_cut, int* first_exceed);
 
+// The same, split so that several independent graphs share one launch: prepare each
+// graph's job, launch them together (up to 4 graphs per cooperative launch, 2 CTAs each),
+// release after the outputs have been consumed.
+struct PeelDpJob;
+PeelDpJob* peel_dp_prepare(DevGraph& g, const int64_t* cpath, int32_t range, int64_t limit, int32_t* seq,
+                           int32_t* pos_of, int32_t* prev_cut, int* first_exceed);
+void peel_dp_launch(dp_ctx* ctx, PeelDpJob* const* jobs, int count);
+void peel_dp_release(PeelDpJob* j);
+struct PeelDpHandle {
+  PeelDpJob* j = nullptr;
+  PeelDpHandle() = default;
+  explicit PeelDpHandle(PeelDpJob* x) : j(x) {}
+  PeelDpHandle(const PeelDpHandle&) = delete;
+  PeelDpHandle& operator=(const PeelDpHandle&) = delete;
+  ~PeelDpHandle() { peel_dp_release(j); }
+};
+
 }  // namespace dpb

@@ -5,6 +5,7 @@
 // (fuse -> coarse levels + cpd_topo -> order_place + adjusting_placement -> 2x expand)
 // runs as one stream of kernels; only the results cross PCIe.
 #include <algorithm>
+#include <memory>
 
 #include "abi_util.cuh"
 #include "fusion.cuh"
@@ -74,22 +75,22 @@ double ccr_dev(DevGraph& g) {
   return static_cast<double>(static_cast<int64_t>(h[1])) / static_cast<double>(tc);
 }
 
-// Everything after the H2D upload: index, validation (pipeline.cpp:33), ccr (:58),
-// cluster limit (:60-65) and the generation window (:67-79).
-void resident_generate(Resident& r, bool with_ccr) {
+// Index + validation of an uploaded graph (pipeline.cpp:33).
+void resident_validate(Resident& r, bool cycle_check) {
+  DevGraph& g = r.g;
+  StageScope st(r.ctx, "index+validate", 16.0 * g.m + 8.0 * g.n);
+  graph_resolve(g);
+  graph_adjacency(g);
+  Validation v = graph_validate(g, r.host, false, cycle_check);
+  if (v.code) fail(v.code, "%s", v.message.c_str());
+}
+
+// The generation window (pipeline.cpp:67-79) after the streamed peel + DP: traceback and
+// coarse graph, coarse levels + cpd_topo, order_place + adjusting_placement, 2x expand.
+void generate_end(Resident& r, FuseStage& fs) {
   dp_ctx* ctx = r.ctx;
   DevGraph& g = r.g;
-  StageScope whole(ctx, "generate", 0.0);
-  {
-    StageScope st(ctx, "index+validate", 16.0 * g.m + 8.0 * g.n);
-    graph_resolve(g);
-    graph_adjacency(g);
-    Validation v = graph_validate(g, r.host, false, false);
-    if (v.code) fail(v.code, "%s", v.message.c_str());
-  }
-  graph_costs(g, r.comm);
-  if (with_ccr) r.original_ccr = ccr_dev(g);
-  fuse_dev(g, r.comm, r.cfg.fusion_range, r.limit, r.f);
+  fuse_end(g, r.f, fs);
   DevGraph& coarse = r.f.coarse;
   levels_dev(coarse, r.comm, r.ct, r.cb, r.cc, true);  // clusters are runs of a topological order
   const int32_t k = coarse.n;
@@ -107,6 +108,36 @@ void resident_generate(Resident& r, bool with_ccr) {
     expand_dev(g, r.f.node_cluster.p, r.po.dev.p, D, r.dev_order.p, r.pdm_order.p);
     expand_dev(g, r.f.node_cluster.p, r.pa.dev.p, D, r.dev_adjust.p, r.pdm_adjust.p);
   }
+}
+
+// Generation windows of independent graphs on one stream (graphs already validated, with
+// costs): each graph's fuse_begin, ONE launch of all the streamed peel + DP cores (4 graphs
+// per cooperative launch, 2 CTAs each), then each graph's generate_end.
+void generate_windows(Resident* const* rs, int count) {
+  std::vector<std::unique_ptr<FuseStage>> fs;
+  std::vector<PeelDpJob*> jobs;
+  for (int i = 0; i < count; ++i) {
+    Resident& r = *rs[i];
+    fs.emplace_back(new FuseStage);
+    fuse_begin(r.g, r.comm, r.cfg.fusion_range, r.limit, r.f, *fs.back());
+    if (fs.back()->streamed) jobs.push_back(fs.back()->job.j);
+  }
+  if (!jobs.empty()) peel_dp_launch(rs[0]->ctx, jobs.data(), static_cast<int>(jobs.size()));
+  for (int i = 0; i < count; ++i) generate_end(*rs[i], *fs[i]);
+}
+
+// Everything after the H2D upload: index, validation (pipeline.cpp:33), ccr (:58),
+// cluster limit (:60-65) and the generation window (:67-79).
+void resident_generate(Resident* const* rs, int count, bool with_ccr) {
+  dp_ctx* ctx = rs[0]->ctx;
+  StageScope whole(ctx, "generate", 0.0);
+  for (int i = 0; i < count; ++i) {
+    Resident& r = *rs[i];
+    resident_validate(r, false);
+    graph_costs(r.g, r.comm);
+    if (with_ccr) r.original_ccr = ccr_dev(r.g);
+  }
+  generate_windows(rs, count);
 }
 
 void resident_init(Resident& r, dp_ctx* ctx, const dp_graph_t* h, const dp_devices_t* devices, dp_comm_t comm,
@@ -154,13 +185,25 @@ extern "C" {
 
 int dp_pipeline(dp_ctx_t* ctx, const dp_graph_t* h, const dp_devices_t* devices, dp_comm_t comm,
                 const dp_pipeline_config_t* cfg, dp_pipeline_result_t** out) {
+  const dp_graph_t* hs[1] = {h};
+  return dp_pipeline_batch(ctx, 1, hs, devices, comm, cfg, out);
+}
+
+int dp_pipeline_batch(dp_ctx_t* ctx, int32_t count, const dp_graph_t* const* graphs, const dp_devices_t* devices,
+                      dp_comm_t comm, const dp_pipeline_config_t* cfg, dp_pipeline_result_t** out) {
   DP_API_BEGIN(ctx)
+  if (count < 0) fail(DP_E_INVALID_VALUE, "graph count must be >= 0");
   const bool dbg = getenv("DP_DEBUG_PIPE") != nullptr;
   auto now = [] { return std::chrono::steady_clock::now(); };
   auto span_ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
   const auto h0 = now();
-  Resident r;
-  resident_init(r, ctx, h, devices, comm, cfg);
+  std::vector<std::unique_ptr<Resident>> rs;
+  std::vector<Resident*> rp;
+  for (int32_t i = 0; i < count; ++i) {
+    rs.emplace_back(new Resident);
+    rp.push_back(rs.back().get());
+    resident_init(*rs.back(), ctx, graphs[i], devices, comm, cfg);
+  }
   if (dbg) sync(ctx);
   const auto h1 = now();
   cudaEvent_t e0, e1;
@@ -174,73 +217,72 @@ int dp_pipeline(dp_ctx_t* ctx, const dp_graph_t* h, const dp_devices_t* devices,
     }
   } guard{e0, e1};
   // require_valid + ccr precede the window (pipeline.cpp:33, :58)
-  {
-    DevGraph& g = r.g;
-    graph_resolve(g);
-    graph_adjacency(g);
-    Validation v = graph_validate(g, h, false, true);
-    if (v.code) fail(v.code, "%s", v.message.c_str());
-    graph_costs(g, comm);
-    r.original_ccr = ccr_dev(g);
+  for (Resident* r : rp) {
+    resident_validate(*r, true);
+    graph_costs(r->g, comm);
+    r->original_ccr = ccr_dev(r->g);
   }
   if (dbg) sync(ctx);
   const auto h2 = now();
   DP_CUDA(cudaEventRecord(e0, ctx->stream));
-  fuse_dev(r.g, r.comm, r.cfg.fusion_range, r.limit, r.f);
-  DevGraph& coarse = r.f.coarse;
-  levels_dev(coarse, r.comm, r.ct, r.cb, r.cc, true);  // clusters are runs of a topological order
-  const int32_t k = coarse.n, n = r.g.n, D = r.devs.D;
-  r.cseq.alloc(ctx, k > 0 ? k : 1);
-  r.cpos.alloc(ctx, k > 0 ? k : 1);
-  topo_order(coarse, DP_TOPO_CPD, r.cc.p, r.cseq.p, r.cpos.p);
-  place_dev(coarse, r.cseq.p, r.devs, &r.po, &r.pa, true);
-  r.dev_order.alloc(ctx, n > 0 ? n : 1);
-  r.dev_adjust.alloc(ctx, n > 0 ? n : 1);
-  r.pdm_order.alloc(ctx, D);
-  r.pdm_adjust.alloc(ctx, D);
-  expand_dev(r.g, r.f.node_cluster.p, r.po.dev.p, D, r.dev_order.p, r.pdm_order.p);
-  expand_dev(r.g, r.f.node_cluster.p, r.pa.dev.p, D, r.dev_adjust.p, r.pdm_adjust.p);
+  if (count > 0) generate_windows(rp.data(), count);
   DP_CUDA(cudaEventRecord(e1, ctx->stream));
   if (dbg) sync(ctx);
   const auto h3 = now();
-  auto* res = halloc<dp_pipeline_result_t>(1);
-  res->original_nodes = n;
-  res->original_edges = r.g.m;
-  res->original_ccr = r.original_ccr;
-  res->coarse_nodes = k;
-  res->coarse_edges = coarse.m;
-  res->fusion = halloc<dp_fusion_result_t>(1);
-  res->fusion->coarse = graph_to_host(coarse, true);
-  res->fusion->map = fuse_map_to_host(r.g, r.f);
-  std::vector<int32_t> cs = to_host(ctx, r.cseq.p, k);
-  res->coarse_sequence = halloc<int64_t>(k);
-  std::vector<int64_t> cids(static_cast<size_t>(k));
-  for (int32_t i = 0; i < k; ++i) cids[i] = res->coarse_sequence[i] = cs[i];
-  res->coarse_order = placement_to_host(ctx, r.devs, r.po, k, &cids, false);
-  res->coarse_adjust = placement_to_host(ctx, r.devs, r.pa, k, &cids, true);
-  res->order_expanded = expanded_to_host(ctx, r.devs, r.dev_order.p, r.pdm_order.p, n);
-  res->adjust_expanded = expanded_to_host(ctx, r.devs, r.dev_adjust.p, r.pdm_adjust.p, n);
+  std::vector<dp_pipeline_result_t*> res(static_cast<size_t>(count), nullptr);
+  struct ResGuard {
+    std::vector<dp_pipeline_result_t*>& v;
+    ~ResGuard() {
+      for (auto* x : v)
+        if (x) dp_pipeline_result_free(x);
+    }
+  } res_guard{res};
   float ms = 0;
   DP_CUDA(cudaEventSynchronize(e1));
   DP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-  res->generation_ms = ms;
-  res->coarse_ccr = 0.0;
-  if (coarse.m > 0) res->coarse_ccr = ccr_dev(coarse);  // pipeline.cpp:83
-  res->order_makespan = res->adjust_makespan = -1;
+  for (int32_t i = 0; i < count; ++i) {
+    Resident& r = *rp[i];
+    DevGraph& coarse = r.f.coarse;
+    const int32_t k = coarse.n, n = r.g.n;
+    auto* x = res[i] = halloc<dp_pipeline_result_t>(1);
+    x->original_nodes = n;
+    x->original_edges = r.g.m;
+    x->original_ccr = r.original_ccr;
+    x->coarse_nodes = k;
+    x->coarse_edges = coarse.m;
+    x->fusion = halloc<dp_fusion_result_t>(1);
+    x->fusion->coarse = graph_to_host(coarse, true);
+    x->fusion->map = fuse_map_to_host(r.g, r.f);
+    std::vector<int32_t> cs = to_host(ctx, r.cseq.p, k);
+    x->coarse_sequence = halloc<int64_t>(k);
+    std::vector<int64_t> cids(static_cast<size_t>(k));
+    for (int32_t q = 0; q < k; ++q) cids[q] = x->coarse_sequence[q] = cs[q];
+    x->coarse_order = placement_to_host(ctx, r.devs, r.po, k, &cids, false);
+    x->coarse_adjust = placement_to_host(ctx, r.devs, r.pa, k, &cids, true);
+    x->order_expanded = expanded_to_host(ctx, r.devs, r.dev_order.p, r.pdm_order.p, n);
+    x->adjust_expanded = expanded_to_host(ctx, r.devs, r.dev_adjust.p, r.pdm_adjust.p, n);
+    x->generation_ms = ms;  // the window of the whole call (all graphs of a batch)
+    x->coarse_ccr = 0.0;
+    if (coarse.m > 0) x->coarse_ccr = ccr_dev(coarse);  // pipeline.cpp:83
+    x->order_makespan = x->adjust_makespan = -1;
+    if (cfg->simulate) {  // pipeline.cpp:89-90
+      dp_sim_report_t* so = sim_report(r.g, r.devs, r.dev_order.p, false);
+      dp_sim_report_t* sa = sim_report(r.g, r.devs, r.dev_adjust.p, false);
+      x->order_makespan = so->makespan;
+      x->adjust_makespan = sa->makespan;
+      free_sim(so);
+      free_sim(sa);
+    }
+  }
   if (dbg) {
     const auto h4 = now();
     fprintf(stderr, "[dp_pipeline] upload %.1f ms, validate+ccr %.1f ms, window %.1f ms, results %.1f ms\n",
             span_ms(h0, h1), span_ms(h1, h2), span_ms(h2, h3), span_ms(h3, h4));
   }
-  if (cfg->simulate) {  // pipeline.cpp:89-90
-    dp_sim_report_t* so = sim_report(r.g, r.devs, r.dev_order.p, false);
-    dp_sim_report_t* sa = sim_report(r.g, r.devs, r.dev_adjust.p, false);
-    res->order_makespan = so->makespan;
-    res->adjust_makespan = sa->makespan;
-    free_sim(so);
-    free_sim(sa);
+  for (int32_t i = 0; i < count; ++i) {
+    out[i] = res[i];
+    res[i] = nullptr;
   }
-  *out = res;
   DP_API_END
 }
 
@@ -264,7 +306,18 @@ int dp_resident_create(dp_ctx_t* ctx, const dp_graph_t* h, const dp_devices_t* d
 
 int dp_resident_generate(dp_resident_t* r) {
   DP_API_BEGIN(r ? r->ctx : nullptr)
-  resident_generate(*r, false);
+  Resident* rs[1] = {r};
+  resident_generate(rs, 1, false);
+  DP_API_END
+}
+
+int dp_resident_generate_batch(dp_resident_t* const* rs, int32_t count) {
+  if (count == 0) return 0;
+  DP_API_BEGIN(count > 0 && rs && rs[0] ? rs[0]->ctx : nullptr)
+  for (int32_t i = 0; i < count; ++i)
+    if (!rs[i] || rs[i]->ctx != rs[0]->ctx) fail(DP_E_INVALID_VALUE, "batched residents must share one context");
+  std::vector<Resident*> v(rs, rs + count);
+  resident_generate(v.data(), count, false);
   DP_API_END
 }
 

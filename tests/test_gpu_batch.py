@@ -1,0 +1,48 @@
+"""dp_pipeline_batch / dp_resident_generate_batch: independent graphs evaluated in one call
+(their peel + DP cores share one cooperative launch, 4 graphs per launch) must give, graph
+by graph, exactly the reference's evaluate_pipeline (oracle/_ref); a failing graph fails the
+call with that graph's error kind and message."""
+import numpy as np
+import pytest
+
+from compare import outcome, same_pipeline
+from graphs import layered, random_dag, shuffled, with_groups
+from cases import GEN, capacity_for, devices
+
+pytestmark = pytest.mark.gpu
+
+
+def _batch_graphs():
+    gs = [layered(40 + s, 2000 + 700 * s, 30 + 10 * s) for s in range(5)]
+    gs.append(shuffled(layered(50, 4000, 64), 1, relabel=True))   # Kahn levels path
+    for s in range(3):  # co-location contraction (some group draws are cyclic: filtered below)
+        gs.append(with_groups(layered(51 + s, 3000, 40), s, 20, 0.05))
+    gs.append(random_dag(55, 1500, 0.004))
+    gs.append(layered(53, 1, 1))                                   # single node
+    return gs
+
+
+def test_pipeline_batch_matches_reference(gpu, ref):
+    gs = _batch_graphs()
+    cap = max(capacity_for(g, 4, 1.25) for g in gs)
+    devs = devices(4, cap)
+    gs = [g for g in gs if outcome(ref.evaluate_pipeline, g, devs, GEN)[0] == "ok"]
+    assert len(gs) >= 7
+    got = gpu.evaluate_pipeline_batch(gs, devs, GEN)
+    assert len(got) == len(gs)
+    for i, (g, r) in enumerate(zip(gs, got)):
+        same_pipeline(r, ref.evaluate_pipeline(g, devs, GEN), f"batch[{i}]")
+
+
+def test_pipeline_batch_error_and_empty(gpu, ref):
+    good = layered(60, 3000, 40)
+    bad = layered(61, 2000, 40)
+    bad.memory_bytes = bad.memory_bytes.copy()
+    bad.memory_bytes[17] = 10 ** 15  # exceeds the cluster limit: NodeExceedsClusterLimit
+    devs = devices(4, capacity_for(good, 4, 1.25))
+    a = outcome(gpu.evaluate_pipeline_batch, [good, bad, good], devs, GEN)
+    b = outcome(ref.evaluate_pipeline, bad, devs, GEN)
+    assert a[0] == b[0] == "err" and a[1:] == b[1:], (a[:1], b[:1])
+    assert gpu.evaluate_pipeline_batch([], devs, GEN) == []
+    # the context stays usable after a failed batch
+    same_pipeline(gpu.evaluate_pipeline_batch([good], devs, GEN)[0], ref.evaluate_pipeline(good, devs, GEN))
