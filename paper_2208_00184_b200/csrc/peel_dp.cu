@@ -396,16 +396,20 @@ __device__ void peel_warp_v5(const PeelArgs& a, int2* sstack, int64_t* sfreed, i
 //    is pushed, its children's rows are prefetched to L2.
 //  * Rows longer than 8 take a CSR path; in-degrees >= 127 use global counters.
 constexpr int kV6Stack = 512;
+// hash buckets (log2): 16,384 x 2 ways (128 KB) when the peel has its SM alone, 8,192 when
+// it shares it with the DP (k_peel_dp_shared)
 constexpr int kV6BucketBits = 14;
+constexpr int kV6BucketBitsShared = 13;
 constexpr uint32_t kV6Empty = 0xffffffffu;
 constexpr int32_t kV6Long = 1 << 30;  // sid flag: out-degree > 8 (CSR path)
 constexpr int kV6FreedCap = 1024;
 
+template <int BB>
 struct V6Smem {
   int4 row[kV6Stack][4];
   int32_t sid[kV6Stack];
-  uint32_t ht[2 << kV6BucketBits];      // way 0 / way 1 of bucket b at [2b], [2b+1]
-  uint32_t ovc[1 << (kV6BucketBits - 1)];  // 16-bit overflow counts, two per word
+  uint32_t ht[2 << BB];      // way 0 / way 1 of bucket b at [2b], [2b+1]
+  uint32_t ovc[1 << (BB - 1)];  // 16-bit overflow counts, two per word
   int64_t freed[kV6FreedCap];
   int32_t seqbuf[32];
 };
@@ -414,13 +418,15 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+template <int BB>
 __device__ __forceinline__ uint32_t v6_bucket(int32_t c) {
-  return (static_cast<uint32_t>(c) * 0x9E3779B1u) >> (32 - kV6BucketBits);
+  return (static_cast<uint32_t>(c) * 0x9E3779B1u) >> (32 - BB);
 }
 
 // One decrement of child c (initial in-degree `code`, 2..126).  Returns true when c is freed.
-__device__ __forceinline__ bool v6_dec(V6Smem& S, int32_t* gover, int32_t c, int code) {
-  const uint32_t b = v6_bucket(c), uc = static_cast<uint32_t>(c);
+template <int BB>
+__device__ __forceinline__ bool v6_dec(V6Smem<BB>& S, int32_t* gover, int32_t c, int code) {
+  const uint32_t b = v6_bucket<BB>(c), uc = static_cast<uint32_t>(c);
   const uint2 w = *reinterpret_cast<const uint2*>(&S.ht[2 * b]);
   const uint32_t sh = (b & 1u) * 16;
   const uint32_t ov = S.ovc[b >> 1];
@@ -448,7 +454,8 @@ __device__ __forceinline__ bool v6_dec(V6Smem& S, int32_t* gover, int32_t c, int
 }
 
 // Loads stack entries [lo, hi] (ids from the global stack, rows from the ELL) into the cache.
-__device__ void v6_fill(const PeelArgs& a, V6Smem& S, int32_t lo, int32_t hi, int lane) {
+template <int BB>
+__device__ void v6_fill(const PeelArgs& a, V6Smem<BB>& S, int32_t lo, int32_t hi, int lane) {
   for (int32_t idx = lane; idx < (hi - lo + 1) * 4; idx += 32) {
     const int32_t i = lo + (idx >> 2);
     const int32_t sv = a.gsid[i];
@@ -464,12 +471,13 @@ __device__ __forceinline__ void v6_publish(const PeelArgs& a, int32_t p) {
   }
 }
 
-__device__ void peel_warp_v6(const PeelArgs& a, V6Smem& S) {
+template <int BB>
+__device__ void peel_warp_v6(const PeelArgs& a, V6Smem<BB>& S) {
   const int lane = threadIdx.x & 31;
   const long long t_start = clock64();
   constexpr int32_t SC = kV6Stack;
-  for (int i = lane; i < (2 << kV6BucketBits); i += 32) S.ht[i] = kV6Empty;
-  for (int i = lane; i < (1 << (kV6BucketBits - 1)); i += 32) S.ovc[i] = 0;
+  for (int i = lane; i < (2 << BB); i += 32) S.ht[i] = kV6Empty;
+  for (int i = lane; i < (1 << (BB - 1)); i += 32) S.ovc[i] = 0;
   int32_t top = a.nsrc - 1;
   int32_t base = max(0, a.nsrc - SC / 2);
   v6_fill(a, S, base, top, lane);
@@ -567,7 +575,7 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem& S) {
       // branch-light table step: one bucket load; remaining = table value on a hit, the
       // initial in-degree on a first touch (code == 1 frees without touching the table)
       const uint32_t code = (static_cast<uint32_t>(my.y) >> 24) & 127u, uc = static_cast<uint32_t>(my.x);
-      const uint32_t b = v6_bucket(my.x), sh = (b & 1u) * 16;
+      const uint32_t b = v6_bucket<BB>(my.x), sh = (b & 1u) * 16;
       const uint2 w = *reinterpret_cast<const uint2*>(&S.ht[2 * b]);
       const uint32_t ov = (S.ovc[b >> 1] >> sh) & 0xffffu;
       const bool h0 = (w.x >> 7) == uc, h1 = (w.y >> 7) == uc, hit = h0 | h1;
@@ -622,9 +630,10 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem& S) {
   }
 }
 
+template <int BB>
 __device__ __forceinline__ void peel_dispatch(const PeelArgs& a, int4* smem4) {
   if (a.v6) {
-    peel_warp_v6(a, *reinterpret_cast<V6Smem*>(smem4));
+    peel_warp_v6(a, *reinterpret_cast<V6Smem<BB>*>(smem4));
     return;
   }
   int64_t* sfreed = reinterpret_cast<int64_t*>(smem4 + kStackCache);
@@ -638,7 +647,7 @@ __device__ __forceinline__ void peel_dispatch(const PeelArgs& a, int4* smem4) {
 
 __global__ void __launch_bounds__(32) k_peel2(PeelArgs a) {
   extern __shared__ int4 smem4[];
-  peel_dispatch(a, smem4);
+  peel_dispatch<kV6BucketBits>(a, smem4);
 }
 
 // ---------------------------------------------------------------- streaming DP
@@ -1053,25 +1062,29 @@ __device__ void dp_warp(const DpArgs& a, DpSmem& S) {
 // recurrence of the block32 path (independent slot updates, then a 31-step chain over the
 // block's own candidates).
 constexpr int kDpProducers = 3;
-constexpr int kDpWarps = 1 + kDpProducers;
 constexpr int kLpMax = 256 + kCh + 1;
+// compacted in-edges per staged chunk (more: the chunk is read from HBM); 1,024 when the DP
+// shares its SM with the peel (k_peel_dp_shared)
 constexpr int kE2Cap = 4096;
+constexpr int kE2CapShared = 1024;
 
+template <int E2>
 struct DpBuf {
   int32_t lo[kCh];   // lo[j] for j = j0 + t + 1 (absolute position)
   int64_t out[kCh];
   int32_t off[kCh + 1];   // all in-edges of position t: [off[t], off[t+1])
   int32_t off2[kCh + 1];  // in-window in-edges of position t in e2
   int32_t cnt2[kCh];
-  int2 e2[kE2Cap + 2];    // {source position, cost << 8}, sources >= block start - 224
+  int2 e2[E2 + 2];    // {source position, cost << 8}, sources >= block start - 224
   int32_t ioff[kCh];
   int64_t lp[kLpMax];
   int32_t node[kCh];
   int32_t cnt, n2;        // n2 > kE2Cap: the compute warp reads in-edges from HBM
 };
 
+template <int E2>
 struct DpSmem3 {
-  DpBuf buf[kDpProducers];
+  DpBuf<E2> buf[kDpProducers];
   int32_t mt[32][33];
   int32_t ct[32][33];
   int ready[kDpProducers];
@@ -1080,7 +1093,8 @@ struct DpSmem3 {
 
 __device__ __forceinline__ int ld_volatile_shared(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 
-__device__ void dp_stage(const DpArgs& a, DpBuf& B, int32_t j0, int32_t cnt, int lane) {
+template <int E2>
+__device__ void dp_stage(const DpArgs& a, DpBuf<E2>& B, int32_t j0, int32_t cnt, int lane) {
   for (int32_t t = lane; t < cnt; t += 32) {
     const int32_t v = a.seq[j0 + t];
     B.node[t] = v;
@@ -1174,7 +1188,7 @@ __device__ void dp_stage(const DpArgs& a, DpBuf& B, int32_t j0, int32_t cnt, int
       const unsigned m = __ballot_sync(FULL, keep);
       if (keep) {
         const int32_t idx = n2 + __popc(m & ((1u << lane) - 1));
-        if (idx < kE2Cap) B.e2[idx] = make_int2(av[u], static_cast<int32_t>(cc[u]) << 8);
+        if (idx < E2) B.e2[idx] = make_int2(av[u], static_cast<int32_t>(cc[u]) << 8);
         atomicAdd(&B.cnt2[tt[u]], 1);
       }
       n2 += __popc(m);
@@ -1200,7 +1214,8 @@ __device__ void dp_stage(const DpArgs& a, DpBuf& B, int32_t j0, int32_t cnt, int
   }
 }
 
-__device__ void dp_producer(const DpArgs& a, DpSmem3& S, int k, int lane) {
+template <int E2>
+__device__ void dp_producer(const DpArgs& a, DpSmem3<E2>& S, int k, int lane) {
   int avail = 0;
   for (int32_t c = k;; c += kDpProducers) {
     const int32_t j0 = c * kCh;
@@ -1218,7 +1233,8 @@ __device__ void dp_producer(const DpArgs& a, DpSmem3& S, int k, int lane) {
   }
 }
 
-__device__ void dp_compute_v3(const DpArgs& a, DpSmem3& S) {
+template <int E2>
+__device__ void dp_compute_v3(const DpArgs& a, DpSmem3<E2>& S) {
   constexpr int NR = 7;
   const int lane = threadIdx.x & 31;
   const int32_t n = a.n;
@@ -1239,9 +1255,9 @@ __device__ void dp_compute_v3(const DpArgs& a, DpSmem3& S) {
     while (ld_volatile_shared(&S.ready[kb]) != c) __nanosleep(32);
     wait_cycles += clock64() - tw0;
     __threadfence_block();
-    const DpBuf& B = S.buf[kb];
+    const DpBuf<E2>& B = S.buf[kb];
     const int32_t cnt = B.cnt;
-    const bool staged = B.n2 <= kE2Cap;
+    const bool staged = B.n2 <= E2;
     for (int32_t tb = 0; tb < cnt; tb += 32) {
       const int32_t P = j0 + tb;
       const int32_t nb = min(32, cnt - tb);
@@ -1334,24 +1350,39 @@ __device__ void dp_compute_v3(const DpArgs& a, DpSmem3& S) {
   }
 }
 
-// Up to kPeelDpBatch independent graphs per launch: CTA 2j peels graph j, CTA 2j + 1 runs
-// its DP (independent graphs of one caller share one launch, so one stream keeps several
-// graphs' sequential cores in flight).
-constexpr int kPeelDpBatch = 4;
+// Up to kPeelDpBatch independent graphs per launch.  Shared mode (k_peel_dp_shared): one
+// CTA per graph — warp 0 peels, warp 1 runs the DP recurrence, warps 2, 3, 5 stage DP
+// chunks (warp 4 exits at once so that the peel warp keeps its SM sub-partition: warps map
+// to sub-partitions by index mod 4); shared memory holds the peel's region (8,192 buckets),
+// then the DP's (1,024 staged in-edges per chunk).  The peel and DP talk through the
+// progress counter only, so one SM per graph and no co-scheduling.  Pair mode (k_peel_dp,
+// a single graph): the peel warp and the DP warps get an SM each, with the full-size tables
+// (cooperative launch: the two CTAs must be co-resident).
+constexpr int kPeelDpBatch = 8;
+constexpr int kPeelDpWarps = 6;
+constexpr int kDpPairWarps = 1 + kDpProducers;
 struct PeelDpBatch {
   PeelArgs pa[kPeelDpBatch];
   DpArgs da[kPeelDpBatch];
 };
+constexpr size_t kPeelSmemV5 = sizeof(int4) * kStackCache + sizeof(int64_t) * kFreedCap + sizeof(int32_t) * 96;
+constexpr size_t kPeelRegion = (std::max(kPeelSmemV5, sizeof(V6Smem<kV6BucketBits>)) + 127) / 128 * 128;
+constexpr size_t kPeelRegionShared = (std::max(kPeelSmemV5, sizeof(V6Smem<kV6BucketBitsShared>)) + 127) / 128 * 128;
+constexpr size_t kSmemPair =
+    std::max(kPeelRegion, std::max(sizeof(DpSmem), sizeof(DpSmem3<kE2Cap>)));
+constexpr size_t kSmemShared = kPeelRegionShared + std::max(sizeof(DpSmem), sizeof(DpSmem3<kE2CapShared>));
+static_assert(kSmemPair <= 227 * 1024 && kSmemShared <= 227 * 1024, "peel / DP shared memory exceeds one SM");
 
-__global__ void __launch_bounds__(kDpWarps * 32, 1) k_peel_dp(const __grid_constant__ PeelDpBatch b) {
+__global__ void __launch_bounds__(kDpPairWarps * 32, 1) k_peel_dp(const __grid_constant__ PeelDpBatch b) {
   extern __shared__ int4 smem4[];
   const int warp = threadIdx.x >> 5;
-  const PeelArgs& pa = b.pa[blockIdx.x >> 1];
-  const DpArgs& da = b.da[blockIdx.x >> 1];
-  if ((blockIdx.x & 1) == 0) {
-    if (warp == 0) peel_dispatch(pa, smem4);
-  } else if (da.v3) {
-    DpSmem3& S = *reinterpret_cast<DpSmem3*>(smem4);
+  if (blockIdx.x == 0) {
+    if (warp == 0) peel_dispatch<kV6BucketBits>(b.pa[0], smem4);
+    return;
+  }
+  const DpArgs& da = b.da[0];
+  if (da.v3) {
+    DpSmem3<kE2Cap>& S = *reinterpret_cast<DpSmem3<kE2Cap>*>(smem4);
     if (threadIdx.x < kDpProducers) S.ready[threadIdx.x] = -1;
     if (threadIdx.x == 0) S.consumed = 0;
     __syncthreads();
@@ -1359,6 +1390,28 @@ __global__ void __launch_bounds__(kDpWarps * 32, 1) k_peel_dp(const __grid_const
     else dp_producer(da, S, warp - 1, threadIdx.x & 31);
   } else if (warp == 0) {
     dp_warp(da, *reinterpret_cast<DpSmem*>(smem4));
+  }
+}
+
+__global__ void __launch_bounds__(kPeelDpWarps * 32, 1) k_peel_dp_shared(const __grid_constant__ PeelDpBatch b) {
+  extern __shared__ int4 smem4[];
+  const int warp = threadIdx.x >> 5;
+  const PeelArgs& pa = b.pa[blockIdx.x];
+  const DpArgs& da = b.da[blockIdx.x];
+  int4* dsm = smem4 + kPeelRegionShared / sizeof(int4);
+  DpSmem3<kE2CapShared>& S = *reinterpret_cast<DpSmem3<kE2CapShared>*>(dsm);
+  if (da.v3) {
+    if (threadIdx.x < kDpProducers) S.ready[threadIdx.x] = -1;
+    if (threadIdx.x == 0) S.consumed = 0;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    peel_dispatch<kV6BucketBitsShared>(pa, smem4);
+  } else if (warp == 1) {
+    if (da.v3) dp_compute_v3(da, S);
+    else dp_warp(da, *reinterpret_cast<DpSmem*>(dsm));
+  } else if (da.v3 && warp != 4) {
+    dp_producer(da, S, warp == 5 ? 2 : warp - 2, threadIdx.x & 31);
   }
 }
 
@@ -1504,9 +1557,7 @@ __global__ void k_out_sum(const int32_t* out_off, const int64_t* out_cost, int32
   }
 }
 
-size_t peel_smem() {
-  return std::max(sizeof(int4) * kStackCache + sizeof(int64_t) * kFreedCap + sizeof(int32_t) * 96, sizeof(V6Smem));
-}
+size_t peel_smem() { return kPeelRegion; }  // k_peel2 (topo_order)
 
 }  // namespace
 
@@ -1687,12 +1738,15 @@ PeelDpJob* peel_dp_prepare(DevGraph& g, const int64_t* cpath, int32_t range, int
 }
 
 void peel_dp_launch(dp_ctx* ctx, PeelDpJob* const* jobs, int count) {
-  const size_t sm = std::max(peel_smem(), std::max(sizeof(DpSmem), sizeof(DpSmem3)));
   static bool attr = false;
   if (!attr) {
-    DP_CUDA(cudaFuncSetAttribute(k_peel_dp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    DP_CUDA(cudaFuncSetAttribute(k_peel_dp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemPair)));
+    DP_CUDA(cudaFuncSetAttribute(k_peel_dp_shared, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kSmemShared)));
     attr = true;
   }
+  // one graph: pair mode (an SM each for peel and DP); several: shared mode (an SM per graph)
+  const bool pair = count == 1 && getenv("DP_PEEL_DP_SHARED") == nullptr;
   for (int b0 = 0; b0 < count; b0 += kPeelDpBatch) {
     const int k = std::min(kPeelDpBatch, count - b0);
     PeelDpBatch batch{};
@@ -1702,11 +1756,15 @@ void peel_dp_launch(dp_ctx* ctx, PeelDpJob* const* jobs, int count) {
       batch.da[q] = jobs[b0 + q]->da;
       bytes += jobs[b0 + q]->bytes;
     }
-    void* args[] = {&batch};
     StageScope s(ctx, "peel+dp (streamed)", bytes);
-    DP_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_peel_dp), 2 * k, kDpWarps * 32, args, sm,
-                                        ctx->stream));
-    ++ctx->launches;
+    if (pair) {
+      void* args[] = {&batch};
+      DP_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_peel_dp), 2, kDpPairWarps * 32, args,
+                                          kSmemPair, ctx->stream));
+      ++ctx->launches;
+    } else {
+      DP_LAUNCH(ctx, k_peel_dp_shared, k, kPeelDpWarps * 32, kSmemShared, batch);
+    }
   }
   for (int q = 0; q < count; ++q) {
     PeelDpJob* j = jobs[q];

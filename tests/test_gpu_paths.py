@@ -140,3 +140,24 @@ def test_levels_dataflow_lookahead(gpu, oracle, monkeypatch, ahead):
     # the lookahead only throttles ticket holders: any value must give the same levels
     monkeypatch.setenv("DP_FLOW_AHEAD", ahead)
     _levels_same(gpu, oracle, layered(35, 40000, 700))
+
+
+@pytest.mark.parametrize("case", ["r32", "r225", "r226", "wide_cost", "spill", "hub"])
+def test_shared_sm_mode(gpu, oracle, monkeypatch, case):
+    """The one-SM-per-graph peel + DP kernel used by batched calls (k_peel_dp_shared:
+    8,192 hash buckets, 1,024 staged in-edges per chunk), forced for single graphs."""
+    monkeypatch.setenv("DP_PEEL_DP_SHARED", "1")
+    if case == "spill":
+        g, r = layered(13, 120000, 40000, fan_lo=2, fan_hi=5), 200
+    elif case == "hub":
+        g, r = _fanin_hub(11, hubs=3, preds=400, n=20000), 150
+    elif case == "wide_cost":
+        g, r = layered(23, 6000, 32, nbytes=(1 << 26, 2 << 26)), 200
+    else:
+        g, r = layered(17, 12000, 48, fan_lo=4, fan_hi=12), int(case[1:])
+    total = int(g.memory_bytes.sum())
+    for limit in (total // 4, total // 300):
+        ca, ma = gpu.fuse(g, GEN, r, limit)
+        cb, mb = oracle.fuse(g, GEN, r, limit)
+        same_graph(ca, cb, case)
+        same_map(ma, mb, case)

@@ -1,0 +1,9 @@
+#!/bin/bash
+mkdir -p gpurun_out
+PYTHONUNBUFFERED=1 timeout 900 python -u -m pytest tests -m gpu -x -q --timeout 300 -p no:cacheprovider > gpurun_out/q_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/q_pytest.log
+timeout 300 python bench.py --steps 3 --warmup 1 --replicas 1 --batch 1 --no-e2e --no-cpu-baseline --candidates 0 --stages > gpurun_out/b_single.json 2> gpurun_out/b_single.err
+timeout 300 python bench.py --variant wide --steps 2 --warmup 1 --replicas 1 --batch 1 --no-e2e --no-cpu-baseline --candidates 0 --stages > gpurun_out/b_wide.json 2> gpurun_out/b_wide.err
+for RK in "32 2" "32 3" "32 4" "24 4" "16 8"; do set -- $RK
+  timeout 600 python bench.py --no-cpu-baseline --candidates 0 --no-e2e --steps 6 --replicas $1 --batch $2 > gpurun_out/d_r$1_k$2.json 2> gpurun_out/d_r$1_k$2.err
+done
+nvidia-smi --query-gpu=memory.used,memory.total --format=csv >> gpurun_out/d_mem.txt
