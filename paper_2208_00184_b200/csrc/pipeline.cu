@@ -86,34 +86,38 @@ void resident_validate(Resident& r, bool cycle_check) {
 }
 
 // The generation window (pipeline.cpp:67-79) after the streamed peel + DP: traceback and
-// coarse graph, coarse levels + cpd_topo, order_place + adjusting_placement, 2x expand.
-void generate_end(Resident& r, FuseStage& fs) {
+// coarse graph, coarse levels + cpd_topo, then the placement job (launched by the caller,
+// batched over graphs), then 2x expand.
+PlaceJob* generate_mid(Resident& r, FuseStage& fs) {
   dp_ctx* ctx = r.ctx;
-  DevGraph& g = r.g;
-  fuse_end(g, r.f, fs);
+  fuse_end(r.g, r.f, fs);
   DevGraph& coarse = r.f.coarse;
   levels_dev(coarse, r.comm, r.ct, r.cb, r.cc, true);  // clusters are runs of a topological order
   const int32_t k = coarse.n;
   r.cseq.alloc(ctx, k > 0 ? k : 1);
   r.cpos.alloc(ctx, k > 0 ? k : 1);
   topo_order(coarse, DP_TOPO_CPD, r.cc.p, r.cseq.p, r.cpos.p);
-  place_dev(coarse, r.cseq.p, r.devs, &r.po, &r.pa, r.decisions);
+  return place_prepare(coarse, r.cseq.p, r.devs, &r.po, &r.pa, r.decisions);
+}
+
+void generate_tail(Resident& r) {
+  dp_ctx* ctx = r.ctx;
+  DevGraph& g = r.g;
   const int32_t D = r.devs.D;
   r.dev_order.alloc(ctx, g.n > 0 ? g.n : 1);
   r.dev_adjust.alloc(ctx, g.n > 0 ? g.n : 1);
   r.pdm_order.alloc(ctx, D);
   r.pdm_adjust.alloc(ctx, D);
-  {
-    StageScope st(ctx, "expand", 2.0 * (12.0 * g.n));
-    expand_dev(g, r.f.node_cluster.p, r.po.dev.p, D, r.dev_order.p, r.pdm_order.p);
-    expand_dev(g, r.f.node_cluster.p, r.pa.dev.p, D, r.dev_adjust.p, r.pdm_adjust.p);
-  }
+  StageScope st(ctx, "expand", 2.0 * (12.0 * g.n));
+  expand_dev(g, r.f.node_cluster.p, r.po.dev.p, D, r.dev_order.p, r.pdm_order.p);
+  expand_dev(g, r.f.node_cluster.p, r.pa.dev.p, D, r.dev_adjust.p, r.pdm_adjust.p);
 }
 
 // Generation windows of independent graphs on one stream (graphs already validated, with
-// costs): each graph's fuse_begin, ONE launch of all the streamed peel + DP cores (4 graphs
-// per cooperative launch, 2 CTAs each), then each graph's generate_end.
+// costs): each graph's fuse_begin, ONE launch of all the streamed peel + DP cores, each
+// graph's traceback / coarse levels / cpd_topo, ONE launch of all the placements, expand.
 void generate_windows(Resident* const* rs, int count) {
+  dp_ctx* ctx = rs[0]->ctx;
   std::vector<std::unique_ptr<FuseStage>> fs;
   std::vector<PeelDpJob*> jobs;
   for (int i = 0; i < count; ++i) {
@@ -122,8 +126,15 @@ void generate_windows(Resident* const* rs, int count) {
     fuse_begin(r.g, r.comm, r.cfg.fusion_range, r.limit, r.f, *fs.back());
     if (fs.back()->streamed) jobs.push_back(fs.back()->job.j);
   }
-  if (!jobs.empty()) peel_dp_launch(rs[0]->ctx, jobs.data(), static_cast<int>(jobs.size()));
-  for (int i = 0; i < count; ++i) generate_end(*rs[i], *fs[i]);
+  if (!jobs.empty()) peel_dp_launch(ctx, jobs.data(), static_cast<int>(jobs.size()));
+  std::vector<std::unique_ptr<PlaceHandle>> ph;
+  std::vector<PlaceJob*> pj;
+  for (int i = 0; i < count; ++i) {
+    ph.emplace_back(new PlaceHandle(generate_mid(*rs[i], *fs[i])));
+    pj.push_back(ph.back()->j);
+  }
+  place_launch(ctx, pj.data(), count);
+  for (int i = 0; i < count; ++i) generate_tail(*rs[i]);
 }
 
 // Everything after the H2D upload: index, validation (pipeline.cpp:33), ccr (:58),

@@ -325,14 +325,22 @@ __device__ int32_t most_free(const int64_t* avail, int32_t D) {  // placement.cp
   return best;
 }
 
-__global__ void __launch_bounds__(256) k_place(PlaceArgs a) {
+// Up to kPlaceBatch independent (order, graph) jobs per launch: CTA 2j runs job j's
+// order_place, CTA 2j + 1 its adjusting_placement.
+constexpr int kPlaceBatch = 8;
+struct PlaceBatch {
+  PlaceArgs a[kPlaceBatch];
+};
+
+__global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatch batch) {
+  const PlaceArgs& a = batch.a[blockIdx.x >> 1];
   __shared__ int32_t sK[kMaxD], snb[kMaxD];
   __shared__ int64_t sg[kMaxD], sl[kMaxD], savail[kMaxD], spdm[kMaxD];
   __shared__ long long sA[kMaxD], sB[kMaxD];
   __shared__ int64_t sest[kMaxD], spre[kMaxD];
   __shared__ int32_t s_chosen, s_be;
   __shared__ int64_t s_start;
-  const int which = blockIdx.x;  // 0 order_place, 1 adjusting_placement
+  const int which = blockIdx.x & 1;  // 0 order_place, 1 adjusting_placement
   const long long t0 = clock64();
   if (!a.run[which]) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
@@ -551,12 +559,25 @@ Devices devices_sorted(const dp_devices_t* d) {
   return out;
 }
 
-void place_dev(DevGraph& g, const int32_t* seq, const Devices& devs, PlaceOut* order_out, PlaceOut* adjust_out,
-               bool want_decisions) {
+struct PlaceJob {
+  dp_ctx* ctx = nullptr;
+  PlaceArgs a{};
+  DevBuf<int64_t> back, cap, finish;
+  DevBuf<int64_t> store[2];
+  DevBuf<int32_t> store32[2];
+  DevBuf<long long> dbg;
+  size_t dyn = 0;
+};
+
+PlaceJob* place_prepare(DevGraph& g, const int32_t* seq, const Devices& devs, PlaceOut* order_out,
+                        PlaceOut* adjust_out, bool want_decisions) {
   dp_ctx* ctx = g.ctx;
   const int32_t n = g.n, D = devs.D;
   if (D > kMaxD) fail(DP_E_UNSUPPORTED, "at most %d devices are supported", kMaxD);
-  PlaceArgs a{};
+  auto* j = new PlaceJob;
+  PlaceHandle guard(j);
+  j->ctx = ctx;
+  PlaceArgs& a = j->a;
   a.n = n;
   a.D = D;
   a.seq = seq;
@@ -565,19 +586,20 @@ void place_dev(DevGraph& g, const int32_t* seq, const Devices& devs, PlaceOut* o
   a.in_off = g.in_off.p;
   a.in_src = g.in_src.p;
   a.in_cost = g.in_cost.p;
-  DevBuf<int64_t> back(ctx, n > 0 ? n : 1), cap(ctx, D), finish(ctx, n > 0 ? n : 1);
-  cap.upload(devs.cap.data(), D);
-  DP_LAUNCH(ctx, k_back_cost, grid_for(n, 256), 256, 0, g.out_off.p, g.has_cost ? g.out_cost.p : nullptr, n, back.p);
-  a.back = back.p;
-  a.cap = cap.p;
-  a.finish = finish.p;
-  DevBuf<int64_t> store[2];
-  DevBuf<int32_t> store32[2];
+  j->back.alloc(ctx, n > 0 ? n : 1);
+  j->cap.alloc(ctx, D);
+  j->finish.alloc(ctx, n > 0 ? n : 1);
+  j->cap.upload(devs.cap.data(), D);
+  DP_LAUNCH(ctx, k_back_cost, grid_for(n, 256), 256, 0, g.out_off.p, g.has_cost ? g.out_cost.p : nullptr, n,
+            j->back.p);
+  a.back = j->back.p;
+  a.cap = j->cap.p;
+  a.finish = j->finish.p;
   PlaceOut* outs[2] = {order_out, adjust_out};
   for (int w = 0; w < 2; ++w) {
     a.run[w] = outs[w] != nullptr;
     if (!outs[w]) continue;
-    alloc_tl(ctx, D, n > 0 ? n : 1, store[w], store32[w], a.tl[w]);
+    alloc_tl(ctx, D, n > 0 ? n : 1, j->store[w], j->store32[w], a.tl[w]);
     outs[w]->dev.alloc(ctx, n > 0 ? n : 1);
     outs[w]->per_dev_mem.alloc(ctx, D);
     outs[w]->flags.alloc(ctx, 1);
@@ -600,29 +622,54 @@ void place_dev(DevGraph& g, const int32_t* seq, const Devices& devs, PlaceOut* o
     a.dec_reloc = adjust_out->dec_reloc.p;
     a.dec_be = adjust_out->dec_be.p;
   }
-  StageScope st(ctx, "placement", 0.0);
   // block meta on chip when it fits: (5 x 8 + 2 x 4) bytes per block slot
   const size_t meta_bytes = static_cast<size_t>(48) * D * std::max(a.tl[0].maxb, a.tl[1].maxb);
   a.meta_smem = meta_bytes <= 190 * 1024 && getenv("DP_PLACE_GLOBAL_META") == nullptr;
-  const size_t dyn = a.meta_smem ? meta_bytes : 0;
-  if (dyn) {
-    static size_t attr = 0;
-    if (dyn > attr) {
-      DP_CUDA(cudaFuncSetAttribute(k_place, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
-      attr = dyn;
+  j->dyn = a.meta_smem ? meta_bytes : 0;
+  j->dbg.alloc(ctx, 2);
+  a.debug = getenv("DP_DEBUG_PLACE") ? j->dbg.p : nullptr;
+  if (a.debug) j->dbg.zero();
+  guard.j = nullptr;
+  return j;
+}
+
+void place_launch(dp_ctx* ctx, PlaceJob* const* jobs, int count) {
+  StageScope st(ctx, "placement", 0.0);
+  for (int b0 = 0; b0 < count; b0 += kPlaceBatch) {
+    const int k = std::min(kPlaceBatch, count - b0);
+    PlaceBatch batch{};
+    size_t dyn = 0;
+    for (int q = 0; q < k; ++q) {
+      batch.a[q] = jobs[b0 + q]->a;
+      dyn = std::max(dyn, jobs[b0 + q]->dyn);
+    }
+    if (dyn) {
+      static size_t attr = 0;
+      if (dyn > attr) {
+        DP_CUDA(cudaFuncSetAttribute(k_place, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
+        attr = dyn;
+      }
+    }
+    DP_LAUNCH(ctx, k_place, 2 * k, 256, dyn, batch);
+  }
+  for (int q = 0; q < count; ++q) {
+    PlaceJob* j = jobs[q];
+    if (j->a.debug) {
+      long long h[2];
+      j->dbg.download(h, 2);
+      sync(ctx);
+      fprintf(stderr, "[place] order_place %.2f ms, adjusting %.2f ms (n=%d, D=%d, meta %s)\n", h[0] / 1.965e6,
+              h[1] / 1.965e6, j->a.n, j->a.D, j->a.meta_smem ? "smem" : "global");
     }
   }
-  DevBuf<long long> dbg(ctx, 2);
-  a.debug = getenv("DP_DEBUG_PLACE") ? dbg.p : nullptr;
-  if (a.debug) dbg.zero();
-  DP_LAUNCH(ctx, k_place, 2, 256, dyn, a);
-  if (a.debug) {
-    long long h[2];
-    dbg.download(h, 2);
-    sync(ctx);
-    fprintf(stderr, "[place] order_place %.2f ms, adjusting %.2f ms (n=%d, D=%d, meta %s)\n", h[0] / 1.965e6,
-            h[1] / 1.965e6, n, D, a.meta_smem ? "smem" : "global");
-  }
+}
+
+void place_release(PlaceJob* j) { delete j; }
+
+void place_dev(DevGraph& g, const int32_t* seq, const Devices& devs, PlaceOut* order_out, PlaceOut* adjust_out,
+               bool want_decisions) {
+  PlaceHandle h(place_prepare(g, seq, devs, order_out, adjust_out, want_decisions));
+  place_launch(g.ctx, &h.j, 1);
 }
 
 void expand_dev(DevGraph& g, const int32_t* node_cluster, const int32_t* coarse_dev, int32_t D, int32_t* dev_node,

@@ -29,6 +29,23 @@ struct PlaceOut {
 void place_dev(DevGraph& g, const int32_t* seq, const Devices& devs, PlaceOut* order_out, PlaceOut* adjust_out,
                bool want_decisions);
 
+// place_dev split so that independent graphs share one launch (2 CTAs per graph, up to 8
+// graphs per launch): prepare each job, launch them together, release after the outputs
+// have been consumed.
+struct PlaceJob;
+PlaceJob* place_prepare(DevGraph& g, const int32_t* seq, const Devices& devs, PlaceOut* order_out,
+                        PlaceOut* adjust_out, bool want_decisions);
+void place_launch(dp_ctx* ctx, PlaceJob* const* jobs, int count);
+void place_release(PlaceJob* j);
+struct PlaceHandle {
+  PlaceJob* j = nullptr;
+  PlaceHandle() = default;
+  explicit PlaceHandle(PlaceJob* x) : j(x) {}
+  PlaceHandle(const PlaceHandle&) = delete;
+  PlaceHandle& operator=(const PlaceHandle&) = delete;
+  ~PlaceHandle() { place_release(j); }
+};
+
 // expand_placement (placement.cpp:239-268) as a gather: dev_node[v] = coarse_dev[cl[v]],
 // per-device memory sums.
 void expand_dev(DevGraph& g, const int32_t* node_cluster, const int32_t* coarse_dev, int32_t D, int32_t* dev_node,
