@@ -77,7 +77,7 @@ __global__ void k_find_direct(const int32_t* out_off, const int32_t* out_dst, co
 
 }  // namespace
 
-dp_graph_out_t* graph_to_host(DevGraph& g, bool dense_ids_out) {
+dp_graph_out_t* graph_to_host_async(DevGraph& g, bool dense_ids_out, Finalizers& fin) {
   dp_ctx* ctx = g.ctx;
   dp_graph_out_t* o = new_graph_out(g.n, g.m);
   if (dense_ids_out) {
@@ -88,17 +88,30 @@ dp_graph_out_t* graph_to_host(DevGraph& g, bool dense_ids_out) {
   g.w.download(o->compute_us, g.n);
   g.mem.download(o->memory_bytes, g.n);
   if (g.has_group) g.group.download(o->group, g.n);
-  std::vector<int32_t> s = to_host(ctx, g.esrc.p, g.m), d = to_host(ctx, g.edst.p, g.m);
-  g.bytes.download(o->edge_bytes, g.m);
-  std::vector<int64_t> ids;
-  if (!dense_ids_out) ids.assign(o->node_id, o->node_id + g.n);
-  sync(ctx);
-  if (!g.has_group)
-    for (int32_t i = 0; i < g.n; ++i) o->group[i] = -1;
-  for (int32_t e = 0; e < g.m; ++e) {
-    o->edge_src[e] = dense_ids_out ? s[e] : ids[s[e]];
-    o->edge_dst[e] = dense_ids_out ? d[e] : ids[d[e]];
+  auto s = std::make_shared<std::vector<int32_t>>(g.m), d = std::make_shared<std::vector<int32_t>>(g.m);
+  if (g.m) {
+    download_bytes(ctx, s->data(), g.esrc.p, sizeof(int32_t) * g.m);
+    download_bytes(ctx, d->data(), g.edst.p, sizeof(int32_t) * g.m);
   }
+  g.bytes.download(o->edge_bytes, g.m);
+  const bool has_group = g.has_group;
+  const int32_t n = g.n, m = g.m;
+  fin.push_back([o, s, d, dense_ids_out, has_group, n, m] {
+    if (!has_group)
+      for (int32_t i = 0; i < n; ++i) o->group[i] = -1;
+    for (int32_t e = 0; e < m; ++e) {
+      o->edge_src[e] = dense_ids_out ? (*s)[e] : o->node_id[(*s)[e]];
+      o->edge_dst[e] = dense_ids_out ? (*d)[e] : o->node_id[(*d)[e]];
+    }
+  });
+  return o;
+}
+
+dp_graph_out_t* graph_to_host(DevGraph& g, bool dense_ids_out) {
+  Finalizers fin;
+  dp_graph_out_t* o = graph_to_host_async(g, dense_ids_out, fin);
+  sync(g.ctx);
+  for (auto& x : fin) x();
   return o;
 }
 

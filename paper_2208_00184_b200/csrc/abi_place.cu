@@ -32,34 +32,56 @@ void graph_index_checks(DevGraph& g, const dp_graph_t* h) {
 }
 
 // Host view of a device placement (device positions -> ids).
-dp_placement_result_t* placement_to_host(dp_ctx* ctx, const Devices& devs, PlaceOut& p, int32_t n,
-                                         const std::vector<int64_t>* seq_ids, bool decisions) {
+dp_placement_result_t* placement_to_host_async(dp_ctx* ctx, const Devices& devs, PlaceOut& p, int32_t n,
+                                               std::shared_ptr<const std::vector<int64_t>> seq_ids, bool decisions,
+                                               Finalizers& fin) {
   const int32_t D = devs.D;
   dp_placement_result_t* r = new_placement(n, D, decisions ? n : 0);
-  std::vector<int32_t> dev = to_host(ctx, p.dev.p, n);
-  std::vector<int64_t> pdm = to_host(ctx, p.per_dev_mem.p, D);
-  int32_t oom = scalar_to_host(ctx, p.flags.p);
-  for (int32_t v = 0; v < n; ++v) r->device[v] = devs.ids[dev[v]];
-  for (int32_t d = 0; d < D; ++d) {
-    r->device_ids[d] = devs.ids[d];
-    r->per_device_memory[d] = pdm[d];
-    r->device_present[d] = 1;
-  }
-  r->oom_risk = oom;
-  if (decisions && n) {
-    std::vector<int32_t> prev = to_host(ctx, p.dec_prev.p, n), ch = to_host(ctx, p.dec_chosen.p, n);
-    std::vector<int64_t> est = to_host(ctx, p.dec_est.p, (size_t)n * D);
+  auto dev = std::make_shared<std::vector<int32_t>>(n);
+  auto pdm = std::make_shared<std::vector<int64_t>>(D);
+  auto oom = std::make_shared<int32_t>(0);
+  if (n) download_bytes(ctx, dev->data(), p.dev.p, sizeof(int32_t) * n);
+  download_bytes(ctx, pdm->data(), p.per_dev_mem.p, sizeof(int64_t) * D);
+  download_bytes(ctx, oom.get(), p.flags.p, sizeof(int32_t));
+  auto prev = std::make_shared<std::vector<int32_t>>(), ch = std::make_shared<std::vector<int32_t>>();
+  const bool dec = decisions && n;
+  if (dec) {
+    prev->resize(n);
+    ch->resize(n);
+    download_bytes(ctx, prev->data(), p.dec_prev.p, sizeof(int32_t) * n);
+    download_bytes(ctx, ch->data(), p.dec_chosen.p, sizeof(int32_t) * n);
+    p.dec_est.download(r->dec_est, (size_t)n * D);
     p.dec_back.download(r->dec_back_cost, n);
     p.dec_reloc.download(r->dec_relocated, n);
     p.dec_be.download(r->dec_best_effort, n);
-    sync(ctx);
-    for (int32_t k = 0; k < n; ++k) {
-      r->dec_node[k] = (*seq_ids)[k];
-      r->dec_prev[k] = devs.ids[prev[k]];
-      r->dec_chosen[k] = devs.ids[ch[k]];
-    }
-    std::memcpy(r->dec_est, est.data(), sizeof(int64_t) * est.size());
   }
+  std::vector<int32_t> ids = devs.ids;
+  fin.push_back([r, dev, pdm, oom, prev, ch, dec, ids, seq_ids, n, D] {
+    for (int32_t v = 0; v < n; ++v) r->device[v] = ids[(*dev)[v]];
+    for (int32_t d = 0; d < D; ++d) {
+      r->device_ids[d] = ids[d];
+      r->per_device_memory[d] = (*pdm)[d];
+      r->device_present[d] = 1;
+    }
+    r->oom_risk = *oom;
+    if (dec) {
+      for (int32_t k = 0; k < n; ++k) {
+        r->dec_node[k] = (*seq_ids)[k];
+        r->dec_prev[k] = ids[(*prev)[k]];
+        r->dec_chosen[k] = ids[(*ch)[k]];
+      }
+    }
+  });
+  return r;
+}
+
+dp_placement_result_t* placement_to_host(dp_ctx* ctx, const Devices& devs, PlaceOut& p, int32_t n,
+                                         const std::vector<int64_t>* seq_ids, bool decisions) {
+  Finalizers fin;
+  auto seq = std::make_shared<const std::vector<int64_t>>(seq_ids ? *seq_ids : std::vector<int64_t>());
+  dp_placement_result_t* r = placement_to_host_async(ctx, devs, p, n, seq, decisions, fin);
+  sync(ctx);
+  for (auto& x : fin) x();
   return r;
 }
 

@@ -1,5 +1,7 @@
 // common.cuh — context, stream-ordered buffers, errors, launch accounting, grid barrier.
 #pragma once
+#include <functional>
+#include <memory>
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -171,6 +173,9 @@ struct DevBuf {
 void download_bytes(dp_ctx* ctx, void* host, const void* dev, size_t bytes);
 // Waits for the context stream and completes the pending D2H copies.
 void sync(dp_ctx* ctx);
+// Host-side steps to run after the next sync(ctx), in order (results assembled from
+// downloads that several graphs enqueue before one sync).
+using Finalizers = std::vector<std::function<void()>>;
 // Drops pending copies (error paths: their destinations may be gone).
 void discard_pending(dp_ctx* ctx);
 

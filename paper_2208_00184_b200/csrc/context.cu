@@ -91,11 +91,14 @@ void download_bytes(dp_ctx* ctx, void* host, const void* dev, size_t bytes) {
   const size_t need = (bytes + 255) & ~static_cast<size_t>(255);
   if (ctx->pin_off + need > ctx->pin_cap) {
     sync(ctx);  // completes (and empties) the pending copies
+    // grow only for a single copy larger than the arena: growing to everything pending
+    // (hundreds of MB per context) costs cudaFreeHost / cudaHostAlloc, which stall every
+    // stream, for no measured gain
     if (need > ctx->pin_cap) {
       if (ctx->pin) cudaFreeHost(ctx->pin);
       ctx->pin = nullptr;
       ctx->pin_cap = 0;
-      const size_t cap = std::max<size_t>(need, std::max<size_t>(1 << 20, 2 * ctx->pin_cap));
+      const size_t cap = std::max<size_t>(need, 1 << 20);
       DP_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->pin), cap, cudaHostAllocDefault));
       ctx->pin_cap = cap;
     }

@@ -722,7 +722,7 @@ void fuse_dev(DevGraph& g, dp_comm_t comm, int32_t range, int64_t limit, FuseOut
   fuse_end(g, out, fs);
 }
 
-dp_cluster_map_t* fuse_map_to_host(DevGraph& g, FuseOut& f) {
+dp_cluster_map_t* fuse_map_to_host_async(DevGraph& g, FuseOut& f, Finalizers& fin) {
   dp_ctx* ctx = g.ctx;
   const int B = 256;
   DevGraph& work = f.con.identity ? g : f.con.work;
@@ -736,14 +736,25 @@ dp_cluster_map_t* fuse_map_to_host(DevGraph& g, FuseOut& f) {
             (f.con.identity && g.dense_ids) ? nullptr : work.id.p, poff.p, members.p);
   dp_cluster_map_t* m = new_cluster_map(g.n, k, k > 0 ? k - 1 : 0);
   f.node_cluster.download(m->node_cluster, g.n);
-  members.download(m->members, g.n);
+  members.download(m->members, g.n);  // stream-ordered: the buffers are freed after the copies
   f.cl.tot_w.download(m->total_compute, k);
   f.cl.tot_mem.download(m->total_memory, k);
-  std::vector<int32_t> cuts = to_host(ctx, f.cl.cut_pos.p, (size_t)k + 1);
-  std::vector<int64_t> po = to_host(ctx, poff.p, (size_t)nw + 1);
-  for (int32_t c = 0; c <= k; ++c) m->member_off[c] = po[cuts[c]];
-  for (int32_t c = 1; c < k; ++c) m->breakpoints[c - 1] = cuts[c];
-  sync(ctx);
+  auto cuts = std::make_shared<std::vector<int32_t>>((size_t)k + 1);
+  auto po = std::make_shared<std::vector<int64_t>>((size_t)nw + 1);
+  download_bytes(ctx, cuts->data(), f.cl.cut_pos.p, sizeof(int32_t) * ((size_t)k + 1));
+  download_bytes(ctx, po->data(), poff.p, sizeof(int64_t) * ((size_t)nw + 1));
+  fin.push_back([m, cuts, po, k] {
+    for (int32_t c = 0; c <= k; ++c) m->member_off[c] = (*po)[(*cuts)[c]];
+    for (int32_t c = 1; c < k; ++c) m->breakpoints[c - 1] = (*cuts)[c];
+  });
+  return m;
+}
+
+dp_cluster_map_t* fuse_map_to_host(DevGraph& g, FuseOut& f) {
+  Finalizers fin;
+  dp_cluster_map_t* m = fuse_map_to_host_async(g, f, fin);
+  sync(g.ctx);
+  for (auto& x : fin) x();
   return m;
 }
 

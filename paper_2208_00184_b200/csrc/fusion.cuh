@@ -69,5 +69,7 @@ void fuse_end(DevGraph& g, FuseOut& out, FuseStage& fs);
 
 // ClusterMap re-expressed over original ids (fusion.cpp:317-333) into host buffers.
 dp_cluster_map_t* fuse_map_to_host(DevGraph& g, FuseOut& f);
+// ... enqueueing its downloads; the map is complete after sync(ctx) and `fin`.
+dp_cluster_map_t* fuse_map_to_host_async(DevGraph& g, FuseOut& f, Finalizers& fin);
 
 }  // namespace dpb

@@ -5,6 +5,7 @@
 // (fuse -> coarse levels + cpd_topo -> order_place + adjusting_placement -> 2x expand)
 // runs as one stream of kernels; only the results cross PCIe.
 #include <algorithm>
+#include <array>
 #include <memory>
 
 #include "abi_util.cuh"
@@ -16,9 +17,10 @@
 
 namespace dpb {
 
-dp_graph_out_t* graph_to_host(DevGraph& g, bool dense_ids_out);
-dp_placement_result_t* placement_to_host(dp_ctx* ctx, const Devices& devs, PlaceOut& p, int32_t n,
-                                         const std::vector<int64_t>* seq_ids, bool decisions);
+dp_graph_out_t* graph_to_host_async(DevGraph& g, bool dense_ids_out, Finalizers& fin);
+dp_placement_result_t* placement_to_host_async(dp_ctx* ctx, const Devices& devs, PlaceOut& p, int32_t n,
+                                               std::shared_ptr<const std::vector<int64_t>> seq_ids, bool decisions,
+                                               Finalizers& fin);
 dp_sim_report_t* sim_report(DevGraph& g, const Devices& devs, const int32_t* dev_pos_dev, bool trace);
 
 namespace {
@@ -167,23 +169,43 @@ void resident_init(Resident& r, dp_ctx* ctx, const dp_graph_t* h, const dp_devic
 }
 
 // Expanded placement with every device listed (present where it received nodes).
-dp_placement_result_t* expanded_to_host(dp_ctx* ctx, const Devices& devs, const int32_t* dev, const int64_t* pdm,
-                                        int32_t n) {
+dp_placement_result_t* expanded_to_host_async(dp_ctx* ctx, const Devices& devs, const int32_t* dev,
+                                              const int64_t* pdm, int32_t n, Finalizers& fin) {
   const int32_t D = devs.D;
   dp_placement_result_t* p = new_placement(n, D, 0);
-  std::vector<int32_t> d = to_host(ctx, dev, n);
-  std::vector<int64_t> m = to_host(ctx, pdm, D);
-  std::vector<uint8_t> present(D, 0);
-  for (int32_t v = 0; v < n; ++v) {
-    p->device[v] = devs.ids[d[v]];
-    present[d[v]] = 1;
-  }
-  for (int32_t i = 0; i < D; ++i) {
-    p->device_ids[i] = devs.ids[i];
-    p->per_device_memory[i] = present[i] ? m[i] : 0;
-    p->device_present[i] = present[i];
-  }
+  auto d = std::make_shared<std::vector<int32_t>>(n);
+  auto m = std::make_shared<std::vector<int64_t>>(D);
+  if (n) download_bytes(ctx, d->data(), dev, sizeof(int32_t) * n);
+  download_bytes(ctx, m->data(), pdm, sizeof(int64_t) * D);
+  std::vector<int32_t> ids = devs.ids;
+  fin.push_back([p, d, m, ids, n, D] {
+    std::vector<uint8_t> present(D, 0);
+    for (int32_t v = 0; v < n; ++v) {
+      p->device[v] = ids[(*d)[v]];
+      present[(*d)[v]] = 1;
+    }
+    for (int32_t i = 0; i < D; ++i) {
+      p->device_ids[i] = ids[i];
+      p->per_device_memory[i] = present[i] ? (*m)[i] : 0;
+      p->device_present[i] = present[i];
+    }
+  });
   return p;
+}
+
+// ccr (graph.cpp:206-215) of a device graph into *out after sync(ctx) and `fin`.
+void ccr_async(DevGraph& g, double* out, Finalizers& fin) {
+  dp_ctx* ctx = g.ctx;
+  DevBuf<unsigned long long> s(ctx, 2);
+  s.zero();
+  DP_LAUNCH(ctx, k_ccr, grid_for(std::max(g.n, g.m), 256, 4 * ctx->num_sms), 256, 0, g.w.p, g.n, g.cost.p, g.m, s.p);
+  auto h = std::make_shared<std::array<unsigned long long, 2>>();
+  download_bytes(ctx, h->data(), s.p, sizeof(unsigned long long) * 2);
+  fin.push_back([h, out] {
+    const int64_t tc = static_cast<int64_t>((*h)[0]);
+    if (tc <= 0) fail(DP_E_ZERO_COMPUTE_TIME, "total compute time is zero");
+    *out = static_cast<double>(static_cast<int64_t>((*h)[1])) / static_cast<double>(tc);
+  });
 }
 
 }  // namespace dpb
@@ -251,6 +273,8 @@ int dp_pipeline_batch(dp_ctx_t* ctx, int32_t count, const dp_graph_t* const* gra
   float ms = 0;
   DP_CUDA(cudaEventSynchronize(e1));
   DP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  // every graph's downloads first, one sync, then the host-side assembly
+  Finalizers fin;
   for (int32_t i = 0; i < count; ++i) {
     Resident& r = *rp[i];
     DevGraph& coarse = r.f.coarse;
@@ -262,25 +286,33 @@ int dp_pipeline_batch(dp_ctx_t* ctx, int32_t count, const dp_graph_t* const* gra
     x->coarse_nodes = k;
     x->coarse_edges = coarse.m;
     x->fusion = halloc<dp_fusion_result_t>(1);
-    x->fusion->coarse = graph_to_host(coarse, true);
-    x->fusion->map = fuse_map_to_host(r.g, r.f);
-    std::vector<int32_t> cs = to_host(ctx, r.cseq.p, k);
+    x->fusion->coarse = graph_to_host_async(coarse, true, fin);
+    x->fusion->map = fuse_map_to_host_async(r.g, r.f, fin);
+    auto cs = std::make_shared<std::vector<int32_t>>(k);
+    if (k) download_bytes(ctx, cs->data(), r.cseq.p, sizeof(int32_t) * k);
     x->coarse_sequence = halloc<int64_t>(k);
-    std::vector<int64_t> cids(static_cast<size_t>(k));
-    for (int32_t q = 0; q < k; ++q) cids[q] = x->coarse_sequence[q] = cs[q];
-    x->coarse_order = placement_to_host(ctx, r.devs, r.po, k, &cids, false);
-    x->coarse_adjust = placement_to_host(ctx, r.devs, r.pa, k, &cids, true);
-    x->order_expanded = expanded_to_host(ctx, r.devs, r.dev_order.p, r.pdm_order.p, n);
-    x->adjust_expanded = expanded_to_host(ctx, r.devs, r.dev_adjust.p, r.pdm_adjust.p, n);
+    auto cids = std::make_shared<std::vector<int64_t>>(static_cast<size_t>(k));
+    fin.push_back([x, cs, cids, k] {
+      for (int32_t q = 0; q < k; ++q) (*cids)[q] = x->coarse_sequence[q] = (*cs)[q];
+    });
+    x->coarse_order = placement_to_host_async(ctx, r.devs, r.po, k, cids, false, fin);
+    x->coarse_adjust = placement_to_host_async(ctx, r.devs, r.pa, k, cids, true, fin);
+    x->order_expanded = expanded_to_host_async(ctx, r.devs, r.dev_order.p, r.pdm_order.p, n, fin);
+    x->adjust_expanded = expanded_to_host_async(ctx, r.devs, r.dev_adjust.p, r.pdm_adjust.p, n, fin);
     x->generation_ms = ms;  // the window of the whole call (all graphs of a batch)
     x->coarse_ccr = 0.0;
-    if (coarse.m > 0) x->coarse_ccr = ccr_dev(coarse);  // pipeline.cpp:83
+    if (coarse.m > 0) ccr_async(coarse, &x->coarse_ccr, fin);  // pipeline.cpp:83
     x->order_makespan = x->adjust_makespan = -1;
-    if (cfg->simulate) {  // pipeline.cpp:89-90
+  }
+  sync(ctx);
+  for (auto& f : fin) f();
+  if (cfg->simulate) {  // pipeline.cpp:89-90
+    for (int32_t i = 0; i < count; ++i) {
+      Resident& r = *rp[i];
       dp_sim_report_t* so = sim_report(r.g, r.devs, r.dev_order.p, false);
       dp_sim_report_t* sa = sim_report(r.g, r.devs, r.dev_adjust.p, false);
-      x->order_makespan = so->makespan;
-      x->adjust_makespan = sa->makespan;
+      res[i]->order_makespan = so->makespan;
+      res[i]->adjust_makespan = sa->makespan;
       free_sim(so);
       free_sim(sa);
     }
