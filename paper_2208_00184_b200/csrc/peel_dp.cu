@@ -71,6 +71,7 @@ struct PeelArgs {
   int32_t* gsid;         // global stack of {node | long flag}
   int32_t* gover;        // remaining in-degree of keys spilled from full buckets (0 = absent)
   long long* debug;      // optional: peel warp cycles
+  bool prefetch;         // v6: prefetch the rows of a pushed child's children to L2
 };
 
 // The peel warp.  Shared memory: stack cache (kStackCache int4) + freed buffer.
@@ -485,7 +486,11 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem<BB>& S) {
   int32_t p = 0, held = 0;
   int32_t* const seq = a.seq;
   int32_t* const pos_of = a.pos_of;
-  const int4* const ell6 = a.ell6;
+  // per-lane row base kept in a register (not re-read from the parameter bank each step)
+  const int4* ell6l = a.ell6 + (lane & 3);
+  const int4* ell6 = a.ell6;
+  asm volatile("" : "+l"(ell6l), "+l"(ell6));
+  const bool pf = a.prefetch;
   while (top >= 0) {
     if (top < base) {
       base = max(0, top + 1 - SC / 2);
@@ -569,7 +574,7 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem<BB>& S) {
     // ---- 8-slot row on chip (slots sorted by rank)
     const int q = lane >> 2;
     int4 crow = make_int4(-1, 0, -1, 0);
-    if (cq.x >= 0) crow = ell6[static_cast<int64_t>(cq.x) * 4 + (lane & 3)];
+    if (cq.x >= 0) crow = ell6l[static_cast<int64_t>(cq.x) * 4];
     bool fr = false;
     if (lane < 8 && my.x >= 0) {
       // branch-light table step: one bucket load; remaining = table value on a hit, the
@@ -609,8 +614,10 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem<BB>& S) {
       // pushed in descending rank: slot k lands above every freed slot of higher rank
       if ((m >> q) & 1u) {
         S.row[(top + 1 + __popc(m >> q >> 1)) & (SC - 1)][lane & 3] = crow;
-        if (crow.x >= 0) prefetch_l2(ell6 + static_cast<int64_t>(crow.x) * 4);
-        if (crow.z >= 0) prefetch_l2(ell6 + static_cast<int64_t>(crow.z) * 4);
+        if (pf) {
+          if (crow.x >= 0) prefetch_l2(ell6 + static_cast<int64_t>(crow.x) * 4);
+          if (crow.z >= 0) prefetch_l2(ell6 + static_cast<int64_t>(crow.z) * 4);
+        }
       }
       if (fr) S.sid[(top + 1 + __popc(m >> lane >> 1)) & (SC - 1)] = my.x | (my.y < 0 ? kV6Long : 0);
       top += nf;
@@ -1653,6 +1660,7 @@ static PeelArgs peel_args(DevGraph& g, PeelState& st, int32_t* seq, int32_t* pos
   a.rem_big = st.indeg.p;
   a.gsid = st.gsid.p;
   a.gover = st.gover.p;
+  a.prefetch = getenv("DP_PEEL_NO_PREFETCH") == nullptr;
   return a;
 }
 
