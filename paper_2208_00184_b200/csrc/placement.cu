@@ -407,18 +407,83 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
     return;
   }
   // adjusting_placement (placement.cpp:172-216)
+  // The static inputs of a step are loaded in a software pipeline over the order, one
+  // dependent stage per step, so no step waits on a chain of global loads: during step k
+  // the CTA loads node k+3's id, node k+2's row bounds / compute / memory, this thread's
+  // in-edge of node k+1 (source, cost) and the finish time / device of node k+1's source
+  // (final unless that source is node k, which is patched from shared memory at step k+1).
+  // In-edges beyond blockDim.x per node are read in the step itself.
+  __shared__ int64_t s_prev_finish;
+  __shared__ int32_t s_prev_v;
   int32_t prev = 0;
   bool oom = false;
-  for (int32_t k = 0; k < a.n; ++k) {
-    const int32_t v = a.seq[k];
-    const int64_t w = a.w[v], mv = a.mem[v];
+  const int32_t n = a.n;
+  const int T = blockDim.x;
+  // stage registers: s (seq id), b (row), c (edge), d (edge with finish/device)
+  int32_t s_v = -1;
+  int32_t b_v = -1, b_ib = 0, b_ie = 0;
+  int64_t b_w = 0, b_mv = 0;
+  int32_t c_v = -1, c_ib = 0, c_ie = 0, c_p = -1;
+  int64_t c_w = 0, c_mv = 0, c_c = 0;
+  int32_t d_v = -1, d_ib = 0, d_ie = 0, d_p = -1, d_dd = 0;
+  int64_t d_w = 0, d_mv = 0, d_c = 0, d_f = 0;
+  if (tid == 0) s_prev_v = -1;
+  // prime: the stages for k = 0 (edges + finish), 1 (edges), 2 (row), 3 (seq id)
+  auto advance = [&](int32_t k) {  // loads issued at step k, consumed one step later
+    // node k+1: finish / device of this thread's in-edge source (from stage c)
+    int32_t nd_v = c_v, nd_ib = c_ib, nd_ie = c_ie, nd_p = c_p, nd_dd = 0;
+    int64_t nd_w = c_w, nd_mv = c_mv, nd_c = c_c, nd_f = 0;
+    if (nd_p >= 0) {
+      nd_f = a.finish[nd_p];
+      nd_dd = dev[nd_p];
+    }
+    // node k+2: this thread's in-edge (from stage b)
+    int32_t nc_v = b_v, nc_ib = b_ib, nc_ie = b_ie, nc_p = -1;
+    int64_t nc_w = b_w, nc_mv = b_mv, nc_c = 0;
+    if (nc_v >= 0 && nc_ib + tid < nc_ie) {
+      nc_p = a.in_src[nc_ib + tid];
+      nc_c = a.in_cost[nc_ib + tid];
+    }
+    // node k+3: row bounds, compute, memory (from stage s)
+    int32_t nb_v = s_v, nb_ib = 0, nb_ie = 0;
+    int64_t nb_w = 0, nb_mv = 0;
+    if (nb_v >= 0) {
+      nb_ib = a.in_off[nb_v];
+      nb_ie = a.in_off[nb_v + 1];
+      nb_w = a.w[nb_v];
+      nb_mv = a.mem[nb_v];
+    }
+    // node k+4: id
+    const int32_t ns_v = k + 4 < n ? a.seq[k + 4] : -1;
+    d_v = nd_v; d_ib = nd_ib; d_ie = nd_ie; d_p = nd_p; d_dd = nd_dd; d_w = nd_w; d_mv = nd_mv; d_c = nd_c; d_f = nd_f;
+    c_v = nc_v; c_ib = nc_ib; c_ie = nc_ie; c_p = nc_p; c_w = nc_w; c_mv = nc_mv; c_c = nc_c;
+    b_v = nb_v; b_ib = nb_ib; b_ie = nb_ie; b_w = nb_w; b_mv = nb_mv;
+    s_v = ns_v;
+  };
+  for (int32_t k = -4; k < 0; ++k) advance(k);  // after this: d = node 0, c = 1, b = 2, s = 3
+  __syncthreads();
+  for (int32_t k = 0; k < n; ++k) {
+    const int32_t v = d_v;
+    const int64_t w = d_w, mv = d_mv;
+    // this step's inputs, then the next steps' loads (consumed from step k+1 on)
+    const int32_t my_p = d_p, my_dd0 = d_dd, ib = d_ib, ie = d_ie;
+    const int64_t my_c = d_c, my_f0 = d_f;
+    const int32_t pv = s_prev_v;
+    const int64_t pf = s_prev_finish;
+    advance(k);
     for (int d = tid; d < D; d += blockDim.x) {
       sA[d] = LLONG_MIN;
       sB[d] = LLONG_MIN;
     }
     __syncthreads();
-    const int32_t ib = a.in_off[v], ie = a.in_off[v + 1];
-    for (int32_t q = ib + tid; q < ie; q += blockDim.x) {
+    if (my_p >= 0) {
+      const bool fresh = my_p == pv;  // placed in the previous step: loaded before its commit
+      const int64_t f = fresh ? pf : my_f0;
+      const int32_t dd = fresh ? prev : my_dd0;
+      atomicMax(&sA[dd], static_cast<long long>(f));
+      atomicMax(&sB[dd], static_cast<long long>(f + my_c));
+    }
+    for (int32_t q = ib + T + tid; q < ie; q += T) {
       const int32_t p = a.in_src[q];
       const int64_t f = a.finish[p];
       const int32_t dd = dev[p];
@@ -488,6 +553,8 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
         dev[v] = chosen;
         savail[chosen] -= mv;
         spdm[chosen] += mv;
+        s_prev_finish = start + w;
+        s_prev_v = v;
       }
     }
     prev = chosen;
