@@ -71,6 +71,9 @@ struct dp_ctx {
   // block freed on one context's stream could be handed to another context's stream
   // with an inserted cross-stream dependency, coupling independent replicas.
   cudaMemPool_t pool = nullptr;
+  // Host->device copies of batched calls run here (created on first use), so the first
+  // graphs' validation overlaps the later graphs' uploads.
+  cudaStream_t copy_stream = nullptr;
 };
 
 namespace dpb {

@@ -191,6 +191,10 @@ void dp_ctx_destroy(dp_ctx_t* ctx) {
   ctx->pending.clear();
   if (ctx->pin) cudaFreeHost(ctx->pin);
   if (ctx->sync_ev) cudaEventDestroy(ctx->sync_ev);
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+  }
   if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
   for (auto& s : ctx->stages) ctx->event_pool.push_back(s);
   for (auto& s : ctx->event_pool) {

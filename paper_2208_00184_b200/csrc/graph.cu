@@ -701,7 +701,7 @@ int coop_grid(const void* kernel, int block, int64_t work, int num_sms) {
 }  // namespace
 
 // ------------------------------------------------------------------ host orchestration
-void graph_upload(DevGraph& g, dp_ctx* ctx, const dp_graph_t* h) {
+void graph_upload(DevGraph& g, dp_ctx* ctx, const dp_graph_t* h, cudaStream_t copy, cudaEvent_t done) {
   if (h->n_nodes < 0 || h->n_edges < 0 || h->n_nodes > INT32_MAX - 2 || h->n_edges > INT32_MAX - 2)
     fail(DP_E_ARGUMENT, "graph sizes out of range (n=%lld, m=%lld)", (long long)h->n_nodes,
          (long long)h->n_edges);
@@ -711,25 +711,33 @@ void graph_upload(DevGraph& g, dp_ctx* ctx, const dp_graph_t* h) {
   g.id.alloc(ctx, g.n);
   g.w.alloc(ctx, g.n);
   g.mem.alloc(ctx, g.n);
-  g.id.upload(h->node_id, g.n);
-  g.w.upload(h->compute_us, g.n);
-  g.mem.upload(h->memory_bytes, g.n);
   g.has_group = false;
   if (h->group) {
     for (int64_t i = 0; i < h->n_nodes; ++i) {
       if (h->group[i] >= 0) { g.has_group = true; break; }
     }
   }
-  if (g.has_group) {
-    g.group.alloc(ctx, g.n);
-    g.group.upload(h->group, g.n);
-  }
+  if (g.has_group) g.group.alloc(ctx, g.n);
   g.src_id.alloc(ctx, g.m);
   g.dst_id.alloc(ctx, g.m);
   g.bytes.alloc(ctx, g.m);
-  g.src_id.upload(h->edge_src, g.m);
-  g.dst_id.upload(h->edge_dst, g.m);
-  g.bytes.upload(h->edge_bytes, g.m);
+  cudaStream_t s = ctx->stream;
+  if (copy) {  // the buffers were allocated on ctx->stream: the copy stream waits for that
+    DP_CUDA(cudaEventRecord(done, ctx->stream));
+    DP_CUDA(cudaStreamWaitEvent(copy, done, 0));
+    s = copy;
+  }
+  auto up = [&](void* d, const void* hsrc, size_t bytes) {
+    if (bytes) DP_CUDA(cudaMemcpyAsync(d, hsrc, bytes, cudaMemcpyHostToDevice, s));
+  };
+  up(g.id.p, h->node_id, sizeof(*h->node_id) * g.n);
+  up(g.w.p, h->compute_us, sizeof(*h->compute_us) * g.n);
+  up(g.mem.p, h->memory_bytes, sizeof(*h->memory_bytes) * g.n);
+  if (g.has_group) up(g.group.p, h->group, sizeof(*h->group) * g.n);
+  up(g.src_id.p, h->edge_src, sizeof(*h->edge_src) * g.m);
+  up(g.dst_id.p, h->edge_dst, sizeof(*h->edge_dst) * g.m);
+  up(g.bytes.p, h->edge_bytes, sizeof(*h->edge_bytes) * g.m);
+  if (copy) DP_CUDA(cudaEventRecord(done, copy));
 }
 
 void graph_adopt_dense(DevGraph& g, dp_ctx* ctx, int32_t n, int32_t m, DevBuf<int64_t>&& w,

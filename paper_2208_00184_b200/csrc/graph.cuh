@@ -46,7 +46,10 @@ struct Validation {
 };
 
 // Host SoA -> HBM (async on ctx->stream).
-void graph_upload(DevGraph& g, dp_ctx* ctx, const dp_graph_t* h);
+// Uploads on ctx->stream, or (copy != null) on `copy` with `done` recorded after the
+// copies: the caller makes ctx->stream wait on `done` before using the graph.
+void graph_upload(DevGraph& g, dp_ctx* ctx, const dp_graph_t* h, cudaStream_t copy = nullptr,
+                  cudaEvent_t done = nullptr);
 // Adopt device arrays of a graph with dense ids 0..n-1 (coarse graph).
 void graph_adopt_dense(DevGraph& g, dp_ctx* ctx, int32_t n, int32_t m, DevBuf<int64_t>&& w,
                        DevBuf<int64_t>&& mem, DevBuf<int32_t>&& esrc, DevBuf<int32_t>&& edst,

@@ -154,7 +154,7 @@ void resident_generate(Resident* const* rs, int count, bool with_ccr) {
 }
 
 void resident_init(Resident& r, dp_ctx* ctx, const dp_graph_t* h, const dp_devices_t* devices, dp_comm_t comm,
-                   const dp_pipeline_config_t* cfg) {
+                   const dp_pipeline_config_t* cfg, cudaStream_t copy = nullptr, cudaEvent_t done = nullptr) {
   if (devices->count <= 0) fail(DP_E_INVALID_VALUE, "device list is empty");
   r.ctx = ctx;
   r.host = h;
@@ -165,7 +165,7 @@ void resident_init(Resident& r, dp_ctx* ctx, const dp_graph_t* h, const dp_devic
   int64_t min_cap = devices->memory_bytes[0];
   for (int32_t i = 0; i < devices->count; ++i) min_cap = std::min(min_cap, devices->memory_bytes[i]);
   r.limit = std::max<int64_t>(1, static_cast<int64_t>(static_cast<double>(min_cap) * r.cfg.cluster_mem_fraction));
-  graph_upload(r.g, ctx, h);
+  graph_upload(r.g, ctx, h, copy, done);
 }
 
 // Expanded placement with every device listed (present where it received nodes).
@@ -232,10 +232,30 @@ int dp_pipeline_batch(dp_ctx_t* ctx, int32_t count, const dp_graph_t* const* gra
   const auto h0 = now();
   std::vector<std::unique_ptr<Resident>> rs;
   std::vector<Resident*> rp;
+  // several graphs: uploads on the context's copy stream, graph i's validation waits only
+  // for its own copies (the later graphs' uploads overlap it)
+  std::vector<cudaEvent_t> up;
+  struct UpGuard {  // before the graphs are freed (stream-ordered on ctx->stream): order the
+    dp_ctx* c;       // frees after every copy, also when a graph fails before its wait
+    std::vector<cudaEvent_t>& v;
+    ~UpGuard() {
+      for (auto e : v) {
+        cudaStreamWaitEvent(c->stream, e, 0);
+        cudaEventDestroy(e);
+      }
+    }
+  } up_guard{ctx, up};
+  if (count > 1 && !ctx->copy_stream)
+    DP_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
   for (int32_t i = 0; i < count; ++i) {
     rs.emplace_back(new Resident);
     rp.push_back(rs.back().get());
-    resident_init(*rs.back(), ctx, graphs[i], devices, comm, cfg);
+    cudaEvent_t e = nullptr;
+    if (count > 1) {
+      DP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      up.push_back(e);
+    }
+    resident_init(*rs.back(), ctx, graphs[i], devices, comm, cfg, count > 1 ? ctx->copy_stream : nullptr, e);
   }
   if (dbg) sync(ctx);
   const auto h1 = now();
@@ -250,7 +270,9 @@ int dp_pipeline_batch(dp_ctx_t* ctx, int32_t count, const dp_graph_t* const* gra
     }
   } guard{e0, e1};
   // require_valid + ccr precede the window (pipeline.cpp:33, :58)
-  for (Resident* r : rp) {
+  for (int32_t i = 0; i < count; ++i) {
+    Resident* r = rp[i];
+    if (!up.empty()) DP_CUDA(cudaStreamWaitEvent(ctx->stream, up[i], 0));
     resident_validate(*r, true);
     graph_costs(r->g, comm);
     r->original_ccr = ccr_dev(r->g);
