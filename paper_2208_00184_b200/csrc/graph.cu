@@ -375,9 +375,30 @@ __device__ __forceinline__ int64_t warp_max_nonneg(int64_t x) {
 // Values of the last kSeqMaxN sweep positions live in a shared-memory ring; older ones
 // (graphs larger than the ring) are read from `gval` in HBM/L2 with ld.global.cg (the
 // sweep writes them there too), so any n works and chain-like graphs hit the ring.
-__global__ void __launch_bounds__(1024) k_levels_seq(int32_t n, const int32_t* off, const int32_t* nbr,
-                                                     const int64_t* cost, const int64_t* w, int64_t* out,
-                                                     bool rev, int64_t* gval) {
+// One CTA per graph (independent graphs of a batched call share the launch).
+struct SeqArgs {
+  int32_t n;
+  const int32_t* off;
+  const int32_t* nbr;
+  const int64_t* cost;
+  const int64_t* w;
+  int64_t* out;
+  int64_t* gval;
+};
+constexpr int kSeqBatch = 8;
+struct SeqBatch {
+  SeqArgs a[kSeqBatch];
+};
+
+__global__ void __launch_bounds__(1024) k_levels_seq(const __grid_constant__ SeqBatch batch, bool rev) {
+  const SeqArgs& A = batch.a[blockIdx.x];
+  const int32_t n = A.n;
+  const int32_t* off = A.off;
+  const int32_t* nbr = A.nbr;
+  const int64_t* cost = A.cost;
+  const int64_t* w = A.w;
+  int64_t* out = A.out;
+  int64_t* gval = A.gval;
   extern __shared__ int64_t sm64[];
   int64_t* val = sm64;                                         // ring [kSeqMaxN]: f (fwd) or blevel (bwd)
   int64_t* ec = val + kSeqMaxN;                                // [kSeqTile]
@@ -847,6 +868,50 @@ void graph_costs(DevGraph& g, dp_comm_t comm) {
   g.cb = comm.b_us;
 }
 
+// The one-CTA index-order sweep of several graphs (index order topological, checked by the
+// caller), one launch per direction.
+void levels_sweep_launch(DevGraph* const* gs, int64_t* const* tlevel, int64_t* const* blevel, int count) {
+  dp_ctx* ctx = gs[0]->ctx;
+  const size_t sm = sizeof(int64_t) * (kSeqMaxN + kSeqTile + kSeqTileN) + sizeof(int32_t) * (kSeqTile + kSeqTileN + 1);
+  static bool attr = false;
+  if (!attr) {
+    DP_CUDA(cudaFuncSetAttribute(k_levels_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    attr = true;
+  }
+  std::vector<DevBuf<int64_t>> gval(count);
+  for (int b0 = 0; b0 < count; b0 += kSeqBatch) {
+    const int k = std::min(kSeqBatch, count - b0);
+    SeqBatch fwd{}, bwd{};
+    for (int q = 0; q < k; ++q) {
+      DevGraph& g = *gs[b0 + q];
+      if (g.n > kSeqMaxN) gval[b0 + q].alloc(ctx, g.n);
+      fwd.a[q] = SeqArgs{g.n, g.in_off.p, g.in_src.p, g.in_cost.p, g.w.p, tlevel[b0 + q], gval[b0 + q].p};
+      bwd.a[q] = SeqArgs{g.n, g.out_off.p, g.out_dst.p, g.out_cost.p, g.w.p, blevel[b0 + q], gval[b0 + q].p};
+    }
+    DP_LAUNCH(ctx, k_levels_seq, k, 1024, sm, fwd, false);
+    DP_LAUNCH(ctx, k_levels_seq, k, 1024, sm, bwd, true);
+  }
+}
+
+// Index-order check of several graphs with one host sync; ok[i] = index order topological.
+std::vector<char> graphs_index_topological(DevGraph* const* gs, int count) {
+  dp_ctx* ctx = gs[0]->ctx;
+  DevBuf<unsigned long long> chk(ctx, 2 * (size_t)count);
+  std::vector<unsigned long long> init(2 * (size_t)count, 0ull);
+  for (int i = 0; i < count; ++i) init[2 * i] = 1ull;
+  chk.upload(init.data(), init.size());
+  for (int i = 0; i < count; ++i) {
+    DevGraph& g = *gs[i];
+    if (g.n > 0)
+      DP_LAUNCH(ctx, k_index_topo, grid_for(g.n, 256), 256, 0, g.in_off.p, g.in_src.p, g.n,
+                reinterpret_cast<int*>(chk.p + 2 * i), chk.p + 2 * i + 1);
+  }
+  std::vector<unsigned long long> h = to_host(ctx, chk.p, 2 * (size_t)count);
+  std::vector<char> ok(count);
+  for (int i = 0; i < count; ++i) ok[i] = gs[i]->n > 0 && static_cast<int>(h[2 * i]) == 1;
+  return ok;
+}
+
 // Levels when the node index order is topological (every edge u->v has u < v): the
 // one-CTA sweep for small or chain-like graphs (the coarse graph of fuse), the dataflow
 // kernel otherwise.  Returns false when the index order is not topological (caller uses
@@ -866,17 +931,10 @@ bool graph_levels_indexorder(DevGraph& g, int64_t* tlevel, int64_t* blevel, bool
   if (static_cast<int>(h[0]) != 1) return false;
   const bool sweep = (n <= kSeqMaxN || chainlike) && getenv("DP_LEVELS_FLOW") == nullptr;
   if (sweep) {
-    const size_t sm =
-        sizeof(int64_t) * (kSeqMaxN + kSeqTile + kSeqTileN) + sizeof(int32_t) * (kSeqTile + kSeqTileN + 1);
-    static bool attr = false;
-    if (!attr) {
-      DP_CUDA(cudaFuncSetAttribute(k_levels_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-      attr = true;
-    }
-    DevBuf<int64_t> gval;
-    if (n > kSeqMaxN) gval.alloc(ctx, n);
-    DP_LAUNCH(ctx, k_levels_seq, 1, 1024, sm, n, g.in_off.p, g.in_src.p, g.in_cost.p, g.w.p, tlevel, false, gval.p);
-    DP_LAUNCH(ctx, k_levels_seq, 1, 1024, sm, n, g.out_off.p, g.out_dst.p, g.out_cost.p, g.w.p, blevel, true, gval.p);
+    DevGraph* gs[1] = {&g};
+    int64_t* t1[1] = {tlevel};
+    int64_t* b1[1] = {blevel};
+    levels_sweep_launch(gs, t1, b1, 1);
     g.processed = n;
     return true;
   }

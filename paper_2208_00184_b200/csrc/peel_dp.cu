@@ -18,6 +18,8 @@
 // sequential part of fuse() costs max(peel, DP) instead of their sum.
 #include <algorithm>
 #include <cstdlib>
+#include <memory>
+#include <vector>
 
 #include "fusion.cuh"
 #include "graph.cuh"
@@ -652,9 +654,15 @@ __device__ __forceinline__ void peel_dispatch(const PeelArgs& a, int4* smem4) {
   else peel_warp_v5<32>(a, reinterpret_cast<int2*>(smem4), sfreed, srow, stop, seqbuf);
 }
 
-__global__ void __launch_bounds__(32) k_peel2(PeelArgs a) {
+// One CTA (one warp) per graph: independent graphs of a batched call share the launch.
+constexpr int kPeelBatch = 8;
+struct PeelBatch {
+  PeelArgs a[kPeelBatch];
+};
+
+__global__ void __launch_bounds__(32) k_peel2(const __grid_constant__ PeelBatch b) {
   extern __shared__ int4 smem4[];
-  peel_dispatch<kV6BucketBits>(a, smem4);
+  peel_dispatch<kV6BucketBits>(b.a[blockIdx.x], smem4);
 }
 
 // ---------------------------------------------------------------- streaming DP
@@ -1664,26 +1672,53 @@ static PeelArgs peel_args(DevGraph& g, PeelState& st, int32_t* seq, int32_t* pos
   return a;
 }
 
-int32_t topo_order(DevGraph& g, int policy, const int64_t* cpath, int32_t* seq, int32_t* pos_of) {
-  dp_ctx* ctx = g.ctx;
-  if (g.n == 0) return 0;
+std::vector<int32_t> topo_order_batch(DevGraph* const* gs, int count, int policy, const int64_t* const* cpath,
+                                      int32_t* const* seq, int32_t* const* pos_of) {
+  std::vector<int32_t> emitted(count, 0);
+  if (count == 0) return emitted;
+  dp_ctx* ctx = gs[0]->ctx;
   const size_t sm = peel_smem();
   static bool attr = false;
   if (!attr) {
     DP_CUDA(cudaFuncSetAttribute(k_peel2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
     attr = true;
   }
-  PeelState st;
-  peel_prepare(g, policy, cpath, st);
-  PeelArgs a = peel_args(g, st, seq, pos_of, false);
-  {
-    StageScope s(ctx, policy == DP_TOPO_CPD ? "cpd_peel" : "peel", 72.0 * g.n + 8.0 * g.m_ok);
-    DP_LAUNCH(ctx, k_peel2, 1, 32, sm, a);
+  std::vector<std::unique_ptr<PeelState>> st(count);
+  std::vector<int> live;
+  double bytes = 0.0;
+  for (int i = 0; i < count; ++i) {
+    if (gs[i]->n == 0) continue;
+    st[i].reset(new PeelState);
+    peel_prepare(*gs[i], policy, cpath[i], *st[i]);
+    live.push_back(i);
+    bytes += 72.0 * gs[i]->n + 8.0 * gs[i]->m_ok;
   }
-  const int32_t emitted = scalar_to_host(ctx, st.counters.p + 1);
-  if (st.stack_mode && emitted == g.n)
-    DP_LAUNCH(ctx, k_scatter_pos_of, grid_for(g.n, 256), 256, 0, seq, g.n, pos_of);
+  {
+    StageScope s(ctx, policy == DP_TOPO_CPD ? "cpd_peel" : "peel", bytes);
+    for (size_t b0 = 0; b0 < live.size(); b0 += kPeelBatch) {
+      const int k = static_cast<int>(std::min<size_t>(kPeelBatch, live.size() - b0));
+      PeelBatch batch{};
+      for (int q = 0; q < k; ++q) {
+        const int i = live[b0 + q];
+        batch.a[q] = peel_args(*gs[i], *st[i], seq[i], pos_of[i], false);
+      }
+      DP_LAUNCH(ctx, k_peel2, k, 32, sm, batch);
+    }
+  }
+  for (int i : live) download_bytes(ctx, &emitted[i], st[i]->counters.p + 1, sizeof(int32_t));
+  sync(ctx);
+  for (int i : live)
+    if (st[i]->stack_mode && emitted[i] == gs[i]->n)
+      DP_LAUNCH(ctx, k_scatter_pos_of, grid_for(gs[i]->n, 256), 256, 0, seq[i], gs[i]->n, pos_of[i]);
   return emitted;
+}
+
+int32_t topo_order(DevGraph& g, int policy, const int64_t* cpath, int32_t* seq, int32_t* pos_of) {
+  DevGraph* gs[1] = {&g};
+  const int64_t* cp[1] = {cpath};
+  int32_t* sq[1] = {seq};
+  int32_t* po[1] = {pos_of};
+  return topo_order_batch(gs, 1, policy, cp, sq, po)[0];
 }
 
 struct PeelDpJob {

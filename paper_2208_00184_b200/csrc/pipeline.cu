@@ -87,21 +87,7 @@ void resident_validate(Resident& r, bool cycle_check) {
   if (v.code) fail(v.code, "%s", v.message.c_str());
 }
 
-// The generation window (pipeline.cpp:67-79) after the streamed peel + DP: traceback and
-// coarse graph, coarse levels + cpd_topo, then the placement job (launched by the caller,
-// batched over graphs), then 2x expand.
-PlaceJob* generate_mid(Resident& r, FuseStage& fs) {
-  dp_ctx* ctx = r.ctx;
-  fuse_end(r.g, r.f, fs);
-  DevGraph& coarse = r.f.coarse;
-  levels_dev(coarse, r.comm, r.ct, r.cb, r.cc, true);  // clusters are runs of a topological order
-  const int32_t k = coarse.n;
-  r.cseq.alloc(ctx, k > 0 ? k : 1);
-  r.cpos.alloc(ctx, k > 0 ? k : 1);
-  topo_order(coarse, DP_TOPO_CPD, r.cc.p, r.cseq.p, r.cpos.p);
-  return place_prepare(coarse, r.cseq.p, r.devs, &r.po, &r.pa, r.decisions);
-}
-
+// The end of the generation window (pipeline.cpp:67-79): 2x expand.
 void generate_tail(Resident& r) {
   dp_ctx* ctx = r.ctx;
   DevGraph& g = r.g;
@@ -117,7 +103,8 @@ void generate_tail(Resident& r) {
 
 // Generation windows of independent graphs on one stream (graphs already validated, with
 // costs): each graph's fuse_begin, ONE launch of all the streamed peel + DP cores, each
-// graph's traceback / coarse levels / cpd_topo, ONE launch of all the placements, expand.
+// graph's traceback and coarse graph, ONE launch (per direction) of all the coarse-level
+// sweeps, ONE launch of all the coarse CPD peels, ONE launch of all the placements, expand.
 void generate_windows(Resident* const* rs, int count) {
   dp_ctx* ctx = rs[0]->ctx;
   std::vector<std::unique_ptr<FuseStage>> fs;
@@ -129,10 +116,34 @@ void generate_windows(Resident* const* rs, int count) {
     if (fs.back()->streamed) jobs.push_back(fs.back()->job.j);
   }
   if (!jobs.empty()) peel_dp_launch(ctx, jobs.data(), static_cast<int>(jobs.size()));
+  for (int i = 0; i < count; ++i) fuse_end(rs[i]->g, rs[i]->f, *fs[i]);
+  // coarse levels + cpd_topo of all graphs: one sweep launch per direction, one peel launch
+  std::vector<DevGraph*> cg(count);
+  std::vector<DevBuf<int64_t>*> ct(count), cb(count), cc(count);
+  for (int i = 0; i < count; ++i) {
+    cg[i] = &rs[i]->f.coarse;
+    ct[i] = &rs[i]->ct;
+    cb[i] = &rs[i]->cb;
+    cc[i] = &rs[i]->cc;
+  }
+  levels_dev_chainlike_batch(cg.data(), count, rs[0]->comm, ct.data(), cb.data(), cc.data());
+  std::vector<const int64_t*> cpath(count);
+  std::vector<int32_t*> cseq(count), cpos(count);
+  for (int i = 0; i < count; ++i) {
+    Resident& r = *rs[i];
+    const int32_t k = r.f.coarse.n;
+    r.cseq.alloc(ctx, k > 0 ? k : 1);
+    r.cpos.alloc(ctx, k > 0 ? k : 1);
+    cpath[i] = r.cc.p;
+    cseq[i] = r.cseq.p;
+    cpos[i] = r.cpos.p;
+  }
+  topo_order_batch(cg.data(), count, DP_TOPO_CPD, cpath.data(), cseq.data(), cpos.data());
   std::vector<std::unique_ptr<PlaceHandle>> ph;
   std::vector<PlaceJob*> pj;
   for (int i = 0; i < count; ++i) {
-    ph.emplace_back(new PlaceHandle(generate_mid(*rs[i], *fs[i])));
+    Resident& r = *rs[i];
+    ph.emplace_back(new PlaceHandle(place_prepare(r.f.coarse, r.cseq.p, r.devs, &r.po, &r.pa, r.decisions)));
     pj.push_back(ph.back()->j);
   }
   place_launch(ctx, pj.data(), count);
