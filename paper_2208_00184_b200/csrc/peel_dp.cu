@@ -1408,9 +1408,14 @@ __global__ void __launch_bounds__(kDpPairWarps * 32, 1) k_peel_dp(const __grid_c
   }
 }
 
-__global__ void __launch_bounds__(kPeelDpWarps * 32, 1) k_peel_dp_shared(const __grid_constant__ PeelDpBatch b) {
+// Launched with kPeelDpWarps * 32 threads, or with kPeelDpExclusive threads whose extra
+// warps exit at once: their registers keep other kernels' CTAs off the SM, so the peel warp
+// does not share its issue slots and L1 (DP_PEEL_EXCLUSIVE=1).
+constexpr int kPeelDpExclusive = 512;
+__global__ void __launch_bounds__(kPeelDpExclusive, 1) k_peel_dp_shared(const __grid_constant__ PeelDpBatch b) {
   extern __shared__ int4 smem4[];
   const int warp = threadIdx.x >> 5;
+  if (warp >= kPeelDpWarps) return;
   const PeelArgs& pa = b.pa[blockIdx.x];
   const DpArgs& da = b.da[blockIdx.x];
   int4* dsm = smem4 + kPeelRegionShared / sizeof(int4);
@@ -1419,7 +1424,7 @@ __global__ void __launch_bounds__(kPeelDpWarps * 32, 1) k_peel_dp_shared(const _
     if (threadIdx.x < kDpProducers) S.ready[threadIdx.x] = -1;
     if (threadIdx.x == 0) S.consumed = 0;
   }
-  __syncthreads();
+  asm volatile("bar.sync 1, %0;" ::"r"(kPeelDpWarps * 32) : "memory");  // the working warps only
   if (warp == 0) {
     peel_dispatch<kV6BucketBitsShared>(pa, smem4);
   } else if (warp == 1) {
@@ -1806,7 +1811,8 @@ void peel_dp_launch(dp_ctx* ctx, PeelDpJob* const* jobs, int count) {
                                           kSmemPair, ctx->stream));
       ++ctx->launches;
     } else {
-      DP_LAUNCH(ctx, k_peel_dp_shared, k, kPeelDpWarps * 32, kSmemShared, batch);
+      DP_LAUNCH(ctx, k_peel_dp_shared, k, getenv("DP_PEEL_EXCLUSIVE") ? kPeelDpExclusive : kPeelDpWarps * 32,
+                kSmemShared, batch);
     }
   }
   for (int q = 0; q < count; ++q) {
