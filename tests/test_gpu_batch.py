@@ -46,3 +46,41 @@ def test_pipeline_batch_error_and_empty(gpu, ref):
     assert gpu.evaluate_pipeline_batch([], devs, GEN) == []
     # the context stays usable after a failed batch
     same_pipeline(gpu.evaluate_pipeline_batch([good], devs, GEN)[0], ref.evaluate_pipeline(good, devs, GEN))
+
+
+def test_resident_generate_batch_matches_single(gpu):
+    """dp_resident_generate_batch (the throughput path of bench.py) against one
+    dp_resident_generate per graph: identical expanded placements and coarse sizes."""
+    import ctypes as C
+    from paper_2208_00184_b200._abi import PipelineCfgC, comm_c, devices_c
+    lib = gpu.lib
+    gs = [layered(70 + s, 5000 + 1000 * s, 50 + 20 * s) for s in range(5)]
+    devs = devices(8, max(capacity_for(g, 8, 1.25) for g in gs))
+    cfg = PipelineCfgC(200, 0.25, 1, 0)
+    dc = devices_c(devs)
+
+    def create(g):
+        h = C.c_void_p()
+        gc = g.c()
+        assert lib.dp_resident_create(gpu.ctx, C.byref(gc), C.byref(dc), comm_c(GEN), C.byref(cfg), C.byref(h)) == 0
+        return h.value
+
+    def fetch(h, g):
+        a, b = np.zeros(g.n, np.int32), np.zeros(g.n, np.int32)
+        cn, ce = C.c_int64(), C.c_int64()
+        assert lib.dp_resident_fetch(C.c_void_p(h), a.ctypes.data_as(C.POINTER(C.c_int32)),
+                                     b.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(cn), C.byref(ce)) == 0
+        return a, b, cn.value, ce.value
+
+    single, batch = [create(g) for g in gs], [create(g) for g in gs]
+    try:
+        for h in single:
+            assert lib.dp_resident_generate(C.c_void_p(h)) == 0
+        arr = (C.c_void_p * len(batch))(*batch)
+        assert lib.dp_resident_generate_batch(arr, len(batch)) == 0
+        for g, h1, h2 in zip(gs, single, batch):
+            x, y = fetch(h1, g), fetch(h2, g)
+            assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1]) and x[2:] == y[2:]
+    finally:
+        for h in single + batch:
+            lib.dp_resident_destroy(C.c_void_p(h))
