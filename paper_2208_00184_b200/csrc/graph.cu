@@ -938,9 +938,11 @@ bool graph_levels_indexorder(DevGraph& g, int64_t* tlevel, int64_t* blevel, bool
     g.processed = n;
     return true;
   }
-  // lookahead: four mean edge spans, in 32-node chunks, at least 256 chunks
+  // lookahead: two mean edge spans, in 32-node chunks, at least 64 chunks (a deep graph's
+  // wavefront needs few; more polling warps only cost when many graphs run at once:
+  // 64 vs 256 chunks = 2.47 vs 2.33 ms alone, 707 vs 730 ms per 128-graph step)
   const double mean_span = g.m_ok > 0 ? static_cast<double>(h[1]) / g.m_ok : 32.0;
-  int32_t ahead = static_cast<int32_t>(std::min(1.0e6, std::max(256.0, 4.0 * mean_span / 32.0)));
+  int32_t ahead = static_cast<int32_t>(std::min(1.0e6, std::max(64.0, 2.0 * mean_span / 32.0)));
   if (const char* s = getenv("DP_FLOW_AHEAD")) ahead = atoi(s);
   unsigned sleep_cap = 256;
   if (const char* s = getenv("DP_FLOW_SLEEP")) sleep_cap = static_cast<unsigned>(atoi(s));
