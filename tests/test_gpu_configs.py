@@ -50,3 +50,18 @@ def test_full_size_properties(gpu, name):
     limit = max(1, int(min(c for _, c in devs) * 0.25))
     assert int(m.total_memory.max()) <= limit
     assert gpu.is_valid_topo_order(rep.coarse, rep.coarse_sequence)
+
+
+def test_config4_batched_matches_reference(gpu):
+    """The throughput path at full size: config #4 deep twice in one dp_pipeline_batch call
+    (shared-SM peel + DP kernel, batched coarse phase and placement) against the
+    reference's golden digests."""
+    g, devs, comm = build_config("4d")
+    gold = GOLD["4d"]
+    for rep in gpu.evaluate_pipeline_batch([g, g], devs, comm, simulate=True):
+        got = pipeline_digests(rep)
+        for k, v in got.items():
+            if isinstance(v, float):
+                assert v == pytest.approx(gold[k], rel=0, abs=0), k
+            else:
+                assert v == gold[k], f"4d batched.{k}: {v} vs {gold[k]}"
