@@ -84,3 +84,13 @@ def test_resident_generate_batch_matches_single(gpu):
     finally:
         for h in single + batch:
             lib.dp_resident_destroy(C.c_void_p(h))
+
+
+def test_pipeline_batch_chunks_beyond_launch_width(gpu, ref):
+    """12 graphs in one call: the per-launch argument batches (8 graphs for the peel + DP,
+    coarse sweep, coarse peel and placement launches) are split across two launches."""
+    gs = [layered(80 + s, 800 + 150 * s, 16 + 4 * (s % 5)) for s in range(12)]
+    devs = devices(4, max(capacity_for(g, 4, 1.25) for g in gs))
+    got = gpu.evaluate_pipeline_batch(gs, devs, GEN)
+    for i, (g, r) in enumerate(zip(gs, got)):
+        same_pipeline(r, ref.evaluate_pipeline(g, devs, GEN), f"batch12[{i}]")
