@@ -51,7 +51,7 @@ struct PeelArgs {
   const int4* slot;     // per CSR slot: child, rank(child), row_start(child), deg(child)
   int32_t* indeg;       // working in-degrees
   int4* gstack;         // global stack backing store (n entries), initial sources at [0, nsrc)
-  int32_t nsrc;
+  const int32_t* nsrc;  // number of sources (device: no host round trip before the launch)
   bool stack_mode;      // false: FIFO (M-TOPO)
   int32_t* seq;         // node index by position
   int32_t* pos_of;
@@ -81,11 +81,12 @@ __device__ void peel_warp(const PeelArgs& a, int4* sstack, int64_t* sfreed) {
   const int lane = threadIdx.x & 31;
   const int32_t SC = kStackCache;
   // ---------------- stack (stack mode): logical entries [0, top]; [base, top] cached
-  int32_t top = a.nsrc - 1, base = 0;
+  const int32_t nsrc = *a.nsrc;
+  int32_t top = nsrc - 1, base = 0;
   // ---------------- queue (FIFO mode): entries [head, tail) in gstack
-  int32_t head = 0, tail = a.nsrc;
+  int32_t head = 0, tail = nsrc;
   if (a.stack_mode) {
-    base = max(0, a.nsrc - SC / 2);
+    base = max(0, nsrc - SC / 2);
     for (int32_t i = base + lane; i <= top; i += 32) sstack[i & (SC - 1)] = a.gstack[i];
   }
   __syncwarp();
@@ -227,8 +228,9 @@ __device__ void peel_warp_v5(const PeelArgs& a, int2* sstack, int64_t* sfreed, i
                              int32_t* seqbuf) {
   const int lane = threadIdx.x & 31;
   const int32_t SC = 2 * kStackCache;
-  int32_t top = a.nsrc - 1;
-  int32_t base = max(0, a.nsrc - SC / 2);
+  const int32_t nsrc = *a.nsrc;
+  int32_t top = nsrc - 1;
+  int32_t base = max(0, nsrc - SC / 2);
   for (int32_t i = base + lane; i <= top; i += 32) sstack[i & (SC - 1)] = a.gstack2[i];
   __syncwarp();
   int32_t p = 0;
@@ -481,8 +483,9 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem<BB>& S) {
   constexpr int32_t SC = kV6Stack;
   for (int i = lane; i < (2 << BB); i += 32) S.ht[i] = kV6Empty;
   for (int i = lane; i < (1 << (BB - 1)); i += 32) S.ovc[i] = 0;
-  int32_t top = a.nsrc - 1;
-  int32_t base = max(0, a.nsrc - SC / 2);
+  const int32_t nsrc = *a.nsrc;
+  int32_t top = nsrc - 1;
+  int32_t base = max(0, nsrc - SC / 2);
   v6_fill(a, S, base, top, lane);
   __syncwarp();
   int32_t p = 0, held = 0;
@@ -1463,7 +1466,8 @@ __global__ void k_src_flags2(const int32_t* by_rank, const int32_t* in_off, int3
 }
 
 __global__ void k_src_place2(const int32_t* by_rank, const int32_t* flag, const int32_t* pos, const int32_t* out_off,
-                             int32_t n, int32_t nsrc, bool stack, int4* buf) {
+                             int32_t n, const int32_t* nsrc_p, bool stack, int4* buf) {
+  const int32_t nsrc = *nsrc_p;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
     if (!flag[r]) continue;
     const int32_t v = by_rank[r], p = pos[r];
@@ -1488,7 +1492,8 @@ __global__ void k_ell(const int32_t* out_off, const int32_t* out_dst, int32_t n,
 }
 
 __global__ void k_src_place_v5(const int32_t* by_rank, const int32_t* flag, const int32_t* pos, const int32_t* out_off,
-                               int32_t n, int32_t nsrc, int2* buf) {
+                               int32_t n, const int32_t* nsrc_p, int2* buf) {
+  const int32_t nsrc = *nsrc_p;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
     if (!flag[r]) continue;
     const int32_t v = by_rank[r], p = pos[r];
@@ -1542,7 +1547,8 @@ __global__ void k_cmeta(const int32_t* in_off, const int32_t* out_off, const int
 }
 
 __global__ void k_src_place_v6(const int32_t* by_rank, const int32_t* flag, const int32_t* pos, const int32_t* out_off,
-                               int32_t n, int32_t nsrc, int32_t* buf) {
+                               int32_t n, const int32_t* nsrc_p, int32_t* buf) {
+  const int32_t nsrc = *nsrc_p;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
     if (!flag[r]) continue;
     const int32_t v = by_rank[r];
@@ -1602,7 +1608,7 @@ void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st, 
   flag.zero();
   DP_LAUNCH(ctx, k_src_flags2, grid_for(n, B), B, 0, by_rank.p, g.in_off.p, n, flag.p);
   exclusive_scan_i32(ctx, flag.p, fpos.p, (int64_t)n + 1);
-  st.nsrc = scalar_to_host(ctx, fpos.p + n);
+  const int32_t* nsrc_p = fpos.p + n;  // the scan's total: read on the device
   st.stack_mode = policy != DP_TOPO_M;
   st.v6 = st.stack_mode && n < (1 << 24) && static_cast<int64_t>(m) <= 6 * static_cast<int64_t>(n) && !force_v5 &&
           getenv("DP_PEEL_V5") == nullptr;
@@ -1613,7 +1619,7 @@ void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st, 
     st.cmeta.alloc(ctx, m > 0 ? m : 1);
     DP_LAUNCH(ctx, k_cmeta, grid_for(m, B), B, 0, g.in_off.p, g.out_off.p, g.out_dst.p, rank.p, m, st.cmeta.p);
     st.gsid.alloc(ctx, (size_t)n + 1);
-    DP_LAUNCH(ctx, k_src_place_v6, grid_for(n, B), B, 0, by_rank.p, flag.p, fpos.p, g.out_off.p, n, st.nsrc,
+    DP_LAUNCH(ctx, k_src_place_v6, grid_for(n, B), B, 0, by_rank.p, flag.p, fpos.p, g.out_off.p, n, nsrc_p,
               st.gsid.p);
     st.indeg.alloc(ctx, n);
     DP_LAUNCH(ctx, k_indeg_init2, grid_for(n, B), B, 0, g.in_off.p, n, st.indeg.p);
@@ -1622,6 +1628,7 @@ void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st, 
     st.spill.alloc(ctx, m > 0 ? m : 1);
     st.counters.alloc(ctx, 3);
     st.counters.zero();
+    DP_CUDA(cudaMemcpyAsync(st.counters.p + 2, nsrc_p, sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
     return;
   }
   st.gstack.alloc(ctx, (size_t)n + 1);
@@ -1632,11 +1639,11 @@ void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st, 
     st.ell.alloc(ctx, (size_t)n * st.ellw);
     DP_LAUNCH(ctx, k_ell, grid_for((int64_t)n * st.ellw, B), B, 0, g.out_off.p, g.out_dst.p, n, st.ellw, st.ell.p);
     st.gstack2.alloc(ctx, (size_t)n + 1);
-    DP_LAUNCH(ctx, k_src_place_v5, grid_for(n, B), B, 0, by_rank.p, flag.p, fpos.p, g.out_off.p, n, st.nsrc,
+    DP_LAUNCH(ctx, k_src_place_v5, grid_for(n, B), B, 0, by_rank.p, flag.p, fpos.p, g.out_off.p, n, nsrc_p,
               st.gstack2.p);
   } else {
     if (st.stack_mode) fail(DP_E_UNSUPPORTED, "graphs with 2^24 or more nodes are not supported by the peel");
-    DP_LAUNCH(ctx, k_src_place2, grid_for(n, B), B, 0, by_rank.p, flag.p, fpos.p, g.out_off.p, n, st.nsrc,
+    DP_LAUNCH(ctx, k_src_place2, grid_for(n, B), B, 0, by_rank.p, flag.p, fpos.p, g.out_off.p, n, nsrc_p,
               st.stack_mode, st.gstack.p);
     st.indeg.alloc(ctx, n);
     DP_LAUNCH(ctx, k_indeg_init2, grid_for(n, B), B, 0, g.in_off.p, n, st.indeg.p);
@@ -1646,6 +1653,7 @@ void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st, 
   st.spill.alloc(ctx, m > 0 ? m : 1);
   st.counters.alloc(ctx, 3);
   st.counters.zero();
+  DP_CUDA(cudaMemcpyAsync(st.counters.p + 2, nsrc_p, sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
 }
 
 static PeelArgs peel_args(DevGraph& g, PeelState& st, int32_t* seq, int32_t* pos_of, bool progress) {
@@ -1654,7 +1662,7 @@ static PeelArgs peel_args(DevGraph& g, PeelState& st, int32_t* seq, int32_t* pos
   a.slot = st.slot.p;
   a.indeg = st.indeg.p;
   a.gstack = st.gstack.p;
-  a.nsrc = st.nsrc;
+  a.nsrc = st.counters.p + 2;
   a.stack_mode = st.stack_mode;
   a.seq = seq;
   a.pos_of = pos_of;
@@ -1752,6 +1760,8 @@ PeelDpJob* peel_dp_prepare(DevGraph& g, const int64_t* cpath, int32_t range, int
   j->mx.zero();
   DP_LAUNCH(ctx, k_max_abs, grid_for(n, 256), 256, 0, j->out_sum.p, n, j->mx.p);
   DP_LAUNCH(ctx, k_max_abs, grid_for(g.m_ok, 256), 256, 0, g.out_cost.p, g.m_ok, j->mx.p);
+  // the peel's preparation is enqueued before the one host round trip of this function
+  peel_prepare(g, DP_TOPO_CPD, cpath, j->st);
   const unsigned long long max_out = scalar_to_host(ctx, j->mx.p);
   DpArgs& da = j->da;
   da.keys32 = static_cast<double>(max_out) * (range + 2) < static_cast<double>(1 << 21);
@@ -1774,7 +1784,6 @@ PeelDpJob* peel_dp_prepare(DevGraph& g, const int64_t* cpath, int32_t range, int
   j->dbg.alloc(ctx, 4);
   j->dbg.zero();
   da.debug = getenv("DP_DEBUG_DP") ? j->dbg.p : nullptr;
-  peel_prepare(g, DP_TOPO_CPD, cpath, j->st);
   j->pa = peel_args(g, j->st, seq, pos_of, true);
   j->pa.debug = da.debug ? j->dbg.p + 3 : nullptr;
   da.progress = j->st.counters.p;

@@ -5,7 +5,6 @@
 namespace dpb {
 
 struct PeelState {
-  int32_t nsrc = 0;
   bool stack_mode = true;
   DevBuf<int4> gstack, slot;
   DevBuf<int2> nr2, gstack2;
@@ -13,7 +12,7 @@ struct PeelState {
   int32_t ellw = 8;
   DevBuf<int32_t> indeg;
   DevBuf<int64_t> spill;
-  DevBuf<int> counters;  // [0] progress, [1] emitted, [2] unused
+  DevBuf<int> counters;  // [0] progress, [1] emitted, [2] number of sources
   // peel v6
   bool v6 = false;
   DevBuf<int4> ell6;
