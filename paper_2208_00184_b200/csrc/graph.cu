@@ -160,6 +160,11 @@ __global__ void k_dup_edges(const int32_t* out_off, const int32_t* out_eid, cons
   }
 }
 
+__global__ void k_big_rows(const int32_t* out_off, int32_t n, int* big) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
+    if (out_off[u + 1] - out_off[u] > 64) atomicExch(big, 1);
+}
+
 __global__ void k_pair_keys(const int32_t* esrc, const int32_t* edst, int32_t m, uint64_t* keys,
                             int32_t* vals) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
@@ -832,7 +837,19 @@ void graph_adjacency(DevGraph& g) {
   cnt.zero();
   DP_LAUNCH(ctx, k_row_keys, grid_for(m, B), B, 0, g.esrc.p, g.edst.p, m, n, true, keys.p, vals.p, cnt.p);
   exclusive_scan_i32(ctx, cnt.p, g.out_off.p, (int64_t)n + 1);
-  if (scalar_to_host(ctx, sorted.p) == 1) {
+  // one host round trip for the three facts the host needs: already sorted by source,
+  // edges with resolved endpoints, some row longer than 64
+  DevBuf<int> big(ctx, 1);
+  big.zero();
+  DP_LAUNCH(ctx, k_big_rows, grid_for(n, B), B, 0, g.out_off.p, n, big.p);
+  int hs[3] = {0, 0, 0};
+  sorted.download(&hs[0], 1);
+  download_bytes(ctx, &hs[1], g.out_off.p + n, sizeof(int32_t));
+  big.download(&hs[2], 1);
+  sync(ctx);
+  g.m_ok = hs[1];
+  g.big_rows = hs[2] != 0;
+  if (hs[0] == 1) {
     DP_LAUNCH(ctx, k_iota, grid_for(m, B), B, 0, g.out_eid.p, (int64_t)m);
   } else {
     sort_pairs_u32(ctx, keys.p, keys_out.p, vals.p, g.out_eid.p, m, endbit);
@@ -842,7 +859,6 @@ void graph_adjacency(DevGraph& g) {
   DP_LAUNCH(ctx, k_row_keys, grid_for(m, B), B, 0, g.esrc.p, g.edst.p, m, n, false, keys.p, vals.p, cnt.p);
   exclusive_scan_i32(ctx, cnt.p, g.in_off.p, (int64_t)n + 1);
   sort_pairs_u32(ctx, keys.p, keys_out.p, vals.p, g.in_eid.p, m, endbit);
-  g.m_ok = scalar_to_host(ctx, g.out_off.p + n);
   g.out_dst.alloc(ctx, g.m_ok);
   g.in_src.alloc(ctx, g.m_ok);
   DP_LAUNCH(ctx, k_gather_i32, grid_for(g.m_ok, B), B, 0, g.edst.p, g.out_eid.p, g.out_dst.p, (int64_t)g.m_ok);
@@ -1079,10 +1095,7 @@ Validation graph_validate(DevGraph& g, const dp_graph_t* h, bool all, bool cycle
   first.upload(init, 3);
   DP_LAUNCH(ctx, k_dup_edges, grid_for(n, B), B, 0, g.out_off.p, g.out_eid.p, g.out_dst.p, n, dupflag.p,
             first.p + 2);
-  int big = 0;
-  DP_CUDA(cudaMemcpyAsync(&big, first.p + 2, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  sync(ctx);
-  if (big) {
+  if (g.big_rows) {  // rows longer than 64 (known from graph_adjacency): sort-based pass
     DevBuf<uint64_t> k(ctx, m), ko(ctx, m);
     DevBuf<int32_t> v(ctx, m), vo(ctx, m);
     DP_LAUNCH(ctx, k_pair_keys, grid_for(m, B), B, 0, g.esrc.p, g.edst.p, m, k.p, v.p);

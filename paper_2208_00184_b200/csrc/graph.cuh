@@ -23,6 +23,7 @@ struct DevGraph {
   DevBuf<int32_t> sorted_idx;         // node index per sorted key (ascending idx on ties)
   // adjacency over edges whose endpoints both resolve
   bool has_adj = false;
+  bool big_rows = false;  // some CSR row is longer than 64 (duplicate-edge check sorts)
   int32_t m_ok = 0;
   DevBuf<int32_t> out_off, out_eid, in_off, in_eid, out_dst, in_src;
   // costs
