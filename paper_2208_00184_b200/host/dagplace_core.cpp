@@ -62,6 +62,9 @@ dp_ctx_t* ctx() {
     std::string body = what.compare(0, prefix.size(), prefix) == 0 ? what.substr(prefix.size()) : what;
     throw DagError(kind, body);
   }
+  // size limits of the device path (more than 256 devices, 2^24 or more peel nodes): the
+  // reference has no such limit, so they surface as the library's own error type
+  if (rc == DP_E_UNSUPPORTED) throw DagError(ErrorKind::InstanceTooLarge, what);
   throw std::runtime_error("libdagplace_b200: " + what);
 }
 
