@@ -11,7 +11,9 @@
 // uint64 (static_cast), which is what the reference's number<T>() does.
 #include <cmath>
 #include <cstdlib>
+#include <clocale>
 #include <cstring>
+#include <locale.h>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -199,7 +201,9 @@ struct Reader {
       }
     }
     n.kind = Num::kFloat;
-    n.d = std::strtod(tok.c_str(), nullptr);
+    // the "C" locale whatever LC_NUMERIC says (nlohmann reads '.' under any locale)
+    static const locale_t c_locale = newlocale(LC_ALL_MASK, "C", static_cast<locale_t>(0));
+    n.d = strtod_l(tok.c_str(), nullptr, c_locale);
     return n;
   }
   void literal(const char* w) {
@@ -207,44 +211,64 @@ struct Reader {
     if (static_cast<size_t>(end - p) < k || std::memcmp(p, w, k) != 0) syntax("invalid literal");
     p += k;
   }
-  // Validates one value and returns its span.
-  Span value(int depth = 0) {
-    if (depth > 512) syntax("nesting too deep");
+  // Validates one value and returns its span.  Iterative (an explicit stack of open
+  // containers), so nesting depth is bounded by memory only, as in json::parse.
+  Span value() {
     ws();
     if (p >= end) syntax("unexpected end of input");
     Span s;
     s.b = p;
-    switch (*p) {
-      case '{': {
-        ++p;
-        if (!eat('}')) {
-          do {
+    std::vector<char> open;
+    for (;;) {
+      ws();
+      if (p >= end) syntax("unexpected end of input");
+      bool closed = true;  // a complete value was just read
+      switch (*p) {
+        case '{':
+          ++p;
+          if (!eat('}')) {
+            open.push_back('{');
             ws();
             string(nullptr);
             expect(':', "expected ':'");
-            value(depth + 1);
-          } while (eat(','));
-          expect('}', "expected ',' or '}'");
-        }
-        break;
+            closed = false;
+          }
+          break;
+        case '[':
+          ++p;
+          if (!eat(']')) {
+            open.push_back('[');
+            closed = false;
+          }
+          break;
+        case '"': string(nullptr); break;
+        case 't': literal("true"); break;
+        case 'f': literal("false"); break;
+        case 'n': literal("null"); break;
+        default: number(); break;
       }
-      case '[': {
-        ++p;
-        if (!eat(']')) {
-          do value(depth + 1);
-          while (eat(','));
+      if (!closed) continue;
+      // after a complete value: the next member / element, or close containers
+      for (;;) {
+        if (open.empty()) {
+          s.e = p;
+          return s;
+        }
+        if (open.back() == '{') {
+          if (eat(',')) {
+            ws();
+            string(nullptr);
+            expect(':', "expected ':'");
+            break;
+          }
+          expect('}', "expected ',' or '}'");
+        } else {
+          if (eat(',')) break;
           expect(']', "expected ',' or ']'");
         }
-        break;
+        open.pop_back();
       }
-      case '"': string(nullptr); break;
-      case 't': literal("true"); break;
-      case 'f': literal("false"); break;
-      case 'n': literal("null"); break;
-      default: number(); break;
     }
-    s.e = p;
-    return s;
   }
 };
 

@@ -47,7 +47,11 @@ struct Resident {
   dp_ctx* ctx = nullptr;
   const dp_graph_t* host = nullptr;  // only for error messages during generate
   dp_graph_t host_copy{};
+  std::vector<int64_t> h_id, h_src, h_dst;  // what host_copy points at (dp_resident_create)
   DevGraph g;
+  dp_devices_t dev_in{};                      // the caller's list, checked at placement
+  std::vector<int32_t> dev_in_id;
+  std::vector<int64_t> dev_in_mem;
   Devices devs;
   dp_comm_t comm{};
   dp_pipeline_config_t cfg{};
@@ -143,6 +147,9 @@ void generate_windows(Resident* const* rs, int count) {
   std::vector<PlaceJob*> pj;
   for (int i = 0; i < count; ++i) {
     Resident& r = *rs[i];
+    // SchedulerState::for_devices runs inside order_place (placement.cpp:132,34-53), after
+    // the graph, ccr and fuse errors: the device list is checked here, not at init
+    r.devs = devices_sorted(&r.dev_in);
     ph.emplace_back(new PlaceHandle(place_prepare(r.f.coarse, r.cseq.p, r.devs, &r.po, &r.pa, r.decisions)));
     pj.push_back(ph.back()->j);
   }
@@ -170,9 +177,10 @@ void resident_init(Resident& r, dp_ctx* ctx, const dp_graph_t* h, const dp_devic
   r.ctx = ctx;
   r.host = h;
   r.comm = comm;
-  r.cfg = *cfg;
-  if (r.cfg.fusion_range == 0) r.cfg.fusion_range = 200;
-  r.devs = devices_sorted(devices);
+  r.cfg = *cfg;  // fusion_range < 1 fails in fuse like fusion.cpp:96
+  r.dev_in_id.assign(devices->id, devices->id + devices->count);
+  r.dev_in_mem.assign(devices->memory_bytes, devices->memory_bytes + devices->count);
+  r.dev_in = dp_devices_t{devices->count, r.dev_in_id.data(), r.dev_in_mem.data()};
   int64_t min_cap = devices->memory_bytes[0];
   for (int32_t i = 0; i < devices->count; ++i) min_cap = std::min(min_cap, devices->memory_bytes[i]);
   r.limit = std::max<int64_t>(1, static_cast<int64_t>(static_cast<double>(min_cap) * r.cfg.cluster_mem_fraction));
@@ -368,8 +376,19 @@ int dp_resident_create(dp_ctx_t* ctx, const dp_graph_t* h, const dp_devices_t* d
   auto* r = new dp_resident;
   try {
     resident_init(*r, ctx, h, devices, comm, cfg);
-    // keep a private host copy of the ids/edges for error messages raised later
+    // a private copy of the ids / edge endpoints for error messages raised by later
+    // generate calls (the caller may free its arrays once the graph is on the device)
+    r->h_id.assign(h->node_id, h->node_id + h->n_nodes);
+    r->h_src.assign(h->edge_src, h->edge_src + h->n_edges);
+    r->h_dst.assign(h->edge_dst, h->edge_dst + h->n_edges);
     r->host_copy = *h;
+    r->host_copy.node_id = r->h_id.data();
+    r->host_copy.edge_src = r->h_src.data();
+    r->host_copy.edge_dst = r->h_dst.data();
+    r->host_copy.compute_us = nullptr;
+    r->host_copy.memory_bytes = nullptr;
+    r->host_copy.edge_bytes = nullptr;
+    r->host_copy.group = nullptr;
     r->host = &r->host_copy;
     sync(ctx);
   } catch (...) {

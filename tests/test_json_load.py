@@ -160,3 +160,20 @@ def test_devices(libs):
     ]
     for t in docs:
         _same(_outcome(devices_from_json, dp, t, "dp_"), _outcome(devices_from_json, ref, t, "dpr_"), t)
+
+
+def test_deep_nesting(libs):
+    """json::parse has no nesting limit; neither does the loader (iterative validation)."""
+    dp, ref = libs
+    for depth in (600, 5000):
+        deep = "[" * depth + "]" * depth
+        obj = '{"a":' * depth + "1" + "}" * depth
+        for t in ('{"nodes":[],"edges":[],"meta":%s,"x":%s}' % (deep, obj),
+                  '{"nodes":[{"id":1,"compute_us":2,"memory_bytes":3,"extra":%s}],"edges":[]}' % deep):
+            a = _outcome(graph_from_json, dp, t, "dp_")
+            assert a[0] == "ok", a
+            _same(a, _outcome(graph_from_json, ref, t, "dpr_"), t)
+        bad = '{"nodes":[],"edges":[],"meta":' + "[" * depth + "]" * (depth - 1) + "}"
+        a, b = _outcome(graph_from_json, dp, bad, "dp_"), _outcome(graph_from_json, ref, bad, "dpr_")
+        assert b[0] == "err"
+        _same(a, b, bad, syntax_kind_only=True)
