@@ -55,3 +55,37 @@ def reference_backend() -> Backend:
         be.pipeline_replicas = f
         _cache["dpr"] = be
     return _cache["dpr"]
+
+
+def reference_layered(n: int, width: int, fan_lo: int = 2, fan_hi: int = 6, seed: int = 12345):
+    """The SURVEY §8(d) layered recipe synthesised by oracle/_ref (dpr_gen_layered), so the
+    reference arm of bench.py never maps the product library."""
+    import numpy as np
+
+    from paper_2208_00184_b200._abi import Graph
+    lib = reference_backend().lib
+    f = lib.dpr_gen_layered
+    f.restype = C.c_int
+    p64 = C.POINTER(C.c_int64)
+    f.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_uint64] + [p64] * 7
+    a = [np.zeros(n, np.int64) for _ in range(3)] + [np.zeros(max(1, n * fan_hi), np.int64) for _ in range(3)]
+    m = C.c_int64()
+    rc = f(n, width, fan_lo, fan_hi, seed, *[x.ctypes.data_as(p64) for x in a], C.byref(m))
+    if rc:
+        raise RuntimeError("dpr_gen_layered failed")
+    k = m.value
+    return Graph(a[0], a[1], a[2], a[3][:k].copy(), a[4][:k].copy(), a[5][:k].copy())
+
+
+def reference_candidates(base, D: int, first: int, count: int):
+    """Config #5 candidate rows (SURVEY §8(d) family) from oracle/_ref (dpr_gen_candidates)."""
+    import numpy as np
+    lib = reference_backend().lib
+    f = lib.dpr_gen_candidates
+    f.restype = None
+    u8 = C.POINTER(C.c_uint8)
+    f.argtypes = [u8, C.c_int64, C.c_int32, C.c_int64, C.c_int64, u8]
+    b = np.ascontiguousarray(base, dtype=np.uint8)
+    out = np.zeros((count, b.size), np.uint8)
+    f(b.ctypes.data_as(u8), b.size, D, first, count, out.ctypes.data_as(u8))
+    return out

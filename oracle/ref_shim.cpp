@@ -7,6 +7,8 @@
 // structs of include/dagplace_b200.h.  No algorithm lives here.
 
 #include <algorithm>
+#include <array>
+#include <random>
 #include <chrono>
 #include <cstring>
 #include <map>
@@ -819,6 +821,66 @@ int dpr_pipeline_replicas(const dp_graph_t* g, const dp_devices_t* devices, dp_c
     }
   }
   return 0;
+}
+
+// SURVEY §8(d) common recipe (the bench's config #4 / #5 graphs), restated here so the
+// reference arm of bench.py synthesises its input without the product library:
+// u(lo,hi) = lo + mt19937_64() % (hi-lo+1) (generator.cpp:32-46); node costs in id
+// order, then per non-first-layer node k = u(fan_lo,fan_hi) picks without replacement
+// from the previous layer with bytes u(2^15, 3*2^15); edges sorted by (src, dst).
+int dpr_gen_layered(int64_t n, int64_t width, int64_t fan_lo, int64_t fan_hi, uint64_t seed, int64_t* node_id,
+                    int64_t* compute_us, int64_t* memory_bytes, int64_t* edge_src, int64_t* edge_dst,
+                    int64_t* edge_bytes, int64_t* n_edges) {
+  std::mt19937_64 rng(seed);
+  auto u = [&rng](int64_t lo, int64_t hi) -> int64_t {
+    return hi <= lo ? lo : lo + static_cast<int64_t>(rng() % (static_cast<uint64_t>(hi - lo) + 1));
+  };
+  for (int64_t i = 0; i < n; ++i) {
+    node_id[i] = i;
+    compute_us[i] = u(100, 900);
+    memory_bytes[i] = u(1 << 19, 3 << 19);
+  }
+  std::vector<std::array<int64_t, 3>> es;
+  std::vector<int64_t> taken;  // offsets already picked for v, ascending
+  for (int64_t v = width; v < n; ++v) {
+    const int64_t lo = (v / width - 1) * width, hi = std::min(lo + width, n);
+    const int64_t k = std::min<int64_t>(hi - lo, u(fan_lo, fan_hi));
+    taken.clear();
+    for (int64_t t = 0; t < k; ++t) {
+      // the pick-th entry of the pool with `taken` erased (pool = lo..hi-1 in order)
+      int64_t x = u(0, hi - lo - t - 1);
+      size_t j = 0;
+      for (; j < taken.size() && taken[j] <= x; ++j) ++x;
+      taken.insert(taken.begin() + j, x);
+      es.push_back({lo + x, v, u(1 << 15, 3 << 15)});
+    }
+  }
+  std::sort(es.begin(), es.end(), [](const auto& a, const auto& b) { return a[0] != b[0] ? a[0] < b[0] : a[1] < b[1]; });
+  for (size_t e = 0; e < es.size(); ++e) {
+    edge_src[e] = es[e][0];
+    edge_dst[e] = es[e][1];
+    edge_bytes[e] = es[e][2];
+  }
+  *n_edges = static_cast<int64_t>(es.size());
+  return 0;
+}
+
+// Config #5 candidate family: row k = base with max(1, n_c/100) moves of
+// cluster rk() % n_c -> device rk() % D, rk = mt19937_64(k); row 0 = base.
+void dpr_gen_candidates(const uint8_t* base, int64_t n_clusters, int32_t D, int64_t first, int64_t count,
+                        uint8_t* out) {
+  const int64_t moves = std::max<int64_t>(1, n_clusters / 100);
+  for (int64_t i = 0; i < count; ++i) {
+    const int64_t k = first + i;
+    uint8_t* row = out + i * n_clusters;
+    std::copy(base, base + n_clusters, row);
+    if (k == 0) continue;
+    std::mt19937_64 rk(static_cast<uint64_t>(k));
+    for (int64_t t = 0; t < moves; ++t) {
+      const uint64_t c = rk() % static_cast<uint64_t>(n_clusters);
+      row[c] = static_cast<uint8_t>(rk() % static_cast<uint64_t>(D));
+    }
+  }
 }
 
 }  // extern "C"

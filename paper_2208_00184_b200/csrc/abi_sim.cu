@@ -53,11 +53,11 @@ dp_sim_report_t* sim_report(DevGraph& g, const Devices& devs, const int32_t* dev
   in.D = D;
   in.trace = trace;
   SimOutput out;
-  simulate_dev(g, in, out, 1024);
+  int32_t Q = sim_queue_cap();
+  simulate_dev(g, in, out, Q);
   int64_t ms = scalar_to_host(ctx, out.makespan.p);
-  if (ms < 0 && g.n) {  // a ring overflowed: exact-capacity re-run
-    int32_t Q = 1;
-    while (Q < g.n + g.m + 1) Q <<= 1;
+  while (ms < 0 && g.n) {  // a ring overflowed: re-run with larger rings
+    Q = sim_queue_grow(g, Q);
     simulate_dev(g, in, out, Q);
     ms = scalar_to_host(ctx, out.makespan.p);
   }

@@ -9,6 +9,25 @@
 
 #include "abi_util.cuh"
 
+namespace {
+
+// k picks without replacement from the pool lo..hi-1, each u(0, |pool|-1) and erased
+// from the pool (the recipe's std::vector::erase), without materialising the pool: the
+// pick-th remaining entry is found by skipping the offsets already taken (k <= 6).
+template <typename U, typename F>
+void pick_distinct(U& u, int64_t lo, int64_t hi, int64_t k, std::vector<int64_t>& taken, F emit) {
+  taken.clear();
+  for (int64_t t = 0; t < k; ++t) {
+    int64_t x = u(0, hi - lo - t - 1);
+    size_t j = 0;
+    for (; j < taken.size() && taken[j] <= x; ++j) ++x;
+    taken.insert(taken.begin() + static_cast<std::ptrdiff_t>(j), x);
+    emit(lo + x);
+  }
+}
+
+}  // namespace
+
 extern "C" {
 
 int dp_gen_layered(int64_t n, int64_t width, int64_t fan_lo, int64_t fan_hi, uint64_t seed, int64_t* node_id,
@@ -34,19 +53,12 @@ int dp_gen_layered(int64_t n, int64_t width, int64_t fan_lo, int64_t fan_hi, uin
   };
   std::vector<E> edges;
   edges.reserve(static_cast<size_t>(n * (fan_lo + fan_hi) / 2 + 16));
-  std::vector<int64_t> pool;
+  std::vector<int64_t> taken;
   for (int64_t v = width; v < n; ++v) {
     const int64_t layer = v / width;
     const int64_t lo = (layer - 1) * width, hi = std::min(lo + width, n);
     const int64_t k = std::min<int64_t>(hi - lo, u(fan_lo, fan_hi));
-    pool.resize(static_cast<size_t>(hi - lo));
-    std::iota(pool.begin(), pool.end(), lo);
-    for (int64_t t = 0; t < k; ++t) {
-      const int64_t pick = u(0, static_cast<int64_t>(pool.size()) - 1);
-      const int64_t src = pool[static_cast<size_t>(pick)];
-      pool.erase(pool.begin() + pick);
-      edges.push_back({src, v, u(1 << 15, 3 << 15)});
-    }
+    pick_distinct(u, lo, hi, k, taken, [&](int64_t src) { edges.push_back({src, v, u(1 << 15, 3 << 15)}); });
   }
   std::sort(edges.begin(), edges.end(), [](const E& a, const E& b) { return a.s != b.s ? a.s < b.s : a.d < b.d; });
   for (size_t e = 0; e < edges.size(); ++e) {
@@ -148,19 +160,12 @@ int dp_gen_bert(int64_t n, int64_t width, int64_t skip, uint64_t seed, int64_t* 
     int64_t s, d, b;
   };
   std::vector<E> edges;
-  std::vector<int64_t> pool;
+  std::vector<int64_t> taken;
   for (int64_t v = width; v < n; ++v) {
     const int64_t layer = v / width;
     const int64_t lo = (layer - 1) * width, hi = std::min(lo + width, n);
     const int64_t k = std::min<int64_t>(hi - lo, u(2, 6));
-    pool.resize(static_cast<size_t>(hi - lo));
-    std::iota(pool.begin(), pool.end(), lo);
-    for (int64_t t = 0; t < k; ++t) {
-      const int64_t pick = u(0, static_cast<int64_t>(pool.size()) - 1);
-      const int64_t src = pool[static_cast<size_t>(pick)];
-      pool.erase(pool.begin() + pick);
-      edges.push_back({src, v, u(1 << 15, 3 << 15)});
-    }
+    pick_distinct(u, lo, hi, k, taken, [&](int64_t src) { edges.push_back({src, v, u(1 << 15, 3 << 15)}); });
     if (v >= skip * width && (v / width) % skip == 0) edges.push_back({v - skip * width, v, u(1 << 15, 3 << 15)});
   }
   std::sort(edges.begin(), edges.end(), [](const E& a, const E& b) { return a.s != b.s ? a.s < b.s : a.d < b.d; });

@@ -15,7 +15,7 @@
 //
 // A batch of candidate placements is spread over persistent warps (one candidate per
 // warp at a time).  A candidate whose ring would overflow is marked and re-run with
-// rings sized to the exact bound.
+// 16x larger rings (up to the exact bound, every task queued once per engine).
 #include <algorithm>
 
 #include "simulate.cuh"
@@ -570,20 +570,39 @@ void simulate_dev(DevGraph& g, const SimInput& in, SimOutput& out, int32_t queue
   run_sim(g, in, out, queue_cap, in.n_candidates, nullptr);
 }
 
+int32_t sim_queue_cap() {
+  // DP_SIM_QUEUE (diagnostic, power of two >= 1) shrinks the first-pass rings so tests can
+  // force the overflow -> exact-capacity re-run path
+  if (const char* e = getenv("DP_SIM_QUEUE")) {
+    const int q = atoi(e);
+    if (q >= 1 && (q & (q - 1)) == 0) return q;
+  }
+  return 1024;
+}
+
 void simulate_batch_dev(DevGraph& g, const SimInput& in, SimOutput& out) {
   dp_ctx* ctx = g.ctx;
-  simulate_dev(g, in, out, 1024);
+  int32_t Q = sim_queue_cap();
+  simulate_dev(g, in, out, Q);
   if (g.n == 0) return;
-  std::vector<int64_t> ms = to_host(ctx, out.makespan.p, in.n_candidates);
-  std::vector<int64_t> redo;
-  for (int64_t b = 0; b < in.n_candidates; ++b)
-    if (ms[b] < 0) redo.push_back(b);
-  if (redo.empty()) return;
-  int32_t Q = 1;
-  while (Q < g.n + g.m + 1) Q <<= 1;  // exact bound: every task queued at most once per engine
-  DevBuf<int64_t> list(ctx, redo.size());
-  list.upload(redo.data(), redo.size());
-  run_sim(g, in, out, Q, static_cast<int64_t>(redo.size()), list.p);
+  for (;;) {  // re-run overflowed candidates with 16x larger rings, up to the exact bound
+    std::vector<int64_t> ms = to_host(ctx, out.makespan.p, in.n_candidates);
+    std::vector<int64_t> redo;
+    for (int64_t b = 0; b < in.n_candidates; ++b)
+      if (ms[b] < 0) redo.push_back(b);
+    if (redo.empty()) return;
+    Q = sim_queue_grow(g, Q);
+    DevBuf<int64_t> list(ctx, redo.size());
+    list.upload(redo.data(), redo.size());
+    run_sim(g, in, out, Q, static_cast<int64_t>(redo.size()), list.p);
+  }
+}
+
+int32_t sim_queue_grow(const DevGraph& g, int32_t Q) {
+  int32_t exact = 1;
+  while (exact < g.n + g.m + 1) exact <<= 1;  // every task is queued at most once per engine
+  if (Q >= exact) fail(DP_E_CUDA, "simulate: engine queue overflow at the exact capacity");
+  return static_cast<int32_t>(std::min<int64_t>(exact, static_cast<int64_t>(Q) * 16));
 }
 
 }  // namespace dpb

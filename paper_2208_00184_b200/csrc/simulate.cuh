@@ -25,6 +25,11 @@ struct SimOutput {
 // Requires adjacency + costs on g.  queue_cap: ring capacity per engine (power of 2).
 void simulate_dev(DevGraph& g, const SimInput& in, SimOutput& out, int32_t queue_cap);
 
+// First-pass ring capacity (1024, or DP_SIM_QUEUE for tests).
+int32_t sim_queue_cap();
+// The next ring capacity after an overflow at Q: 16 Q, at most the exact bound.
+int32_t sim_queue_grow(const DevGraph& g, int32_t Q);
+
 // Batch with automatic re-run of overflowed candidates at a larger queue capacity.
 void simulate_batch_dev(DevGraph& g, const SimInput& in, SimOutput& out);
 

@@ -38,6 +38,12 @@ def digest(*arrays) -> str:
     return h.hexdigest()
 
 
+def device_digest(dev) -> str:
+    """Digest of an expanded placement's device ids by node index (int32): what
+    dp_resident_fetch returns, so bench.py can check its own timed outputs."""
+    return digest(np.ascontiguousarray(dev, dtype=np.int32))
+
+
 def pipeline_digests(rep) -> dict:
     off, flat = rep.map.member_arrays()
     d = {
@@ -56,6 +62,8 @@ def pipeline_digests(rep) -> dict:
                                  rep.order_expanded.device_present),
         "adjust_expanded": digest(rep.adjust_expanded.device, rep.adjust_expanded.per_device_memory,
                                   rep.adjust_expanded.device_present),
+        "order_device": device_digest(rep.order_expanded.device),
+        "adjust_device": device_digest(rep.adjust_expanded.device),
         "order_makespan": rep.order_makespan, "adjust_makespan": rep.adjust_makespan,
         "original_ccr": rep.original_ccr, "coarse_ccr": rep.coarse_ccr,
     }
@@ -66,12 +74,35 @@ def graph_digest(g) -> str:
     return digest(g.node_id, g.compute_us, g.memory_bytes, g.edge_src, g.edge_dst, g.edge_bytes)
 
 
+CAND_PREFIX = 512
+
+
+def candidate_prefix(ref, threads: int):
+    """Config #5: makespans of candidates 0..CAND_PREFIX-1 of the family
+    around the reference's adjusting placement, simulated by the reference (a loop of
+    simulate(), simulator.cpp:56-252), and the first strict minimum (:292-294)."""
+    from golden_configs import config5_candidates
+    g, devs, comm, rep, cand = config5_candidates(ref, 0, CAND_PREFIX)
+    t = time.time()
+    ms, am = ref.simulate_candidates(g, rep.map.node_cluster, rep.coarse_nodes, cand, devs, comm, threads)
+    dt = time.time() - t
+    return {"first": 0, "count": CAND_PREFIX, "makespans": [int(x) for x in ms], "argmin": int(am),
+            "base_digest": digest(cand[0]), "rows_digest": digest(cand), "reference_seconds": round(dt, 2),
+            "reference_threads": threads}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default=",".join(CONFIGS))
+    ap.add_argument("--candidates", action="store_true", help="(re)write tests/golden/candidates5.json")
     args = ap.parse_args()
     from oracle.bind import reference_backend
     ref = reference_backend()
+    if args.candidates:
+        c = candidate_prefix(ref, os.cpu_count() or 1)
+        json.dump(c, open(os.path.join(HERE, "candidates5.json"), "w"), indent=0)
+        print("candidates", c["count"], "argmin", c["argmin"], c["makespans"][c["argmin"]], c["reference_seconds"], "s")
+        return
     path = os.path.join(HERE, "configs.json")
     out = json.load(open(path)) if os.path.exists(path) else {}
     for name in args.configs.split(","):
