@@ -595,6 +595,10 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem<BB>& S) {
       } else {
         const uint32_t rem = hit ? (e & 127u) : code;
         fr = rem == 1u;
+        // armed: one predecessor left, so this child is freed (and, if it is the best freed
+        // child, popped next) when that predecessor is popped — usually many steps later.
+        // Its row goes to L2 now, off the chain.
+        if (pf && rem == 2u) prefetch_l2(ell6 + static_cast<int64_t>(my.x) * 4);
         if (hit) {
           S.ht[2 * b + (h0 ? 0 : 1)] = fr ? kV6Empty : e - 1;
         } else if (!fr) {  // first touch: insert (ways taken by concurrent lanes -> spill)

@@ -90,11 +90,17 @@ def test_resident_cycle_in_large_graph(gpu, ref):
     """A back edge deep inside a 50k-node layered graph: the resident generate path (no
     separate Kahn pass) must report the reference's cycle witness."""
     g = layered(9, 50000, 128)
-    src, dst = g.edge_src.copy(), g.edge_dst.copy()
-    e = len(src) // 2
-    src[e], dst[e] = dst[e], src[e]
+    # walk 150 layers up from a node in layer 250 along in-edges, then close the path
+    pred = {}
+    for s_, d_ in zip(g.edge_src.tolist(), g.edge_dst.tolist()):
+        pred.setdefault(d_, s_)
+    end = 250 * 128 + 5
+    v = end
+    for _ in range(150):
+        v = pred[v]
     from paper_2208_00184_b200._abi import Graph
-    bad = Graph(g.node_id, g.compute_us, g.memory_bytes, src, dst, g.edge_bytes)
+    bad = Graph(g.node_id, g.compute_us, g.memory_bytes, np.append(g.edge_src, end), np.append(g.edge_dst, v),
+                np.append(g.edge_bytes, 77))
     devs = devices(8, capacity_for(g, 8, 1.25))
     want = ref_outcome(ref, bad, devs)
     assert want[0] == "err" and want[1] == 1  # CycleDetected
