@@ -196,7 +196,8 @@ typedef struct dp_pipeline_config {
   int32_t fusion_range;          /* default 200 */
   double cluster_mem_fraction;   /* default 0.25 */
   int32_t strategy;              /* 0 Order, 1 Adjust (default) */
-  int32_t simulate;              /* 1: run pipeline.cpp:89-90 simulations */
+  int32_t simulate;              /* 1: run pipeline.cpp:89-90 simulations (makespans);
+                                    2: also return both full SimulationReports (trace) */
 } dp_pipeline_config_t;
 
 /* Output of the generation window (pipeline.cpp:67-79) and the report fields. */
@@ -213,6 +214,8 @@ typedef struct dp_pipeline_result {
   int64_t* coarse_sequence;               /* [coarse_nodes] cpd_topo of the coarse graph */
   int64_t order_makespan, adjust_makespan; /* -1 unless simulate */
   double generation_ms;                   /* device time of the window */
+  dp_sim_report_t* order_sim;             /* simulate == 2: simulate(order_expanded), */
+  dp_sim_report_t* adjust_sim;            /* simulate(adjust_expanded) with trace; else NULL */
 } dp_pipeline_result_t;
 
 /* ---------------------------------------------------------------- context */

@@ -109,7 +109,7 @@ class PipelineC(C.Structure):
                 ("order_expanded", C.POINTER(PlacementC)),
                 ("adjust_expanded", C.POINTER(PlacementC)), ("coarse_sequence", I64P),
                 ("order_makespan", C.c_int64), ("adjust_makespan", C.c_int64),
-                ("generation_ms", C.c_double)]
+                ("generation_ms", C.c_double), ("order_sim", C.c_void_p), ("adjust_sim", C.c_void_p)]
 
 
 # ----------------------------------------------------------------- python-side types

@@ -29,6 +29,8 @@ void dp_pipeline_result_free(dp_pipeline_result_t* r) {
   free_placement(r->order_expanded);
   free_placement(r->adjust_expanded);
   std::free(r->coarse_sequence);
+  dp_sim_report_free(r->order_sim);
+  dp_sim_report_free(r->adjust_sim);
   std::free(r);
 }
 }

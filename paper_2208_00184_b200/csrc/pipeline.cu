@@ -347,15 +347,16 @@ int dp_pipeline_batch(dp_ctx_t* ctx, int32_t count, const dp_graph_t* const* gra
   }
   sync(ctx);
   for (auto& f : fin) f();
-  if (cfg->simulate) {  // pipeline.cpp:89-90
+  if (cfg->simulate) {  // pipeline.cpp:89-90 (full reports kept for simulate == 2)
+    const bool full = cfg->simulate == 2;
     for (int32_t i = 0; i < count; ++i) {
       Resident& r = *rp[i];
-      dp_sim_report_t* so = sim_report(r.g, r.devs, r.dev_order.p, false);
-      dp_sim_report_t* sa = sim_report(r.g, r.devs, r.dev_adjust.p, false);
+      dp_sim_report_t* so = sim_report(r.g, r.devs, r.dev_order.p, full);
       res[i]->order_makespan = so->makespan;
+      if (full) res[i]->order_sim = so; else free_sim(so);
+      dp_sim_report_t* sa = sim_report(r.g, r.devs, r.dev_adjust.p, full);
       res[i]->adjust_makespan = sa->makespan;
-      free_sim(so);
-      free_sim(sa);
+      if (full) res[i]->adjust_sim = sa; else free_sim(sa);
     }
   }
   if (dbg) {

@@ -764,7 +764,7 @@ PipelineReport evaluate_pipeline(const ComputationGraph& graph, const std::optio
   Flat f(working);
   FlatDevices fd(devices);
   dp_pipeline_config_t cfg{config.fusion_range, config.cluster_mem_fraction,
-                           config.strategy == PlaceStrategy::Order ? 0 : 1, 1};
+                           config.strategy == PlaceStrategy::Order ? 0 : 1, 2};
   Owned<dp_pipeline_result_t, void (*)(dp_pipeline_result_t*)> r(dp_pipeline_result_free);
   check(dp_pipeline(ctx(), &f.g, &fd.d, cm(comm), &cfg, &r.p));
   report.original_nodes = r.p->original_nodes;
@@ -791,14 +791,14 @@ PipelineReport evaluate_pipeline(const ComputationGraph& graph, const std::optio
     report.chosen_oom_risk = seq.oom_risk;
     report.chosen_placement = seq.placement;
     report.chosen_simulation = simulate(working, seq.placement, devices, comm);
-  } else if (config.strategy == PlaceStrategy::Order) {
+  } else if (config.strategy == PlaceStrategy::Order) {  // the report of pipeline.cpp:89, reused (:100-103)
     report.chosen_oom_risk = order_res.oom_risk;
     report.chosen_placement = std::move(order_exp);
-    report.chosen_simulation = simulate(working, report.chosen_placement, devices, comm);
-  } else {
+    report.chosen_simulation = sim_from(r.p->order_sim);
+  } else {  // pipeline.cpp:90, reused (:104-107)
     report.chosen_oom_risk = adjust_res.oom_risk;
     report.chosen_placement = std::move(adjust_exp);
-    report.chosen_simulation = simulate(working, report.chosen_placement, devices, comm);
+    report.chosen_simulation = sim_from(r.p->adjust_sim);
   }
   return report;
 }
