@@ -235,6 +235,10 @@ int32_t dp_ctx_stage_count(const dp_ctx_t* ctx);
 const char* dp_ctx_stage_name(const dp_ctx_t* ctx, int32_t i);
 double dp_ctx_stage_ms(const dp_ctx_t* ctx, int32_t i);
 double dp_ctx_stage_bytes(const dp_ctx_t* ctx, int32_t i); /* algorithmic bytes */
+/* Outcomes of the tree peel (csrc/fixpoint.cu) counted while DP_DEBUG_FIXPOINT is set
+ * (diagnostic): out[0] first tree proven, [1] converged by fixed-point rounds, [2] gave up
+ * (chain-like), [3] not a DAG, [4] round budget exhausted (the one-warp peel ran). */
+int dp_ctx_peel_stats(const dp_ctx_t* ctx, int64_t* out5);
 
 const char* dp_last_error_message(void);
 int32_t dp_last_error_code(void);

@@ -13,7 +13,7 @@ I32P = C.POINTER(C.c_int32)
 HEADER_SYMBOLS = [
     "dp_last_error_message", "dp_last_error_code", "dp_ctx_create", "dp_ctx_destroy",
     "dp_ctx_set_stream", "dp_ctx_synchronize", "dp_ctx_launch_count", "dp_ctx_enable_stage_timing",
-    "dp_ctx_stage_count", "dp_ctx_stage_name", "dp_ctx_stage_ms", "dp_ctx_stage_bytes",
+    "dp_ctx_stage_count", "dp_ctx_stage_name", "dp_ctx_stage_ms", "dp_ctx_stage_bytes", "dp_ctx_peel_stats",
     "dp_comm_time", "dp_ccr", "dp_validate", "dp_violation_list_free", "dp_require_valid",
     "dp_graph_index", "dp_compute_levels", "dp_topo_order", "dp_is_valid_topo_order",
     "dp_merge_is_safe", "dp_optimal_breakpoints", "dp_cluster_map_free", "dp_build_coarse_graph",
@@ -48,6 +48,7 @@ def declare(lib: C.CDLL) -> None:
     lib.dp_ctx_stage_ms.restype = C.c_double
     lib.dp_ctx_stage_ms.argtypes = [C.c_void_p, C.c_int32]
     lib.dp_ctx_stage_bytes.restype = C.c_double
+    lib.dp_ctx_peel_stats.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
     lib.dp_ctx_stage_bytes.argtypes = [C.c_void_p, C.c_int32]
     lib.dp_resident_create.restype = C.c_int
     lib.dp_resident_create.argtypes = [C.c_void_p, C.POINTER(GraphC), C.POINTER(DevicesC), CommC,

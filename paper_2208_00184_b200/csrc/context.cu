@@ -225,6 +225,11 @@ int dp_ctx_synchronize(dp_ctx_t* ctx) {
 
 int64_t dp_ctx_launch_count(const dp_ctx_t* ctx) { return ctx->launches; }
 
+int dp_ctx_peel_stats(const dp_ctx_t* ctx, int64_t* out5) {
+  for (int i = 0; i < 5; ++i) out5[i] = ctx->tree_stats[i];
+  return DP_OK;
+}
+
 int dp_ctx_enable_stage_timing(dp_ctx_t* ctx, int32_t on) {
   ctx->timing = on != 0;
   return DP_OK;

@@ -1,0 +1,446 @@
+// fixpoint.cu — the stack peel (ordering.cpp:40-77: cpd_topo :98-114, dfs_topo :88-96) as a
+// level-parallel tree construction plus a parallel proof, instead of a one-warp chain.
+//
+// Characterisation: for a topological order s let T(s) be the forest in
+// which parent(v) is v's predecessor emitted last in s; children, and the roots (the
+// sources), are visited by rank (cpath desc, id asc for CPD; id asc for DFS).  The peel's
+// order is the unique topological s with s = preorder(T(s)): the peel pops a node, then
+// the best child it freed (a node is freed by its last predecessor), and when a subtree is
+// exhausted it resumes with the stack top, which is the next unvisited child of the nearest
+// ancestor.  Any topological s with T(preorder(T(s))) = T(s) is therefore the peel order.
+//
+// The start that makes this cheap: s0 = the Kahn order built level by level where level
+// l+1 lists the nodes freed by level l grouped by their last-processed predecessor (in s0
+// order) and, within a group, by rank.  Then T0 = T(s0) is exactly that freeing forest, a
+// node's T0-parent lies on the level just above it, so the depth of a node in T0 is its hop
+// level, and within one depth the preorder of T0 lists nodes in the same order as the
+// breadth-first order s0 does.  When every edge joins consecutive levels (layered DAGs,
+// config #4 deep and wide) T(preorder(T0)) = T0 follows, i.e. one tree construction is the
+// answer; the proof runs anyway and is cheap.  Otherwise the iteration s <- preorder(T(s))
+// continues from there (it converges: agreement with the peel on a prefix of length P
+// implies agreement on P + 1 after one more step), under a round budget; past it the
+// one-warp peel runs (PeelArgs.skip stays 0).
+//
+// One CTA per graph, __syncthreads between levels (no grid barrier, no cooperative launch,
+// one SM per graph like the one-warp peel):
+//   1  Kahn by levels: A relaxes level l (atomicMax of the parent position, in-degree
+//      decrement), B numbers level l+1 from level l's rows in rank order (block scan)
+//   2  subtree sizes of T0, deepest level first
+//   3  preorder positions, shallowest level first (roots by a block scan)
+//   4  proof: for every node the predecessor with the largest preorder position is its T0
+//      parent; writes seq / pos_of
+// Algorithmic bytes per node and edge: 1 reads the rows twice and relaxes each edge once,
+// 2 and 3 read the rows once more, 4 reads the CSC once (fixpoint_launch).
+#include <algorithm>
+
+#include "fixpoint.cuh"
+#include "graph.cuh"
+
+namespace dpb {
+namespace {
+
+constexpr int kTreeThreads = 1024;
+constexpr int kTreeBatch = 8;
+
+struct TreeArgs {
+  int32_t n;
+  const int32_t* nsrc;  // device: number of sources
+  const int32_t* in_off;
+  const int32_t* in_src;
+  const int32_t* out_off;
+  const int32_t* rowc;   // CSR children, each row sorted by rank (best first)
+  const int32_t* roots;  // sources by rank
+  int32_t* seq0;         // breadth-first order s0 (level-major)
+  int32_t* best;         // s0 position of the T0 parent
+  int32_t* indeg;
+  int32_t* size;
+  int32_t* pre;          // preorder positions
+  int32_t* pre2;         // general rounds: second buffer
+  int32_t* par;          // general rounds: T(s) parent
+  int32_t* lvl_off;      // [n + 1]
+  int32_t max_levels;    // more levels than this: give up (chain-like graph)
+  int32_t max_rounds;    // general rounds after a failed proof (-1: from the cost model)
+  int32_t* seq;
+  int32_t* pos_of;
+  int* skip;
+  int* progress;
+  int* emitted;
+  int* info;             // [0] status (1 ok, 2 too deep, 3 not a DAG, 4 budget), [1] levels, [2] rounds
+};
+
+struct TreeBatch {
+  TreeArgs a[kTreeBatch];
+};
+
+__device__ __forceinline__ int32_t ldcg(const int32_t* p) { return __ldcg(p); }
+
+// Exclusive block scan over kTreeThreads threads; *total = sum.  All threads call.
+__device__ __forceinline__ int32_t block_scan(int32_t x, int32_t* total, int32_t* ws) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t s = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, s, o);
+    if (lane >= o) s += y;
+  }
+  if (lane == 31) ws[warp] = s;
+  __syncthreads();
+  if (warp == 0) {
+    int32_t t = ws[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    ws[lane] = t;
+  }
+  __syncthreads();
+  const int32_t r = (warp ? ws[warp - 1] : 0) + s - x;
+  *total = ws[31];
+  __syncthreads();
+  return r;
+}
+
+// pre[roots in s0 level 0 order] = exclusive scan of their subtree sizes
+__device__ void roots_scan(const TreeArgs& a, int32_t nsrc, const int32_t* size, int32_t* pre, int32_t* ws) {
+  int32_t carry = 0;
+  for (int32_t i0 = 0; i0 < nsrc; i0 += kTreeThreads) {
+    const int32_t i = i0 + threadIdx.x;
+    const int32_t v = i < nsrc ? a.seq0[i] : -1;
+    const int32_t s = v >= 0 ? size[v] : 0;
+    int32_t tot;
+    const int32_t ex = block_scan(s, &tot, ws);
+    if (v >= 0) pre[v] = carry + ex;
+    carry += tot;
+  }
+}
+
+__global__ void __launch_bounds__(kTreeThreads, 1) k_treepeel(const __grid_constant__ TreeBatch batch) {
+  const TreeArgs& a = batch.a[blockIdx.x];
+  __shared__ int32_t ws[32];
+  const int tid = threadIdx.x;
+  const int32_t n = a.n;
+  const int32_t nsrc = *a.nsrc;
+  for (int32_t v = tid; v < n; v += kTreeThreads) {
+    a.best[v] = -1;
+    a.indeg[v] = a.in_off[v + 1] - a.in_off[v];
+  }
+  for (int32_t i = tid; i < nsrc; i += kTreeThreads) a.seq0[i] = a.roots[i];
+  if (tid == 0) a.lvl_off[0] = 0;
+  __syncthreads();
+  // ---- 1: breadth-first order s0 and the freeing forest T0
+  int32_t lb = 0, le = nsrc, L = 0;
+  while (lb < le) {
+    if (tid == 0) a.lvl_off[L + 1] = le;
+    if (L >= a.max_levels) {
+      if (tid == 0) a.info[0] = 2;
+      return;
+    }
+    for (int32_t i = lb + tid; i < le; i += kTreeThreads) {
+      const int32_t v = a.seq0[i];
+      const int32_t kb = a.out_off[v], ke = a.out_off[v + 1];
+      for (int32_t k = kb; k < ke; ++k) {
+        const int32_t c = a.rowc[k];
+        atomicMax(a.best + c, i);
+        atomicSub(a.indeg + c, 1);
+      }
+    }
+    __syncthreads();
+    int32_t carry = 0;
+    for (int32_t i0 = lb; i0 < le; i0 += kTreeThreads) {
+      const int32_t i = i0 + tid;
+      int32_t kb = 0, ke = 0, cnt = 0;
+      unsigned hit = 0;
+      int32_t cc[8];
+      if (i < le) {
+        const int32_t v = a.seq0[i];
+        kb = a.out_off[v];
+        ke = a.out_off[v + 1];
+        if (ke - kb <= 8) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            cc[q] = kb + q < ke ? a.rowc[kb + q] : 0;
+            if (kb + q < ke && ldcg(a.best + cc[q]) == i && ldcg(a.indeg + cc[q]) == 0) hit |= 1u << q;
+          }
+          cnt = __popc(hit);
+        } else {
+          for (int32_t k = kb; k < ke; ++k) {
+            const int32_t c = a.rowc[k];
+            cnt += (ldcg(a.best + c) == i && ldcg(a.indeg + c) == 0) ? 1 : 0;
+          }
+        }
+      }
+      int32_t tot;
+      const int32_t ex = block_scan(cnt, &tot, ws);
+      if (cnt) {
+        int32_t o = le + carry + ex;
+        if (ke - kb <= 8) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (hit >> q & 1u) a.seq0[o++] = cc[q];
+        } else {
+          for (int32_t k = kb; k < ke; ++k) {
+            const int32_t c = a.rowc[k];
+            if (ldcg(a.best + c) == i && ldcg(a.indeg + c) == 0) a.seq0[o++] = c;
+          }
+        }
+      }
+      carry += tot;
+    }
+    __syncthreads();
+    lb = le;
+    le += carry;
+    ++L;
+  }
+  if (le != n) {  // not a DAG: the one-warp peel reports it
+    if (tid == 0) a.info[0] = 3;
+    return;
+  }
+  // ---- 2: subtree sizes of T0 (a child's parent position is best[child])
+  for (int32_t l = L - 1; l >= 0; --l) {
+    const int32_t b = a.lvl_off[l], e = a.lvl_off[l + 1];
+    for (int32_t i = b + tid; i < e; i += kTreeThreads) {
+      const int32_t v = a.seq0[i];
+      int32_t s = 1;
+      for (int32_t k = a.out_off[v]; k < a.out_off[v + 1]; ++k) {
+        const int32_t c = a.rowc[k];
+        if (ldcg(a.best + c) == i) s += a.size[c];
+      }
+      a.size[v] = s;
+    }
+    __syncthreads();
+  }
+  // ---- 3: preorder positions of T0
+  roots_scan(a, nsrc, a.size, a.pre, ws);
+  __syncthreads();
+  for (int32_t l = 0; l + 1 < L; ++l) {
+    const int32_t b = a.lvl_off[l], e = a.lvl_off[l + 1];
+    for (int32_t i = b + tid; i < e; i += kTreeThreads) {
+      const int32_t v = a.seq0[i];
+      int32_t acc = a.pre[v] + 1;
+      for (int32_t k = a.out_off[v]; k < a.out_off[v + 1]; ++k) {
+        const int32_t c = a.rowc[k];
+        if (ldcg(a.best + c) == i) {
+          a.pre[c] = acc;
+          acc += a.size[c];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // ---- 4: proof T(preorder(T0)) = T0
+  bool bad = false;
+  for (int32_t v = tid; v < n; v += kTreeThreads) {
+    const int32_t b = a.in_off[v], e = a.in_off[v + 1];
+    if (b == e) continue;
+    int32_t mx = -1;
+    for (int32_t k = b; k < e; ++k) mx = max(mx, a.pre[a.in_src[k]]);
+    bad |= mx != a.pre[a.seq0[ldcg(a.best + v)]];
+  }
+  int32_t* pos = a.pre;
+  int rounds = 1;
+  if (__syncthreads_or(bad)) {
+    // general rounds s <- preorder(T(s)) on the same levels (a T(s) parent is a
+    // predecessor, so it sits on a shallower level)
+    int32_t budget = a.max_rounds;
+    if (budget < 0) budget = max(0, (n / 8) / (6 * L + 8));
+    int32_t* nxt = a.pre2;
+    bool done = false;
+    for (int r = 0; r < budget && !done; ++r) {
+      ++rounds;
+      for (int32_t v = tid; v < n; v += kTreeThreads) {
+        int32_t bp = -1, bu = -1;
+        for (int32_t k = a.in_off[v]; k < a.in_off[v + 1]; ++k) {
+          const int32_t u = a.in_src[k];
+          const int32_t q = pos[u];
+          if (q > bp) {
+            bp = q;
+            bu = u;
+          }
+        }
+        a.par[v] = bu;
+      }
+      __syncthreads();
+      for (int32_t l = L - 1; l >= 0; --l) {
+        const int32_t b = a.lvl_off[l], e = a.lvl_off[l + 1];
+        for (int32_t i = b + tid; i < e; i += kTreeThreads) {
+          const int32_t v = a.seq0[i];
+          int32_t s = 1;
+          for (int32_t k = a.out_off[v]; k < a.out_off[v + 1]; ++k) {
+            const int32_t c = a.rowc[k];
+            if (a.par[c] == v) s += a.size[c];
+          }
+          a.size[v] = s;
+        }
+        __syncthreads();
+      }
+      roots_scan(a, nsrc, a.size, nxt, ws);
+      __syncthreads();
+      for (int32_t l = 0; l + 1 < L; ++l) {
+        const int32_t b = a.lvl_off[l], e = a.lvl_off[l + 1];
+        for (int32_t i = b + tid; i < e; i += kTreeThreads) {
+          const int32_t v = a.seq0[i];
+          int32_t acc = nxt[v] + 1;
+          for (int32_t k = a.out_off[v]; k < a.out_off[v + 1]; ++k) {
+            const int32_t c = a.rowc[k];
+            if (a.par[c] == v) {
+              nxt[c] = acc;
+              acc += a.size[c];
+            }
+          }
+        }
+        __syncthreads();
+      }
+      bool chg = false;
+      for (int32_t v = tid; v < n; v += kTreeThreads) chg |= nxt[v] != pos[v];
+      done = !__syncthreads_or(chg);
+      int32_t* t = pos;
+      pos = nxt;
+      nxt = t;
+    }
+    if (!done) {
+      if (tid == 0) {
+        a.info[0] = 4;
+        a.info[1] = L;
+        a.info[2] = rounds;
+      }
+      return;
+    }
+  }
+  for (int32_t v = tid; v < n; v += kTreeThreads) {
+    const int32_t p = pos[v];
+    a.seq[p] = v;
+    a.pos_of[v] = p;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    a.info[0] = 1;
+    a.info[1] = L;
+    a.info[2] = rounds;
+    *a.skip = 1;
+    *a.emitted = n;
+    *a.progress = n;
+  }
+}
+
+// Rows of at most 64 children sorted by rank, one thread per row (insertion sort in place).
+__global__ void k_rows_by_rank(const int32_t* out_off, const int32_t* out_dst, const int32_t* rank, int32_t n,
+                               int32_t* rowc, int* long_rows) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t b = out_off[v], d = out_off[v + 1] - b;
+    if (d > 64) {
+      atomicExch(long_rows, 1);
+      continue;
+    }
+    for (int32_t q = 0; q < d; ++q) {
+      const int32_t c = out_dst[b + q];
+      const int32_t rc = rank[c];
+      int32_t j = q;
+      while (j > 0 && rank[rowc[b + j - 1]] > rc) {
+        rowc[b + j] = rowc[b + j - 1];
+        --j;
+      }
+      rowc[b + j] = c;
+    }
+  }
+}
+
+__global__ void k_row_rank_keys(const int32_t* out_off, const int32_t* out_dst, const int32_t* rank, int32_t n,
+                                uint64_t* keys, int32_t* vals) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+    for (int32_t k = out_off[v]; k < out_off[v + 1]; ++k) {
+      keys[k] = (static_cast<uint64_t>(v) << 32) | static_cast<uint32_t>(rank[out_dst[k]]);
+      vals[k] = out_dst[k];
+    }
+}
+
+__global__ void k_roots(const int32_t* by_rank, const int32_t* flag, const int32_t* fpos, int32_t n, int32_t* roots) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    if (flag[r]) roots[fpos[r]] = by_rank[r];
+}
+
+}  // namespace
+
+struct TreeJob {
+  DevBuf<int32_t> rowc, roots, seq0, best, indeg, size, pre, pre2, par, lvl_off;
+  DevBuf<int> info;
+};
+
+bool fixpoint_wanted(const DevGraph& g) {
+  if (getenv("DP_PEEL_NO_FIXPOINT")) return false;
+  return g.n >= (getenv("DP_PEEL_FIXPOINT") ? 1 : 2048) && g.m_ok > 0;
+}
+
+void fixpoint_launch(DevGraph& g, const int32_t* by_rank, const int32_t* rank, const int32_t* flag,
+                     const int32_t* fpos, int32_t* seq, int32_t* pos_of, int* skip, int* progress, int* emitted) {
+  dp_ctx* ctx = g.ctx;
+  const int B = 256;
+  const int32_t n = g.n, m = g.m_ok;
+  TreeJob j;
+  j.rowc.alloc(ctx, m > 0 ? m : 1);
+  DevBuf<int> flags(ctx, 1);
+  flags.zero();
+  DP_LAUNCH(ctx, k_rows_by_rank, grid_for(n, B), B, 0, g.out_off.p, g.out_dst.p, rank, n, j.rowc.p, flags.p);
+  if (g.big_rows && scalar_to_host(ctx, flags.p)) {  // some row > 64: one global sort of (row, rank)
+    DevBuf<uint64_t> keys(ctx, m), keys_out(ctx, m);
+    DevBuf<int32_t> vals(ctx, m);
+    DP_LAUNCH(ctx, k_row_rank_keys, grid_for(n, B), B, 0, g.out_off.p, g.out_dst.p, rank, n, keys.p, vals.p);
+    int bits = 1;
+    while ((1ll << bits) < n) ++bits;
+    sort_pairs_u64(ctx, keys.p, keys_out.p, vals.p, j.rowc.p, m, 0, 32 + bits);
+  }
+  j.roots.alloc(ctx, n);
+  DP_LAUNCH(ctx, k_roots, grid_for(n, B), B, 0, by_rank, flag, fpos, n, j.roots.p);
+  j.seq0.alloc(ctx, n);
+  j.best.alloc(ctx, n);
+  j.indeg.alloc(ctx, n);
+  j.size.alloc(ctx, n);
+  j.pre.alloc(ctx, n);
+  j.pre2.alloc(ctx, n);
+  j.par.alloc(ctx, n);
+  j.lvl_off.alloc(ctx, (size_t)n + 1);
+  j.info.alloc(ctx, 3);
+  j.info.zero();
+  TreeBatch b{};
+  TreeArgs& a = b.a[0];
+  a.n = n;
+  a.nsrc = fpos + n;
+  a.in_off = g.in_off.p;
+  a.in_src = g.in_src.p;
+  a.out_off = g.out_off.p;
+  a.rowc = j.rowc.p;
+  a.roots = j.roots.p;
+  a.seq0 = j.seq0.p;
+  a.best = j.best.p;
+  a.indeg = j.indeg.p;
+  a.size = j.size.p;
+  a.pre = j.pre.p;
+  a.pre2 = j.pre2.p;
+  a.par = j.par.p;
+  a.lvl_off = j.lvl_off.p;
+  // ~8 us per level (all phases) against ~0.4 us per node for the one-warp peel
+  a.max_levels = getenv("DP_PEEL_FIXPOINT") ? n + 1 : std::max(64, n / 40);
+  a.max_rounds = getenv("DP_PEEL_FIXPOINT") ? 4096 : -1;
+  if (const char* e = getenv("DP_FIXPOINT_ROUNDS")) a.max_rounds = std::max(0, atoi(e));
+  a.seq = seq;
+  a.pos_of = pos_of;
+  a.skip = skip;
+  a.progress = progress;
+  a.emitted = emitted;
+  a.info = j.info.p;
+  {
+    StageScope s(ctx, "peel (tree)", 40.0 * n + 20.0 * m);
+    DP_LAUNCH(ctx, k_treepeel, 1, kTreeThreads, 0, b);
+  }
+  if (getenv("DP_DEBUG_FIXPOINT")) {
+    int h[3];
+    j.info.download(h, 3);
+    sync(ctx);
+    fprintf(stderr, "[treepeel] n=%d status=%d levels=%d rounds=%d\n", n, h[0], h[1], h[2]);
+    const int slot = h[0] == 1 ? (h[2] == 1 ? 0 : 1) : h[0];
+    if (slot >= 0 && slot < 5) ++ctx->tree_stats[slot];
+  }
+}
+
+}  // namespace dpb

@@ -271,12 +271,27 @@ __device__ __forceinline__ void kahn_relax_warp(const KahnArgs& a, int32_t u, in
                  : "memory");
     old[q] = r;
   }
-#pragma unroll
-  for (int q = 0; q < 8; ++q) ff[q] = old[q] == 1;
+  // one append per warp for all its lanes' freed children (one atomic on the shared tail
+  // instead of eight)
+  int nf = 0;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    const int slot = warp_append(tail, ff[q]);
-    if (ff[q]) a.order[slot] = fv[q];
+    ff[q] = old[q] == 1;
+    nf += ff[q] ? 1 : 0;
+  }
+  {
+    int incl = nf;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int base = 0;
+    if (lane == 31 && incl) base = atomicAdd(tail, incl);
+    base = __shfl_sync(0xffffffffu, base, 31) + incl - nf;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (ff[q]) a.order[base++] = fv[q];
   }
   unsigned big = __ballot_sync(0xffffffffu, u >= 0 && !small);
   while (big) {
@@ -946,6 +961,7 @@ bool graph_levels_indexorder(DevGraph& g, int64_t* tlevel, int64_t* blevel, bool
   sync(ctx);
   if (static_cast<int>(h[0]) != 1) return false;
   const bool sweep = (n <= kSeqMaxN || chainlike) && getenv("DP_LEVELS_FLOW") == nullptr;
+
   if (sweep) {
     DevGraph* gs[1] = {&g};
     int64_t* t1[1] = {tlevel};

@@ -25,6 +25,7 @@
 #include "graph.cuh"
 #include "peel.cuh"
 #include "peel_dp.cuh"
+#include "fixpoint.cuh"
 
 namespace dpb {
 namespace {
@@ -74,6 +75,7 @@ struct PeelArgs {
   int32_t* gover;        // remaining in-degree of keys spilled from full buckets (0 = absent)
   long long* debug;      // optional: peel warp cycles
   bool prefetch;         // v6: prefetch the rows of a pushed child's children to L2
+  const int* skip;       // *skip != 0: the order was produced by the fixed-point peel (fixpoint.cu)
 };
 
 // The peel warp.  Shared memory: stack cache (kStackCache int4) + freed buffer.
@@ -648,6 +650,7 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem<BB>& S) {
 
 template <int BB>
 __device__ __forceinline__ void peel_dispatch(const PeelArgs& a, int4* smem4) {
+  if (a.skip && *a.skip) return;
   if (a.v6) {
     peel_warp_v6(a, *reinterpret_cast<V6Smem<BB>*>(smem4));
     return;
@@ -1592,7 +1595,8 @@ size_t peel_smem() { return kPeelRegion; }  // k_peel2 (topo_order)
 }  // namespace
 
 // Builds the peel inputs (ranks, 16-byte slot records, initial stack, in-degrees).
-void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st, bool force_v5) {
+void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st, bool force_v5, int32_t* seq,
+                  int32_t* pos_of, bool tree) {
   dp_ctx* ctx = g.ctx;
   const int B = 256;
   const int32_t n = g.n, m = g.m_ok;
@@ -1614,6 +1618,15 @@ void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st, 
   exclusive_scan_i32(ctx, flag.p, fpos.p, (int64_t)n + 1);
   const int32_t* nsrc_p = fpos.p + n;  // the scan's total: read on the device
   st.stack_mode = policy != DP_TOPO_M;
+  // shallow graphs: the fixed-point peel runs first (after the counters are reset below)
+  // and, when it converges, the one-warp peel exits at once
+  const bool fix = st.stack_mode && seq != nullptr && tree && fixpoint_wanted(g);
+  auto fixpoint = [&] {
+    if (!fix) return;
+    st.skip.alloc(ctx, 1);
+    st.skip.zero();
+    fixpoint_launch(g, by_rank.p, rank.p, flag.p, fpos.p, seq, pos_of, st.skip.p, st.counters.p, st.counters.p + 1);
+  };
   st.v6 = st.stack_mode && n < (1 << 24) && static_cast<int64_t>(m) <= 6 * static_cast<int64_t>(n) && !force_v5 &&
           getenv("DP_PEEL_V5") == nullptr;
   if (st.v6) {
@@ -1633,6 +1646,7 @@ void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st, 
     st.counters.alloc(ctx, 3);
     st.counters.zero();
     DP_CUDA(cudaMemcpyAsync(st.counters.p + 2, nsrc_p, sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+    fixpoint();
     return;
   }
   st.gstack.alloc(ctx, (size_t)n + 1);
@@ -1658,6 +1672,7 @@ void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st, 
   st.counters.alloc(ctx, 3);
   st.counters.zero();
   DP_CUDA(cudaMemcpyAsync(st.counters.p + 2, nsrc_p, sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+  fixpoint();
 }
 
 static PeelArgs peel_args(DevGraph& g, PeelState& st, int32_t* seq, int32_t* pos_of, bool progress) {
@@ -1686,11 +1701,12 @@ static PeelArgs peel_args(DevGraph& g, PeelState& st, int32_t* seq, int32_t* pos
   a.gsid = st.gsid.p;
   a.gover = st.gover.p;
   a.prefetch = getenv("DP_PEEL_NO_PREFETCH") == nullptr;
+  a.skip = st.skip.p;
   return a;
 }
 
 std::vector<int32_t> topo_order_batch(DevGraph* const* gs, int count, int policy, const int64_t* const* cpath,
-                                      int32_t* const* seq, int32_t* const* pos_of) {
+                                      int32_t* const* seq, int32_t* const* pos_of, bool tree) {
   std::vector<int32_t> emitted(count, 0);
   if (count == 0) return emitted;
   dp_ctx* ctx = gs[0]->ctx;
@@ -1706,7 +1722,7 @@ std::vector<int32_t> topo_order_batch(DevGraph* const* gs, int count, int policy
   for (int i = 0; i < count; ++i) {
     if (gs[i]->n == 0) continue;
     st[i].reset(new PeelState);
-    peel_prepare(*gs[i], policy, cpath[i], *st[i]);
+    peel_prepare(*gs[i], policy, cpath[i], *st[i], false, seq[i], pos_of[i], tree);
     live.push_back(i);
     bytes += 72.0 * gs[i]->n + 8.0 * gs[i]->m_ok;
   }
@@ -1765,7 +1781,7 @@ PeelDpJob* peel_dp_prepare(DevGraph& g, const int64_t* cpath, int32_t range, int
   DP_LAUNCH(ctx, k_max_abs, grid_for(n, 256), 256, 0, j->out_sum.p, n, j->mx.p);
   DP_LAUNCH(ctx, k_max_abs, grid_for(g.m_ok, 256), 256, 0, g.out_cost.p, g.m_ok, j->mx.p);
   // the peel's preparation is enqueued before the one host round trip of this function
-  peel_prepare(g, DP_TOPO_CPD, cpath, j->st);
+  peel_prepare(g, DP_TOPO_CPD, cpath, j->st, false, seq, pos_of);
   const unsigned long long max_out = scalar_to_host(ctx, j->mx.p);
   DpArgs& da = j->da;
   da.keys32 = static_cast<double>(max_out) * (range + 2) < static_cast<double>(1 << 21);

@@ -19,9 +19,13 @@ struct PeelState {
   DevBuf<int2> cmeta;
   DevBuf<int32_t> gsid;
   DevBuf<int32_t> gover;
+  DevBuf<int> skip;  // set by the fixed-point peel on convergence
 };
 
-void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st, bool force_v5 = false);
+// seq/pos_of given (stack policies) and tree: the tree peel (fixpoint.cu) is enqueued here
+// and, when its proof holds, the peel kernel only checks the skip flag.
+void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st, bool force_v5 = false,
+                  int32_t* seq = nullptr, int32_t* pos_of = nullptr, bool tree = true);
 
 // CPD peel of g streamed into the breakpoint DP (R <= 256); writes seq/pos_of and
 // prev_cut[1..n]; *first_exceed = first position whose node exceeds `limit` (or

@@ -142,7 +142,7 @@ void generate_windows(Resident* const* rs, int count) {
     cseq[i] = r.cseq.p;
     cpos[i] = r.cpos.p;
   }
-  topo_order_batch(cg.data(), count, DP_TOPO_CPD, cpath.data(), cseq.data(), cpos.data());
+  topo_order_batch(cg.data(), count, DP_TOPO_CPD, cpath.data(), cseq.data(), cpos.data(), false);
   std::vector<std::unique_ptr<PlaceHandle>> ph;
   std::vector<PlaceJob*> pj;
   for (int i = 0; i < count; ++i) {

@@ -4,6 +4,8 @@ restatement (oracle/dp_oracle.c).
 
   peel v6        in-degree >= 127 (global counters), out-degree > 8 (CSR rows), full
                  hash buckets (global spill counters), DFS as well as CPD ranks
+                 (the tree peel of fixpoint.cu is switched off where the one-warp peel's
+                 path is the point; test_gpu_fixpoint.py covers the tree peel)
   streamed DP    v3 (R <= 225), 32-step blocks (226..256), per-step 32-bit keys (cost
                  bound), 64-bit keys (large costs), R = 1 / 32 / 33 block edges
   levels         index-order sweep (n <= 16384, index order topological) vs the Kahn
@@ -47,17 +49,23 @@ def _orders(gpu, oracle, g):
         same(x, y, nm)
 
 
-def test_peel_high_indegree(gpu, oracle):
+@pytest.fixture
+def warp_peel(monkeypatch):
+    """The one-warp peel's special paths are the point: no tree peel first."""
+    monkeypatch.setenv("DP_PEEL_NO_FIXPOINT", "1")
+
+
+def test_peel_high_indegree(gpu, oracle, warp_peel):
     _orders(gpu, oracle, _fanin_hub())
 
 
-def test_peel_long_rows(gpu, oracle):
+def test_peel_long_rows(gpu, oracle, warp_peel):
     # fan-out up to 30 from the previous layer: many rows longer than 8
     g = layered(9, 6000, 60, fan_lo=6, fan_hi=30)
     _orders(gpu, oracle, g)
 
 
-def test_peel_bucket_spill(gpu, oracle):
+def test_peel_bucket_spill(gpu, oracle, warp_peel):
     # a 40k-wide layer keeps tens of thousands of nodes open: buckets overflow to HBM
     g = layered(13, 120000, 40000, fan_lo=2, fan_hi=5)
     _orders(gpu, oracle, g)
@@ -147,6 +155,7 @@ def test_shared_sm_mode(gpu, oracle, monkeypatch, case):
     """The one-SM-per-graph peel + DP kernel used by batched calls (k_peel_dp_shared:
     8,192 hash buckets, 1,024 staged in-edges per chunk), forced for single graphs."""
     monkeypatch.setenv("DP_PEEL_DP_SHARED", "1")
+    monkeypatch.setenv("DP_PEEL_NO_FIXPOINT", "1")
     if case == "spill":
         g, r = layered(13, 120000, 40000, fan_lo=2, fan_hi=5), 200
     elif case == "hub":
