@@ -40,33 +40,6 @@ namespace dpb {
 namespace {
 
 constexpr int kTreeThreads = 1024;
-constexpr int kTreeBatch = 8;
-
-struct TreeArgs {
-  int32_t n;
-  const int32_t* nsrc;  // device: number of sources
-  const int32_t* in_off;
-  const int32_t* in_src;
-  const int32_t* out_off;
-  const int32_t* rowc;   // CSR children, each row sorted by rank (best first)
-  const int32_t* roots;  // sources by rank
-  int32_t* seq0;         // breadth-first order s0 (level-major)
-  int32_t* best;         // s0 position of the T0 parent
-  int32_t* indeg;
-  int32_t* size;
-  int32_t* pre;          // preorder positions
-  int32_t* pre2;         // general rounds: second buffer
-  int32_t* par;          // general rounds: T(s) parent
-  int32_t* lvl_off;      // [n + 1]
-  int32_t max_levels;    // more levels than this: give up (chain-like graph)
-  int32_t max_rounds;    // general rounds after a failed proof (-1: from the cost model)
-  int32_t* seq;
-  int32_t* pos_of;
-  int* skip;
-  int* progress;
-  int* emitted;
-  int* info;             // [0] status (1 ok, 2 too deep, 3 not a DAG, 4 budget), [1] levels, [2] rounds
-};
 
 struct TreeBatch {
   TreeArgs a[kTreeBatch];
@@ -362,63 +335,59 @@ __global__ void k_roots(const int32_t* by_rank, const int32_t* flag, const int32
 
 }  // namespace
 
-struct TreeJob {
-  DevBuf<int32_t> rowc, roots, seq0, best, indeg, size, pre, pre2, par, lvl_off;
-  DevBuf<int> info;
-};
-
 bool fixpoint_wanted(const DevGraph& g) {
   if (getenv("DP_PEEL_NO_FIXPOINT")) return false;
   return g.n >= (getenv("DP_PEEL_FIXPOINT") ? 1 : 2048) && g.m_ok > 0;
 }
 
-void fixpoint_launch(DevGraph& g, const int32_t* by_rank, const int32_t* rank, const int32_t* flag,
-                     const int32_t* fpos, int32_t* seq, int32_t* pos_of, int* skip, int* progress, int* emitted) {
+std::unique_ptr<TreeJob> fixpoint_prepare(DevGraph& g, const int32_t* by_rank, const int32_t* rank,
+                                          const int32_t* flag, const int32_t* fpos, int32_t* seq, int32_t* pos_of,
+                                          int* skip, int* progress, int* emitted) {
   dp_ctx* ctx = g.ctx;
   const int B = 256;
   const int32_t n = g.n, m = g.m_ok;
-  TreeJob j;
-  j.rowc.alloc(ctx, m > 0 ? m : 1);
+  std::unique_ptr<TreeJob> j(new TreeJob);
+  j->ctx = ctx;
+  j->rowc.alloc(ctx, m > 0 ? m : 1);
   DevBuf<int> flags(ctx, 1);
   flags.zero();
-  DP_LAUNCH(ctx, k_rows_by_rank, grid_for(n, B), B, 0, g.out_off.p, g.out_dst.p, rank, n, j.rowc.p, flags.p);
+  DP_LAUNCH(ctx, k_rows_by_rank, grid_for(n, B), B, 0, g.out_off.p, g.out_dst.p, rank, n, j->rowc.p, flags.p);
   if (g.big_rows && scalar_to_host(ctx, flags.p)) {  // some row > 64: one global sort of (row, rank)
     DevBuf<uint64_t> keys(ctx, m), keys_out(ctx, m);
     DevBuf<int32_t> vals(ctx, m);
     DP_LAUNCH(ctx, k_row_rank_keys, grid_for(n, B), B, 0, g.out_off.p, g.out_dst.p, rank, n, keys.p, vals.p);
     int bits = 1;
     while ((1ll << bits) < n) ++bits;
-    sort_pairs_u64(ctx, keys.p, keys_out.p, vals.p, j.rowc.p, m, 0, 32 + bits);
+    sort_pairs_u64(ctx, keys.p, keys_out.p, vals.p, j->rowc.p, m, 0, 32 + bits);
   }
-  j.roots.alloc(ctx, n);
-  DP_LAUNCH(ctx, k_roots, grid_for(n, B), B, 0, by_rank, flag, fpos, n, j.roots.p);
-  j.seq0.alloc(ctx, n);
-  j.best.alloc(ctx, n);
-  j.indeg.alloc(ctx, n);
-  j.size.alloc(ctx, n);
-  j.pre.alloc(ctx, n);
-  j.pre2.alloc(ctx, n);
-  j.par.alloc(ctx, n);
-  j.lvl_off.alloc(ctx, (size_t)n + 1);
-  j.info.alloc(ctx, 3);
-  j.info.zero();
-  TreeBatch b{};
-  TreeArgs& a = b.a[0];
+  j->roots.alloc(ctx, n);
+  DP_LAUNCH(ctx, k_roots, grid_for(n, B), B, 0, by_rank, flag, fpos, n, j->roots.p);
+  j->seq0.alloc(ctx, n);
+  j->best.alloc(ctx, n);
+  j->indeg.alloc(ctx, n);
+  j->size.alloc(ctx, n);
+  j->pre.alloc(ctx, n);
+  j->pre2.alloc(ctx, n);
+  j->par.alloc(ctx, n);
+  j->lvl_off.alloc(ctx, (size_t)n + 1);
+  j->info.alloc(ctx, 3);
+  j->info.zero();
+  TreeArgs& a = j->a;
   a.n = n;
   a.nsrc = fpos + n;
   a.in_off = g.in_off.p;
   a.in_src = g.in_src.p;
   a.out_off = g.out_off.p;
-  a.rowc = j.rowc.p;
-  a.roots = j.roots.p;
-  a.seq0 = j.seq0.p;
-  a.best = j.best.p;
-  a.indeg = j.indeg.p;
-  a.size = j.size.p;
-  a.pre = j.pre.p;
-  a.pre2 = j.pre2.p;
-  a.par = j.par.p;
-  a.lvl_off = j.lvl_off.p;
+  a.rowc = j->rowc.p;
+  a.roots = j->roots.p;
+  a.seq0 = j->seq0.p;
+  a.best = j->best.p;
+  a.indeg = j->indeg.p;
+  a.size = j->size.p;
+  a.pre = j->pre.p;
+  a.pre2 = j->pre2.p;
+  a.par = j->par.p;
+  a.lvl_off = j->lvl_off.p;
   // ~8 us per level (all phases) against ~0.4 us per node for the one-warp peel
   a.max_levels = getenv("DP_PEEL_FIXPOINT") ? n + 1 : std::max(64, n / 40);
   a.max_rounds = getenv("DP_PEEL_FIXPOINT") ? 4096 : -1;
@@ -428,18 +397,33 @@ void fixpoint_launch(DevGraph& g, const int32_t* by_rank, const int32_t* rank, c
   a.skip = skip;
   a.progress = progress;
   a.emitted = emitted;
-  a.info = j.info.p;
-  {
-    StageScope s(ctx, "peel (tree)", 40.0 * n + 20.0 * m);
-    DP_LAUNCH(ctx, k_treepeel, 1, kTreeThreads, 0, b);
+  a.info = j->info.p;
+  j->bytes = 40.0 * n + 20.0 * m;
+  return j;
+}
+
+void fixpoint_launch_batch(dp_ctx* ctx, TreeJob* const* jobs, int count) {
+  for (int b0 = 0; b0 < count; b0 += kTreeBatch) {
+    const int k = std::min(kTreeBatch, count - b0);
+    TreeBatch b{};
+    double bytes = 0.0;
+    for (int q = 0; q < k; ++q) {
+      b.a[q] = jobs[b0 + q]->a;
+      bytes += jobs[b0 + q]->bytes;
+    }
+    StageScope s(ctx, "peel (tree)", bytes);
+    DP_LAUNCH(ctx, k_treepeel, k, kTreeThreads, 0, b);
   }
   if (getenv("DP_DEBUG_FIXPOINT")) {
-    int h[3];
-    j.info.download(h, 3);
+    std::vector<int> h(3 * (size_t)count);
+    for (int q = 0; q < count; ++q) jobs[q]->info.download(h.data() + 3 * q, 3);
     sync(ctx);
-    fprintf(stderr, "[treepeel] n=%d status=%d levels=%d rounds=%d\n", n, h[0], h[1], h[2]);
-    const int slot = h[0] == 1 ? (h[2] == 1 ? 0 : 1) : h[0];
-    if (slot >= 0 && slot < 5) ++ctx->tree_stats[slot];
+    for (int q = 0; q < count; ++q) {
+      fprintf(stderr, "[treepeel] n=%d status=%d levels=%d rounds=%d\n", jobs[q]->a.n, h[3 * q], h[3 * q + 1],
+              h[3 * q + 2]);
+      const int slot = h[3 * q] == 1 ? (h[3 * q + 2] == 1 ? 0 : 1) : h[3 * q];
+      if (slot >= 0 && slot < 5) ++ctx->tree_stats[slot];
+    }
   }
 }
 

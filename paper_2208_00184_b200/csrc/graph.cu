@@ -447,9 +447,15 @@ __global__ void __launch_bounds__(1024) k_levels_seq(const __grid_constant__ Seq
     const int32_t e1 = rev ? off[n - done] : off[hi];
     const bool fits = e1 - e0 <= kSeqTile;
     if (fits) {
+      // a source swept before this tile has its value already: stage f[u] + c with en = -1,
+      // so the walk only chains through in-tile sources (en = u, ec = c)
       for (int32_t k = threadIdx.x; k < e1 - e0; k += blockDim.x) {
-        en[k] = nbr[e0 + k];
-        ec[k] = cost[e0 + k];
+        const int32_t u = nbr[e0 + k];
+        const int64_t c = cost[e0 + k];
+        const int32_t pu = rev ? n - 1 - u : u;
+        const bool before = pu < done;
+        en[k] = before ? -1 : u;
+        ec[k] = before ? (done - pu <= kSeqMaxN ? val[pu & (kSeqMaxN - 1)] : __ldcg(gval + u)) + c : c;
       }
     }
     for (int32_t i = done + threadIdx.x; i <= hi; i += blockDim.x) {
@@ -469,10 +475,20 @@ __global__ void __launch_bounds__(1024) k_levels_seq(const __grid_constant__ Seq
         int64_t mx = 0;
         for (int32_t k = b + lane; k < e; k += 32) {
           const int32_t u = fits ? en[k - e0] : nbr[k];
-          const int64_t c = fits ? ec[k - e0] : cost[k];
-          const int32_t pu = rev ? n - 1 - u : u;  // sweep position of u (< i)
-          const int64_t fu = i - pu <= kSeqMaxN ? val[pu & (kSeqMaxN - 1)] : __ldcg(gval + u);
-          mx = max(mx, fu + c);
+          if (fits) {
+            const int64_t x = ec[k - e0];
+            if (u < 0) {
+              mx = max(mx, x);
+            } else {
+              const int32_t pu = rev ? n - 1 - u : u;  // in this tile: the ring holds it
+              mx = max(mx, val[pu & (kSeqMaxN - 1)] + x);
+            }
+          } else {
+            const int64_t c = cost[k];
+            const int32_t pu = rev ? n - 1 - u : u;  // sweep position of u (< i)
+            const int64_t fu = i - pu <= kSeqMaxN ? val[pu & (kSeqMaxN - 1)] : __ldcg(gval + u);
+            mx = max(mx, fu + c);
+          }
         }
         mx = warp_max_nonneg(mx);
         if (lane == 0) {

@@ -1239,8 +1239,8 @@ __device__ void dp_stage(const DpArgs& a, DpBuf<E2>& B, int32_t j0, int32_t cnt,
   }
 }
 
-template <int E2>
-__device__ void dp_producer(const DpArgs& a, DpSmem3<E2>& S, int k, int lane) {
+template <typename SmemT>
+__device__ void dp_producer(const DpArgs& a, SmemT& S, int k, int lane) {
   int avail = 0;
   for (int32_t c = k;; c += kDpProducers) {
     const int32_t j0 = c * kCh;
@@ -1375,6 +1375,181 @@ __device__ void dp_compute_v3(const DpArgs& a, DpSmem3<E2>& S) {
   }
 }
 
+// ---------------------------------------------------------------- DP v4 (order known)
+// The v3 recurrence with its eight candidate rows spread over kDp4Warps = 8 compute warps,
+// for graphs whose order is complete before the DP starts (tree peel, fixpoint.cu).  Rows
+// live in a ring of slots, one per warp: in block b (32 positions) slot b & 7 holds the
+// block's own candidates and slot s the old row r = (s - b - 1) & 7, so the v3 register
+// rotation becomes "+32 on every key" in each warp (the tie byte of a fixed candidate
+// grows by 32 per block) with no data moving between warps.  Per step every warp applies
+// the step's in-window in-edges to its slot and stores its per-lane minimum; per block each
+// warp reduces its 32 x 32 minima (lane = step), one warp runs v3's 31-step chain over the
+// block's own candidates, and the new slot takes the chain's values.  Bit-identical to v3.
+constexpr int kDp4Warps = 8;
+template <int E2>
+struct DpSmem4 {
+  DpBuf<E2> buf[kDpProducers];
+  int32_t mt[kDp4Warps][32][33];
+  int32_t ct[32][33];
+  int32_t rw[kDp4Warps][32];
+  int32_t bk[32];
+  int32_t bvr;
+  int ready[kDpProducers];
+  int consumed;
+};
+
+__device__ __forceinline__ void dp4_sync() { asm volatile("bar.sync 2, %0;" ::"r"(kDp4Warps * 32) : "memory"); }
+
+template <int E2>
+__device__ void dp_compute_v4(const DpArgs& a, DpSmem4<E2>& S, int w) {
+  const int lane = threadIdx.x & 31;
+  const int32_t n = a.n;
+  constexpr int32_t kUnfilled = 0x3f000000;
+  int32_t K = kUnfilled;
+  long long wait_cycles = 0;
+  const long long t_start = clock64();
+  if (w == 0 && lane == 0) S.bvr = 0;
+  dp4_sync();
+  int32_t blk = 0;
+  for (int32_t c = 0;; ++c) {
+    const int32_t j0 = c * kCh;
+    if (j0 >= n) break;
+    const int kb = c % kDpProducers;
+    const long long tw0 = clock64();
+    while (ld_volatile_shared(&S.ready[kb]) != c) __nanosleep(32);
+    wait_cycles += clock64() - tw0;
+    __threadfence_block();
+    const DpBuf<E2>& B = S.buf[kb];
+    const int32_t cnt = B.cnt;
+    const bool staged = B.n2 <= E2;
+    for (int32_t tb = 0; tb < cnt; tb += 32, ++blk) {
+      const int32_t P = j0 + tb;
+      const int32_t nb = min(32, cnt - tb);
+      const int32_t r = (w - blk - 1) & 7;  // 7: this block's own candidates
+      const int32_t c0 = 224 - P - lane;
+      const int32_t kn_lim = -P - lane;
+      const int32_t bvr = S.bvr;
+      // lane u loads step u's inputs (first two in-window in-edges, the number of further
+      // ones, lo); the step loop takes them by shuffle, so no load sits on its critical path
+      int32_t X0 = 0, S0 = 0, X1 = 0, S1 = 0, LO = 0, EB = 0, EX = 0;
+      if (lane < nb) {
+        const int32_t t = tb + lane;
+        LO = B.lo[t];
+        if (staged) {
+          const int32_t eb = B.off2[t], ee = B.off2[t + 1];
+          const int2 x0 = B.e2[eb], x1 = B.e2[eb + 1];
+          X0 = x0.x;
+          S0 = eb < ee ? x0.y : 0;
+          X1 = x1.x;
+          S1 = eb + 1 < ee ? x1.y : 0;
+          EB = eb + 2;
+          EX = max(0, ee - eb - 2);
+        }
+      }
+      const bool extra = !staged || __any_sync(FULL, EX > 0);
+      if (r == 7) {
+#pragma unroll 8
+        for (int32_t u = 0; u < nb; ++u) {
+          const int32_t x0 = __shfl_sync(FULL, X0, u), s0 = __shfl_sync(FULL, S0, u);
+          const int32_t x1 = __shfl_sync(FULL, X1, u), s1 = __shfl_sync(FULL, S1, u);
+          const int32_t lo = __shfl_sync(FULL, LO, u);
+          if (lane == u) K = (u == 0 ? bvr * 256 : 0) + 31 - u;
+          K -= (x0 + kn_lim >= 0 ? s0 : 0) + (x1 + kn_lim >= 0 ? s1 : 0);
+          if (extra) {
+            const int32_t t = tb + u;
+            if (staged) {
+              const int32_t eb = __shfl_sync(FULL, EB, u), ex = __shfl_sync(FULL, EX, u);
+              for (int32_t e = eb; e < eb + ex; ++e) {
+                const int2 x = B.e2[e];
+                K -= x.x + kn_lim >= 0 ? x.y : 0;
+              }
+            } else {
+              const int32_t eb = B.off[t], ee = B.off[t + 1];
+              for (int32_t e = eb; e < ee; ++e) {
+                const int32_t k = B.ioff[t] + (e - eb);
+                const int32_t av = a.pos_of[a.in_src[k]];
+                if (av < P - 224) continue;
+                K -= av + kn_lim >= 0 ? static_cast<int32_t>(a.in_cost[k]) << 8 : 0;
+              }
+            }
+          }
+          S.mt[w][u][lane] = (lane == 0 && P >= lo) ? K : INT32_MAX;
+          if (lane >= 1 && lane <= u) S.ct[u][lane] = K;
+        }
+      } else {
+#pragma unroll 8
+        for (int32_t u = 0; u < nb; ++u) {
+          const int32_t x0 = __shfl_sync(FULL, X0, u), s0 = __shfl_sync(FULL, S0, u);
+          const int32_t x1 = __shfl_sync(FULL, X1, u), s1 = __shfl_sync(FULL, S1, u);
+          const int32_t lo = __shfl_sync(FULL, LO, u);
+          K -= (r <= (x0 + c0) >> 5 ? s0 : 0) + (r <= (x1 + c0) >> 5 ? s1 : 0);
+          if (extra) {
+            const int32_t t = tb + u;
+            if (staged) {
+              const int32_t eb = __shfl_sync(FULL, EB, u), ex = __shfl_sync(FULL, EX, u);
+              for (int32_t e = eb; e < eb + ex; ++e) {
+                const int2 x = B.e2[e];
+                K -= r <= (x.x + c0) >> 5 ? x.y : 0;
+              }
+            } else {
+              const int32_t eb = B.off[t], ee = B.off[t + 1];
+              for (int32_t e = eb; e < ee; ++e) {
+                const int32_t k = B.ioff[t] + (e - eb);
+                const int32_t av = a.pos_of[a.in_src[k]];
+                if (av < P - 224) continue;
+                K -= r <= (av + c0) >> 5 ? static_cast<int32_t>(a.in_cost[k]) << 8 : 0;
+              }
+            }
+          }
+          const int32_t rmin = (lo + c0 + 31) >> 5;
+          S.mt[w][u][lane] = r >= rmin ? K : INT32_MAX;
+        }
+      }
+      __syncwarp();
+      if (lane < nb) {
+        int32_t r4[4] = {INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX};
+#pragma unroll
+        for (int q = 0; q < 32; ++q) r4[q & 3] = min(r4[q & 3], S.mt[w][lane][q]);
+        S.rw[w][lane] = min(min(r4[0], r4[1]), min(r4[2], r4[3]));
+      }
+      dp4_sync();
+      if (w == 0) {  // the chain over the block's own candidates (v3 phase B)
+        int32_t R = INT32_MAX, kmin = 0;
+        if (lane < nb) {
+#pragma unroll
+          for (int q = 0; q < kDp4Warps; ++q) R = min(R, S.rw[q][lane]);
+          kmin = B.lo[tb + lane] - P;
+        }
+        for (int k = 1; k < nb; ++k) {
+          const int32_t b = __shfl_sync(FULL, R, k - 1) >> 8;
+          const int32_t cc = S.ct[lane][k];
+          if (lane >= k && k >= kmin) R = min(R, cc + b * 256);
+        }
+        if (lane < nb) a.prev_cut[P + lane + 1] = P + 31 - (R & 255);
+        S.bk[lane] = __shfl_up_sync(FULL, R, 1) >> 8;
+        const int32_t nb_bvr = __shfl_sync(FULL, R, nb - 1) >> 8;
+        if (lane == 0) S.bvr = nb_bvr;
+      }
+      dp4_sync();
+      if (r == 7 && lane >= 1) K += S.bk[lane] * 256;
+      K += 32;
+      const int32_t nbvr = S.bvr;
+      if (nbvr > (1 << 20) || nbvr < -(1 << 20)) {
+        if (K < kUnfilled) K -= nbvr * 256;
+        dp4_sync();
+        if (w == 0 && lane == 0) S.bvr = 0;
+      }
+      dp4_sync();
+    }
+    if (w == 0 && lane == 0) *reinterpret_cast<volatile int*>(&S.consumed) = c + 1;
+  }
+  if (w == 0 && lane == 0 && a.debug) {
+    a.debug[0] = clock64() - t_start;
+    a.debug[1] = wait_cycles;
+    a.debug[2] = 0;
+  }
+}
+
 // Up to kPeelDpBatch independent graphs per launch.  Shared mode (k_peel_dp_shared): one
 // CTA per graph — warp 0 peels, warp 1 runs the DP recurrence, warps 2, 3, 5 stage DP
 // chunks (warp 4 exits at once so that the peel warp keeps its SM sub-partition: warps map
@@ -1443,6 +1618,23 @@ __global__ void __launch_bounds__(kPeelDpExclusive, 1) k_peel_dp_shared(const __
   } else if (da.v3 && warp != 4) {
     dp_producer(da, S, warp == 5 ? 2 : warp - 2, threadIdx.x & 31);
   }
+}
+
+// DP v4 alone on a finished order (tree peel): one CTA per graph, kDp4Warps compute warps
+// and kDpProducers staging warps.
+constexpr int kDp4Threads = (kDp4Warps + kDpProducers) * 32;
+constexpr size_t kSmemDp4 = sizeof(DpSmem4<kE2Cap>);
+static_assert(kSmemDp4 <= 227 * 1024, "DP v4 shared memory exceeds one SM");
+__global__ void __launch_bounds__(kDp4Threads, 1) k_dp_only(const __grid_constant__ PeelDpBatch b) {
+  extern __shared__ int4 smem4[];
+  const DpArgs& da = b.da[blockIdx.x];
+  DpSmem4<kE2Cap>& S = *reinterpret_cast<DpSmem4<kE2Cap>*>(smem4);
+  if (threadIdx.x < kDpProducers) S.ready[threadIdx.x] = -1;
+  if (threadIdx.x == 0) S.consumed = 0;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5;
+  if (warp < kDp4Warps) dp_compute_v4(da, S, warp);
+  else dp_producer(da, S, warp - kDp4Warps, threadIdx.x & 31);
 }
 
 __global__ void k_slot16(const int32_t* out_off, const int32_t* out_dst, const int32_t* rank, int32_t m, int4* slot) {
@@ -1595,84 +1787,118 @@ size_t peel_smem() { return kPeelRegion; }  // k_peel2 (topo_order)
 }  // namespace
 
 // Builds the peel inputs (ranks, 16-byte slot records, initial stack, in-degrees).
-void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st, bool force_v5, int32_t* seq,
-                  int32_t* pos_of, bool tree) {
+// Ranks, source flags and the peel counters; the tree peel's job when wanted (launched by
+// the caller together with other graphs' jobs: tree_run).
+void peel_prepare_begin(DevGraph& g, int policy, const int64_t* cpath, PeelState& st, int32_t* seq,
+                        int32_t* pos_of, bool tree) {
   dp_ctx* ctx = g.ctx;
   const int B = 256;
-  const int32_t n = g.n, m = g.m_ok;
+  const int32_t n = g.n;
   DevBuf<int32_t> by_id;
   node_order_by_id(g, by_id);
-  DevBuf<int32_t> by_rank(ctx, n), rank(ctx, n);
+  st.by_rank.alloc(ctx, n);
+  st.rank.alloc(ctx, n);
   if (policy == DP_TOPO_CPD) {
     DevBuf<uint64_t> keys(ctx, n), keys_out(ctx, n);
     DevBuf<int32_t> vals(ctx, n);
     DP_LAUNCH(ctx, k_rank_keys2, grid_for(n, B), B, 0, cpath, by_id.p, n, keys.p, vals.p);
-    sort_pairs_u64(ctx, keys.p, keys_out.p, vals.p, by_rank.p, n, 0, 64);
+    sort_pairs_u64(ctx, keys.p, keys_out.p, vals.p, st.by_rank.p, n, 0, 64);
   } else {
-    DP_CUDA(cudaMemcpyAsync(by_rank.p, by_id.p, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    DP_CUDA(cudaMemcpyAsync(st.by_rank.p, by_id.p, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
   }
-  DP_LAUNCH(ctx, k_rank_of2, grid_for(n, B), B, 0, by_rank.p, n, rank.p);
-  DevBuf<int32_t> flag(ctx, (size_t)n + 1), fpos(ctx, (size_t)n + 1);
-  flag.zero();
-  DP_LAUNCH(ctx, k_src_flags2, grid_for(n, B), B, 0, by_rank.p, g.in_off.p, n, flag.p);
-  exclusive_scan_i32(ctx, flag.p, fpos.p, (int64_t)n + 1);
-  const int32_t* nsrc_p = fpos.p + n;  // the scan's total: read on the device
+  DP_LAUNCH(ctx, k_rank_of2, grid_for(n, B), B, 0, st.by_rank.p, n, st.rank.p);
+  st.flag.alloc(ctx, (size_t)n + 1);
+  st.fpos.alloc(ctx, (size_t)n + 1);
+  st.flag.zero();
+  DP_LAUNCH(ctx, k_src_flags2, grid_for(n, B), B, 0, st.by_rank.p, g.in_off.p, n, st.flag.p);
+  exclusive_scan_i32(ctx, st.flag.p, st.fpos.p, (int64_t)n + 1);
   st.stack_mode = policy != DP_TOPO_M;
-  // shallow graphs: the fixed-point peel runs first (after the counters are reset below)
-  // and, when it converges, the one-warp peel exits at once
-  const bool fix = st.stack_mode && seq != nullptr && tree && fixpoint_wanted(g);
-  auto fixpoint = [&] {
-    if (!fix) return;
+  st.counters.alloc(ctx, 3);
+  st.counters.zero();
+  // the number of sources (the scan's total) stays on the device
+  DP_CUDA(cudaMemcpyAsync(st.counters.p + 2, st.fpos.p + n, sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+  st.tree.reset();
+  st.tree_ok = false;
+  if (st.stack_mode && seq != nullptr && tree && fixpoint_wanted(g)) {
     st.skip.alloc(ctx, 1);
     st.skip.zero();
-    fixpoint_launch(g, by_rank.p, rank.p, flag.p, fpos.p, seq, pos_of, st.skip.p, st.counters.p, st.counters.p + 1);
-  };
+    st.tree = fixpoint_prepare(g, st.by_rank.p, st.rank.p, st.flag.p, st.fpos.p, seq, pos_of, st.skip.p,
+                               st.counters.p, st.counters.p + 1);
+  }
+}
+
+// The one-warp peel's inputs (v6 / v5 / FIFO layouts).
+void peel_prepare_end(DevGraph& g, PeelState& st, bool force_v5) {
+  dp_ctx* ctx = g.ctx;
+  const int B = 256;
+  const int32_t n = g.n, m = g.m_ok;
+  const int32_t* nsrc_p = st.fpos.p + n;
+  const int32_t* by_rank = st.by_rank.p;
+  const int32_t* rank = st.rank.p;
   st.v6 = st.stack_mode && n < (1 << 24) && static_cast<int64_t>(m) <= 6 * static_cast<int64_t>(n) && !force_v5 &&
           getenv("DP_PEEL_V5") == nullptr;
   if (st.v6) {
     st.ell6.alloc(ctx, (size_t)n * 4);
-    DP_LAUNCH(ctx, k_ell6, grid_for(n, B), B, 0, g.in_off.p, g.out_off.p, g.out_dst.p, rank.p, n,
+    DP_LAUNCH(ctx, k_ell6, grid_for(n, B), B, 0, g.in_off.p, g.out_off.p, g.out_dst.p, rank, n,
               reinterpret_cast<int2*>(st.ell6.p));
     st.cmeta.alloc(ctx, m > 0 ? m : 1);
-    DP_LAUNCH(ctx, k_cmeta, grid_for(m, B), B, 0, g.in_off.p, g.out_off.p, g.out_dst.p, rank.p, m, st.cmeta.p);
+    DP_LAUNCH(ctx, k_cmeta, grid_for(m, B), B, 0, g.in_off.p, g.out_off.p, g.out_dst.p, rank, m, st.cmeta.p);
     st.gsid.alloc(ctx, (size_t)n + 1);
-    DP_LAUNCH(ctx, k_src_place_v6, grid_for(n, B), B, 0, by_rank.p, flag.p, fpos.p, g.out_off.p, n, nsrc_p,
+    DP_LAUNCH(ctx, k_src_place_v6, grid_for(n, B), B, 0, by_rank, st.flag.p, st.fpos.p, g.out_off.p, n, nsrc_p,
               st.gsid.p);
     st.indeg.alloc(ctx, n);
     DP_LAUNCH(ctx, k_indeg_init2, grid_for(n, B), B, 0, g.in_off.p, n, st.indeg.p);
     st.gover.alloc(ctx, n);
     st.gover.zero();
     st.spill.alloc(ctx, m > 0 ? m : 1);
-    st.counters.alloc(ctx, 3);
-    st.counters.zero();
-    DP_CUDA(cudaMemcpyAsync(st.counters.p + 2, nsrc_p, sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
-    fixpoint();
     return;
   }
   st.gstack.alloc(ctx, (size_t)n + 1);
   if (st.stack_mode && n < (1 << 24)) {
     st.ellw = n > 262144 ? 8 : 32;
     st.nr2.alloc(ctx, n);
-    DP_LAUNCH(ctx, k_node_rec2, grid_for(n, B), B, 0, g.in_off.p, g.out_off.p, rank.p, n, st.nr2.p);
+    DP_LAUNCH(ctx, k_node_rec2, grid_for(n, B), B, 0, g.in_off.p, g.out_off.p, rank, n, st.nr2.p);
     st.ell.alloc(ctx, (size_t)n * st.ellw);
     DP_LAUNCH(ctx, k_ell, grid_for((int64_t)n * st.ellw, B), B, 0, g.out_off.p, g.out_dst.p, n, st.ellw, st.ell.p);
     st.gstack2.alloc(ctx, (size_t)n + 1);
-    DP_LAUNCH(ctx, k_src_place_v5, grid_for(n, B), B, 0, by_rank.p, flag.p, fpos.p, g.out_off.p, n, nsrc_p,
+    DP_LAUNCH(ctx, k_src_place_v5, grid_for(n, B), B, 0, by_rank, st.flag.p, st.fpos.p, g.out_off.p, n, nsrc_p,
               st.gstack2.p);
   } else {
     if (st.stack_mode) fail(DP_E_UNSUPPORTED, "graphs with 2^24 or more nodes are not supported by the peel");
-    DP_LAUNCH(ctx, k_src_place2, grid_for(n, B), B, 0, by_rank.p, flag.p, fpos.p, g.out_off.p, n, nsrc_p,
+    DP_LAUNCH(ctx, k_src_place2, grid_for(n, B), B, 0, by_rank, st.flag.p, st.fpos.p, g.out_off.p, n, nsrc_p,
               st.stack_mode, st.gstack.p);
     st.indeg.alloc(ctx, n);
     DP_LAUNCH(ctx, k_indeg_init2, grid_for(n, B), B, 0, g.in_off.p, n, st.indeg.p);
     st.slot.alloc(ctx, m > 0 ? m : 1);
-    DP_LAUNCH(ctx, k_slot16, grid_for(m, B), B, 0, g.out_off.p, g.out_dst.p, rank.p, m, st.slot.p);
+    DP_LAUNCH(ctx, k_slot16, grid_for(m, B), B, 0, g.out_off.p, g.out_dst.p, rank, m, st.slot.p);
   }
   st.spill.alloc(ctx, m > 0 ? m : 1);
-  st.counters.alloc(ctx, 3);
-  st.counters.zero();
-  DP_CUDA(cudaMemcpyAsync(st.counters.p + 2, nsrc_p, sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
-  fixpoint();
+}
+
+void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st, bool force_v5) {
+  peel_prepare_begin(g, policy, cpath, st, nullptr, nullptr, false);
+  peel_prepare_end(g, st, force_v5);
+}
+
+// Launches the tree peels of states that have one (one launch per kTreeBatch graphs), waits,
+// and records which proofs held (PeelState::tree_ok); one host round trip.
+void tree_run(dp_ctx* ctx, PeelState* const* sts, int count) {
+  std::vector<TreeJob*> jobs;
+  std::vector<int> idx;
+  for (int i = 0; i < count; ++i)
+    if (sts[i] && sts[i]->tree) {
+      jobs.push_back(sts[i]->tree.get());
+      idx.push_back(i);
+    }
+  if (jobs.empty()) return;
+  fixpoint_launch_batch(ctx, jobs.data(), static_cast<int>(jobs.size()));
+  std::vector<int> ok(jobs.size(), 0);
+  for (size_t q = 0; q < jobs.size(); ++q) download_bytes(ctx, &ok[q], sts[idx[q]]->skip.p, sizeof(int));
+  sync(ctx);
+  for (size_t q = 0; q < jobs.size(); ++q) {
+    sts[idx[q]]->tree_ok = ok[q] != 0;
+    sts[idx[q]]->tree.reset();  // stream-ordered frees after the launch
+  }
 }
 
 static PeelArgs peel_args(DevGraph& g, PeelState& st, int32_t* seq, int32_t* pos_of, bool progress) {
@@ -1718,21 +1944,30 @@ std::vector<int32_t> topo_order_batch(DevGraph* const* gs, int count, int policy
   }
   std::vector<std::unique_ptr<PeelState>> st(count);
   std::vector<int> live;
-  double bytes = 0.0;
+  std::vector<PeelState*> sp;
   for (int i = 0; i < count; ++i) {
     if (gs[i]->n == 0) continue;
     st[i].reset(new PeelState);
-    peel_prepare(*gs[i], policy, cpath[i], *st[i], false, seq[i], pos_of[i], tree);
+    peel_prepare_begin(*gs[i], policy, cpath[i], *st[i], seq[i], pos_of[i], tree);
     live.push_back(i);
-    bytes += 72.0 * gs[i]->n + 8.0 * gs[i]->m_ok;
+    sp.push_back(st[i].get());
   }
-  {
+  tree_run(ctx, sp.data(), static_cast<int>(sp.size()));
+  std::vector<int> run;  // graphs the one-warp peel orders
+  double bytes = 0.0;
+  for (int i : live)
+    if (!st[i]->tree_ok) {
+      peel_prepare_end(*gs[i], *st[i], false);
+      run.push_back(i);
+      bytes += 72.0 * gs[i]->n + 8.0 * gs[i]->m_ok;
+    }
+  if (!run.empty()) {
     StageScope s(ctx, policy == DP_TOPO_CPD ? "cpd_peel" : "peel", bytes);
-    for (size_t b0 = 0; b0 < live.size(); b0 += kPeelBatch) {
-      const int k = static_cast<int>(std::min<size_t>(kPeelBatch, live.size() - b0));
+    for (size_t b0 = 0; b0 < run.size(); b0 += kPeelBatch) {
+      const int k = static_cast<int>(std::min<size_t>(kPeelBatch, run.size() - b0));
       PeelBatch batch{};
       for (int q = 0; q < k; ++q) {
-        const int i = live[b0 + q];
+        const int i = run[b0 + q];
         batch.a[q] = peel_args(*gs[i], *st[i], seq[i], pos_of[i], false);
       }
       DP_LAUNCH(ctx, k_peel2, k, 32, sm, batch);
@@ -1740,7 +1975,7 @@ std::vector<int32_t> topo_order_batch(DevGraph* const* gs, int count, int policy
   }
   for (int i : live) download_bytes(ctx, &emitted[i], st[i]->counters.p + 1, sizeof(int32_t));
   sync(ctx);
-  for (int i : live)
+  for (int i : run)
     if (st[i]->stack_mode && emitted[i] == gs[i]->n)
       DP_LAUNCH(ctx, k_scatter_pos_of, grid_for(gs[i]->n, 256), 256, 0, seq[i], gs[i]->n, pos_of[i]);
   return emitted;
@@ -1756,6 +1991,9 @@ int32_t topo_order(DevGraph& g, int policy, const int64_t* cpath, int32_t* seq, 
 
 struct PeelDpJob {
   dp_ctx* ctx = nullptr;
+  DevGraph* g = nullptr;
+  int32_t* seq = nullptr;
+  int32_t* pos_of = nullptr;
   PeelState st;
   DevBuf<int64_t> out_sum;
   DevBuf<unsigned long long> mx;
@@ -1780,8 +2018,13 @@ PeelDpJob* peel_dp_prepare(DevGraph& g, const int64_t* cpath, int32_t range, int
   j->mx.zero();
   DP_LAUNCH(ctx, k_max_abs, grid_for(n, 256), 256, 0, j->out_sum.p, n, j->mx.p);
   DP_LAUNCH(ctx, k_max_abs, grid_for(g.m_ok, 256), 256, 0, g.out_cost.p, g.m_ok, j->mx.p);
-  // the peel's preparation is enqueued before the one host round trip of this function
-  peel_prepare(g, DP_TOPO_CPD, cpath, j->st, false, seq, pos_of);
+  // the peel's preparation is enqueued before the one host round trip of this function;
+  // with a tree peel the one-warp peel's inputs wait for its verdict (peel_dp_launch)
+  peel_prepare_begin(g, DP_TOPO_CPD, cpath, j->st, seq, pos_of, true);
+  if (!j->st.tree) peel_prepare_end(g, j->st, false);
+  j->g = &g;
+  j->seq = seq;
+  j->pos_of = pos_of;
   const unsigned long long max_out = scalar_to_host(ctx, j->mx.p);
   DpArgs& da = j->da;
   da.keys32 = static_cast<double>(max_out) * (range + 2) < static_cast<double>(1 << 21);
@@ -1804,8 +2047,6 @@ PeelDpJob* peel_dp_prepare(DevGraph& g, const int64_t* cpath, int32_t range, int
   j->dbg.alloc(ctx, 4);
   j->dbg.zero();
   da.debug = getenv("DP_DEBUG_DP") ? j->dbg.p : nullptr;
-  j->pa = peel_args(g, j->st, seq, pos_of, true);
-  j->pa.debug = da.debug ? j->dbg.p + 3 : nullptr;
   da.progress = j->st.counters.p;
   // algorithmic bytes: peel 64 B row + 8 B seq/pos_of per node; DP 4+8+8+4 B per position
   // (node, memory, out-cost sum, cut) + 12 B per in-edge (source position, cost)
@@ -1820,18 +2061,50 @@ void peel_dp_launch(dp_ctx* ctx, PeelDpJob* const* jobs, int count) {
     DP_CUDA(cudaFuncSetAttribute(k_peel_dp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemPair)));
     DP_CUDA(cudaFuncSetAttribute(k_peel_dp_shared, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(kSmemShared)));
+    DP_CUDA(cudaFuncSetAttribute(k_dp_only, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemDp4)));
     attr = true;
   }
-  // one graph: pair mode (an SM each for peel and DP); several: shared mode (an SM per graph)
-  const bool pair = count == 1 && getenv("DP_PEEL_DP_SHARED") == nullptr;
-  for (int b0 = 0; b0 < count; b0 += kPeelDpBatch) {
-    const int k = std::min(kPeelDpBatch, count - b0);
+  // tree peels of all graphs in one go; the one-warp peel's inputs where a proof failed
+  {
+    std::vector<PeelState*> sp;
+    for (int q = 0; q < count; ++q) sp.push_back(&jobs[q]->st);
+    std::vector<char> had(count);
+    for (int q = 0; q < count; ++q) had[q] = jobs[q]->st.tree != nullptr;
+    tree_run(ctx, sp.data(), count);
+    for (int q = 0; q < count; ++q) {
+      PeelDpJob* j = jobs[q];
+      if (had[q] && !j->st.tree_ok) peel_prepare_end(*j->g, j->st, false);
+      j->pa = peel_args(*j->g, j->st, j->seq, j->pos_of, true);
+      j->pa.debug = j->da.debug ? j->dbg.p + 3 : nullptr;
+    }
+  }
+  // finished orders: the multi-warp DP alone (DP v4), one CTA per graph
+  std::vector<PeelDpJob*> dp4, rest;
+  for (int q = 0; q < count; ++q) {
+    if (jobs[q]->st.tree_ok && jobs[q]->da.v3 && getenv("DP_DP_V3") == nullptr) dp4.push_back(jobs[q]);
+    else rest.push_back(jobs[q]);
+  }
+  for (size_t b0 = 0; b0 < dp4.size(); b0 += kPeelDpBatch) {
+    const int k = static_cast<int>(std::min<size_t>(kPeelDpBatch, dp4.size() - b0));
     PeelDpBatch batch{};
     double bytes = 0.0;
     for (int q = 0; q < k; ++q) {
-      batch.pa[q] = jobs[b0 + q]->pa;
-      batch.da[q] = jobs[b0 + q]->da;
-      bytes += jobs[b0 + q]->bytes;
+      batch.da[q] = dp4[b0 + q]->da;
+      bytes += 32.0 * dp4[b0 + q]->da.n + 12.0 * dp4[b0 + q]->g->m_ok;
+    }
+    StageScope s(ctx, "dp", bytes);
+    DP_LAUNCH(ctx, k_dp_only, k, kDp4Threads, kSmemDp4, batch);
+  }
+  // one graph: pair mode (an SM each for peel and DP); several: shared mode (an SM per graph)
+  const bool pair = count == 1 && rest.size() == 1 && getenv("DP_PEEL_DP_SHARED") == nullptr;
+  for (size_t b0 = 0; b0 < rest.size(); b0 += kPeelDpBatch) {
+    const int k = static_cast<int>(std::min<size_t>(kPeelDpBatch, rest.size() - b0));
+    PeelDpBatch batch{};
+    double bytes = 0.0;
+    for (int q = 0; q < k; ++q) {
+      batch.pa[q] = rest[b0 + q]->pa;
+      batch.da[q] = rest[b0 + q]->da;
+      bytes += rest[b0 + q]->bytes;
     }
     StageScope s(ctx, "peel+dp (streamed)", bytes);
     if (pair) {
@@ -1851,8 +2124,9 @@ void peel_dp_launch(dp_ctx* ctx, PeelDpJob* const* jobs, int count) {
       j->dbg.download(h, 4);
       sync(ctx);
       fprintf(stderr,
-              "[peel_dp] dp warp: total %.1f ms, waiting %.1f ms, staging %.1f ms; peel warp %.1f ms (at 1.965 GHz)\n",
-              h[0] / 1.965e6, h[1] / 1.965e6, h[2] / 1.965e6, h[3] / 1.965e6);
+              "[peel_dp] dp %s: total %.1f ms, waiting %.1f ms, staging %.1f ms; peel warp %.1f ms (at 1.965 GHz)\n",
+              j->st.tree_ok && j->da.v3 ? "v4 (8 warps, tree-peeled order)" : "warp", h[0] / 1.965e6, h[1] / 1.965e6,
+              h[2] / 1.965e6, h[3] / 1.965e6);
     }
   }
 }

@@ -1,5 +1,6 @@
 // peel_dp.cuh — latency-engineered peel and the streamed breakpoint DP.
 #pragma once
+#include "fixpoint.cuh"
 #include "graph.cuh"
 
 namespace dpb {
@@ -19,13 +20,24 @@ struct PeelState {
   DevBuf<int2> cmeta;
   DevBuf<int32_t> gsid;
   DevBuf<int32_t> gover;
-  DevBuf<int> skip;  // set by the fixed-point peel on convergence
+  // ranks and sources (peel_prepare_begin)
+  DevBuf<int32_t> by_rank, rank, flag, fpos;
+  // tree peel (fixpoint.cu): the job until tree_run launched it; skip = 1 on the device and
+  // tree_ok on the host once its proof held (seq/pos_of and the counters are then final)
+  std::unique_ptr<TreeJob> tree;
+  bool tree_ok = false;
+  DevBuf<int> skip;
 };
 
-// seq/pos_of given (stack policies) and tree: the tree peel (fixpoint.cu) is enqueued here
-// and, when its proof holds, the peel kernel only checks the skip flag.
-void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st, bool force_v5 = false,
-                  int32_t* seq = nullptr, int32_t* pos_of = nullptr, bool tree = true);
+// Ranks, sources, counters; with seq/pos_of and tree (stack policies) the tree peel's job.
+void peel_prepare_begin(DevGraph& g, int policy, const int64_t* cpath, PeelState& st, int32_t* seq,
+                        int32_t* pos_of, bool tree);
+// The one-warp peel's inputs (needed unless the tree peel's proof held).
+void peel_prepare_end(DevGraph& g, PeelState& st, bool force_v5);
+// begin + end without a tree peel.
+void peel_prepare(DevGraph& g, int policy, const int64_t* cpath, PeelState& st, bool force_v5 = false);
+// Launches the tree peels of the given states together and waits for their verdicts.
+void tree_run(dp_ctx* ctx, PeelState* const* sts, int count);
 
 // CPD peel of g streamed into the breakpoint DP (R <= 256); writes seq/pos_of and
 // prev_cut[1..n]; *first_exceed = first position whose node exceeds `limit` (or

@@ -10,7 +10,7 @@ from graphs import layered, shuffled
 pytestmark = pytest.mark.gpu
 
 SWITCHES = ["DP_LEVELS_KAHN", "DP_LEVELS_FLOW", "DP_PEEL_V5", "DP_PEEL_DP_SHARED", "DP_PEEL_EXCLUSIVE",
-            "DP_PEEL_NO_PREFETCH", "DP_PEEL_FIXPOINT", "DP_PEEL_NO_FIXPOINT", "DP_DP_V2", "DP_DP_PERSTEP", "DP_PLACE_GLOBAL_META", "DP_SPIN_SYNC"]
+            "DP_PEEL_NO_PREFETCH", "DP_PEEL_FIXPOINT", "DP_PEEL_NO_FIXPOINT", "DP_DP_V3", "DP_DP_V2", "DP_DP_PERSTEP", "DP_PLACE_GLOBAL_META", "DP_SPIN_SYNC"]
 
 
 @pytest.mark.parametrize("var", SWITCHES)
