@@ -105,6 +105,40 @@ void levels_dev(DevGraph& g, dp_comm_t comm, DevBuf<int64_t>& t, DevBuf<int64_t>
   DP_LAUNCH(ctx, k_cpath, grid_for(g.n, 256), 256, 0, t.p, b.p, g.n, c.p);
 }
 
+// levels_dev(g, comm, t, b, c, chainlike = false) of several graphs: one index-order check
+// and shared sweep / dataflow launches (graphs_levels_indexorder), Kahn for the others.
+void levels_dev_batch(DevGraph* const* gs, int count, dp_comm_t comm, DevBuf<int64_t>* const* t,
+                      DevBuf<int64_t>* const* b, DevBuf<int64_t>* const* c) {
+  if (count == 0) return;
+  dp_ctx* ctx = gs[0]->ctx;
+  double bytes = 0.0;
+  std::vector<int64_t*> tp(count), bp(count);
+  for (int i = 0; i < count; ++i) {
+    DevGraph& g = *gs[i];
+    graph_costs(g, comm);
+    t[i]->alloc(ctx, g.n > 0 ? g.n : 1);
+    b[i]->alloc(ctx, g.n > 0 ? g.n : 1);
+    c[i]->alloc(ctx, g.n > 0 ? g.n : 1);
+    tp[i] = t[i]->p;
+    bp[i] = b[i]->p;
+    bytes += 40.0 * g.m_ok + 48.0 * g.n;
+  }
+  {
+    StageScope st(ctx, "levels", bytes);
+    std::vector<char> ok = graphs_levels_indexorder(gs, count, tp.data(), bp.data());
+    for (int i = 0; i < count; ++i)
+      if (!ok[i]) graph_kahn(*gs[i], tp[i], bp[i], nullptr);
+  }
+  for (int i = 0; i < count; ++i) {
+    DevGraph& g = *gs[i];
+    if (g.processed != g.n) {
+      std::vector<int64_t> wit = graph_cycle_witness(g);
+      fail(DP_E_CYCLE_DETECTED, "cycle: [%s]", join_ids(wit).c_str());
+    }
+    DP_LAUNCH(ctx, k_cpath, grid_for(g.n, 256), 256, 0, t[i]->p, b[i]->p, g.n, c[i]->p);
+  }
+}
+
 // levels_dev(g, comm, t, b, c, chainlike = true) of several graphs: one index-order check
 // (one host sync) and one sweep launch per direction for all of them.
 void levels_dev_chainlike_batch(DevGraph* const* gs, int count, dp_comm_t comm, DevBuf<int64_t>* const* t,

@@ -53,6 +53,8 @@ template <typename T>
 struct DevBuf;
 void levels_dev(DevGraph& g, dp_comm_t comm, DevBuf<int64_t>& t, DevBuf<int64_t>& b, DevBuf<int64_t>& c,
                 bool chainlike = false);
+void levels_dev_batch(DevGraph* const* gs, int count, dp_comm_t comm, DevBuf<int64_t>* const* t,
+                      DevBuf<int64_t>* const* b, DevBuf<int64_t>* const* c);
 void levels_dev_chainlike_batch(DevGraph* const* gs, int count, dp_comm_t comm, DevBuf<int64_t>* const* t,
                                 DevBuf<int64_t>* const* b, DevBuf<int64_t>* const* c);
 void seq_ids(DevGraph& g, const int32_t* seq, int32_t n, int64_t* out_dev);

@@ -50,6 +50,7 @@ struct dp_ctx {
   int num_sms = 148;
   int64_t launches = 0;
   int64_t tree_stats[5] = {0, 0, 0, 0, 0};  // tree-peel outcomes (DP_DEBUG_FIXPOINT)
+  int64_t sync_count = 0;                    // host round trips (diagnostics)
   bool timing = false;
   std::vector<dpb::Stage> stages;      // events of the last timed call
   std::vector<dpb::Stage> event_pool;  // recycled events

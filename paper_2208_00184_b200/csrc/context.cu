@@ -109,6 +109,7 @@ void download_bytes(dp_ctx* ctx, void* host, const void* dev, size_t bytes) {
 }
 
 void sync(dp_ctx* ctx) {
+  ++ctx->sync_count;
   if (ctx->sync_ev) {
     DP_CUDA(cudaEventRecord(ctx->sync_ev, ctx->stream));
     DP_CUDA(cudaEventSynchronize(ctx->sync_ev));

@@ -39,7 +39,13 @@
 namespace dpb {
 namespace {
 
-constexpr int kTreeThreads = 1024;
+// One graph alone: 1,024 threads (a level of the deep config is one node per thread).  Several
+// graphs per call: 512 threads per CTA, which leaves room on the SM for other graphs'
+// kernels (throughput mode).
+template <int T>
+struct TreeCfg {
+  static constexpr int kThreads = T, kWarps = T / 32;
+};
 
 struct TreeBatch {
   TreeArgs a[kTreeBatch];
@@ -47,7 +53,8 @@ struct TreeBatch {
 
 __device__ __forceinline__ int32_t ldcg(const int32_t* p) { return __ldcg(p); }
 
-// Exclusive block scan over kTreeThreads threads; *total = sum.  All threads call.
+// Exclusive block scan over TT::kThreads threads; *total = sum.  All threads call.
+template <typename TT>
 __device__ __forceinline__ int32_t block_scan(int32_t x, int32_t* total, int32_t* ws) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int32_t s = x;
@@ -59,7 +66,7 @@ __device__ __forceinline__ int32_t block_scan(int32_t x, int32_t* total, int32_t
   if (lane == 31) ws[warp] = s;
   __syncthreads();
   if (warp == 0) {
-    int32_t t = ws[lane];
+    int32_t t = lane < TT::kWarps ? ws[lane] : 0;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int32_t y = __shfl_up_sync(0xffffffffu, t, o);
@@ -69,36 +76,38 @@ __device__ __forceinline__ int32_t block_scan(int32_t x, int32_t* total, int32_t
   }
   __syncthreads();
   const int32_t r = (warp ? ws[warp - 1] : 0) + s - x;
-  *total = ws[31];
+  *total = ws[TT::kWarps - 1];
   __syncthreads();
   return r;
 }
 
 // pre[roots in s0 level 0 order] = exclusive scan of their subtree sizes
+template <typename TT>
 __device__ void roots_scan(const TreeArgs& a, int32_t nsrc, const int32_t* size, int32_t* pre, int32_t* ws) {
   int32_t carry = 0;
-  for (int32_t i0 = 0; i0 < nsrc; i0 += kTreeThreads) {
+  for (int32_t i0 = 0; i0 < nsrc; i0 += TT::kThreads) {
     const int32_t i = i0 + threadIdx.x;
     const int32_t v = i < nsrc ? a.seq0[i] : -1;
     const int32_t s = v >= 0 ? size[v] : 0;
     int32_t tot;
-    const int32_t ex = block_scan(s, &tot, ws);
+    const int32_t ex = block_scan<TT>(s, &tot, ws);
     if (v >= 0) pre[v] = carry + ex;
     carry += tot;
   }
 }
 
-__global__ void __launch_bounds__(kTreeThreads, 1) k_treepeel(const __grid_constant__ TreeBatch batch) {
+template <typename TT>
+__global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(const __grid_constant__ TreeBatch batch) {
   const TreeArgs& a = batch.a[blockIdx.x];
   __shared__ int32_t ws[32];
   const int tid = threadIdx.x;
   const int32_t n = a.n;
   const int32_t nsrc = *a.nsrc;
-  for (int32_t v = tid; v < n; v += kTreeThreads) {
+  for (int32_t v = tid; v < n; v += TT::kThreads) {
     a.best[v] = -1;
     a.indeg[v] = a.in_off[v + 1] - a.in_off[v];
   }
-  for (int32_t i = tid; i < nsrc; i += kTreeThreads) a.seq0[i] = a.roots[i];
+  for (int32_t i = tid; i < nsrc; i += TT::kThreads) a.seq0[i] = a.roots[i];
   if (tid == 0) a.lvl_off[0] = 0;
   __syncthreads();
   // ---- 1: breadth-first order s0 and the freeing forest T0
@@ -109,7 +118,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_treepeel(const __grid_const
       if (tid == 0) a.info[0] = 2;
       return;
     }
-    for (int32_t i = lb + tid; i < le; i += kTreeThreads) {
+    for (int32_t i = lb + tid; i < le; i += TT::kThreads) {
       const int32_t v = a.seq0[i];
       const int32_t kb = a.out_off[v], ke = a.out_off[v + 1];
       for (int32_t k = kb; k < ke; ++k) {
@@ -120,7 +129,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_treepeel(const __grid_const
     }
     __syncthreads();
     int32_t carry = 0;
-    for (int32_t i0 = lb; i0 < le; i0 += kTreeThreads) {
+    for (int32_t i0 = lb; i0 < le; i0 += TT::kThreads) {
       const int32_t i = i0 + tid;
       int32_t kb = 0, ke = 0, cnt = 0;
       unsigned hit = 0;
@@ -144,7 +153,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_treepeel(const __grid_const
         }
       }
       int32_t tot;
-      const int32_t ex = block_scan(cnt, &tot, ws);
+      const int32_t ex = block_scan<TT>(cnt, &tot, ws);
       if (cnt) {
         int32_t o = le + carry + ex;
         if (ke - kb <= 8) {
@@ -172,7 +181,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_treepeel(const __grid_const
   // ---- 2: subtree sizes of T0 (a child's parent position is best[child])
   for (int32_t l = L - 1; l >= 0; --l) {
     const int32_t b = a.lvl_off[l], e = a.lvl_off[l + 1];
-    for (int32_t i = b + tid; i < e; i += kTreeThreads) {
+    for (int32_t i = b + tid; i < e; i += TT::kThreads) {
       const int32_t v = a.seq0[i];
       int32_t s = 1;
       for (int32_t k = a.out_off[v]; k < a.out_off[v + 1]; ++k) {
@@ -184,11 +193,11 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_treepeel(const __grid_const
     __syncthreads();
   }
   // ---- 3: preorder positions of T0
-  roots_scan(a, nsrc, a.size, a.pre, ws);
+  roots_scan<TT>(a, nsrc, a.size, a.pre, ws);
   __syncthreads();
   for (int32_t l = 0; l + 1 < L; ++l) {
     const int32_t b = a.lvl_off[l], e = a.lvl_off[l + 1];
-    for (int32_t i = b + tid; i < e; i += kTreeThreads) {
+    for (int32_t i = b + tid; i < e; i += TT::kThreads) {
       const int32_t v = a.seq0[i];
       int32_t acc = a.pre[v] + 1;
       for (int32_t k = a.out_off[v]; k < a.out_off[v + 1]; ++k) {
@@ -203,7 +212,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_treepeel(const __grid_const
   }
   // ---- 4: proof T(preorder(T0)) = T0
   bool bad = false;
-  for (int32_t v = tid; v < n; v += kTreeThreads) {
+  for (int32_t v = tid; v < n; v += TT::kThreads) {
     const int32_t b = a.in_off[v], e = a.in_off[v + 1];
     if (b == e) continue;
     int32_t mx = -1;
@@ -221,7 +230,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_treepeel(const __grid_const
     bool done = false;
     for (int r = 0; r < budget && !done; ++r) {
       ++rounds;
-      for (int32_t v = tid; v < n; v += kTreeThreads) {
+      for (int32_t v = tid; v < n; v += TT::kThreads) {
         int32_t bp = -1, bu = -1;
         for (int32_t k = a.in_off[v]; k < a.in_off[v + 1]; ++k) {
           const int32_t u = a.in_src[k];
@@ -236,7 +245,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_treepeel(const __grid_const
       __syncthreads();
       for (int32_t l = L - 1; l >= 0; --l) {
         const int32_t b = a.lvl_off[l], e = a.lvl_off[l + 1];
-        for (int32_t i = b + tid; i < e; i += kTreeThreads) {
+        for (int32_t i = b + tid; i < e; i += TT::kThreads) {
           const int32_t v = a.seq0[i];
           int32_t s = 1;
           for (int32_t k = a.out_off[v]; k < a.out_off[v + 1]; ++k) {
@@ -247,11 +256,11 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_treepeel(const __grid_const
         }
         __syncthreads();
       }
-      roots_scan(a, nsrc, a.size, nxt, ws);
+      roots_scan<TT>(a, nsrc, a.size, nxt, ws);
       __syncthreads();
       for (int32_t l = 0; l + 1 < L; ++l) {
         const int32_t b = a.lvl_off[l], e = a.lvl_off[l + 1];
-        for (int32_t i = b + tid; i < e; i += kTreeThreads) {
+        for (int32_t i = b + tid; i < e; i += TT::kThreads) {
           const int32_t v = a.seq0[i];
           int32_t acc = nxt[v] + 1;
           for (int32_t k = a.out_off[v]; k < a.out_off[v + 1]; ++k) {
@@ -265,7 +274,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_treepeel(const __grid_const
         __syncthreads();
       }
       bool chg = false;
-      for (int32_t v = tid; v < n; v += kTreeThreads) chg |= nxt[v] != pos[v];
+      for (int32_t v = tid; v < n; v += TT::kThreads) chg |= nxt[v] != pos[v];
       done = !__syncthreads_or(chg);
       int32_t* t = pos;
       pos = nxt;
@@ -280,7 +289,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_treepeel(const __grid_const
       return;
     }
   }
-  for (int32_t v = tid; v < n; v += kTreeThreads) {
+  for (int32_t v = tid; v < n; v += TT::kThreads) {
     const int32_t p = pos[v];
     a.seq[p] = v;
     a.pos_of[v] = p;
@@ -412,7 +421,8 @@ void fixpoint_launch_batch(dp_ctx* ctx, TreeJob* const* jobs, int count) {
       bytes += jobs[b0 + q]->bytes;
     }
     StageScope s(ctx, "peel (tree)", bytes);
-    DP_LAUNCH(ctx, k_treepeel, k, kTreeThreads, 0, b);
+    if (count == 1) DP_LAUNCH(ctx, k_treepeel<TreeCfg<1024>>, k, 1024, 0, b);
+    else DP_LAUNCH(ctx, k_treepeel<TreeCfg<512>>, k, 512, 0, b);
   }
   if (getenv("DP_DEBUG_FIXPOINT")) {
     std::vector<int> h(3 * (size_t)count);

@@ -22,6 +22,8 @@ namespace dpb {
 
 void levels_dev(DevGraph& g, dp_comm_t comm, DevBuf<int64_t>& t, DevBuf<int64_t>& b, DevBuf<int64_t>& c,
                 bool chainlike);
+void levels_dev_batch(DevGraph* const* gs, int count, dp_comm_t comm, DevBuf<int64_t>* const* t,
+                      DevBuf<int64_t>* const* b, DevBuf<int64_t>* const* c);
 
 namespace {
 
@@ -648,7 +650,9 @@ void contract_dev(DevGraph& g, Contraction& c, bool materialize_identity) {
   graph_adjacency(w);
 }
 
-void fuse_begin(DevGraph& g, dp_comm_t comm, int32_t range, int64_t limit, FuseOut& out, FuseStage& fs) {
+// fuse_begin = fuse_contract + levels (levels_dev) + fuse_order; the batched pipeline runs
+// the levels of all its graphs together between the two.
+DevGraph& fuse_contract(DevGraph& g, int64_t limit, FuseOut& out, FuseStage& fs) {
   dp_ctx* ctx = g.ctx;
   const int B = 256;
   fs.limit = limit;
@@ -672,7 +676,12 @@ void fuse_begin(DevGraph& g, dp_comm_t comm, int32_t range, int64_t limit, FuseO
            (long long)limit);
     }
   }
-  levels_dev(work, comm, fs.t, fs.b, fs.c, false);
+  return work;
+}
+
+void fuse_order(DevGraph& g, int32_t range, int64_t limit, FuseOut& out, FuseStage& fs) {
+  dp_ctx* ctx = g.ctx;
+  DevGraph& work = out.con.identity ? g : out.con.work;
   const int32_t n = work.n;
   out.seq.alloc(ctx, n > 0 ? n : 1);
   out.pos_of.alloc(ctx, n > 0 ? n : 1);
@@ -690,6 +699,33 @@ void fuse_begin(DevGraph& g, dp_comm_t comm, int32_t range, int64_t limit, FuseO
     if (limit <= 0) fail(DP_E_INVALID_VALUE, "cluster memory limit must be > 0");
     breakpoints_dev(work, out.seq.p, out.pos_of.p, range, limit, out.cl);
   }
+}
+
+void fuse_begin(DevGraph& g, dp_comm_t comm, int32_t range, int64_t limit, FuseOut& out, FuseStage& fs) {
+  DevGraph& work = fuse_contract(g, limit, out, fs);
+  levels_dev(work, comm, fs.t, fs.b, fs.c, false);
+  fuse_order(g, range, limit, out, fs);
+}
+
+void fuse_begin_batch(DevGraph* const* gs, int count, dp_comm_t comm, int32_t range, const int64_t* limit,
+                      FuseOut* const* out, FuseStage* const* fs) {
+  // errors in graph order, as if each graph ran fuse_begin alone: a graph whose contraction
+  // fails is reported after the levels of the graphs before it (cycles) are checked
+  std::vector<DevGraph*> work(count);
+  std::vector<DevBuf<int64_t>*> t(count), b(count), c(count);
+  for (int i = 0; i < count; ++i) {
+    try {
+      work[i] = &fuse_contract(*gs[i], limit[i], *out[i], *fs[i]);
+    } catch (DpFail&) {
+      for (int q = 0; q < i; ++q) levels_dev(*work[q], comm, fs[q]->t, fs[q]->b, fs[q]->c, false);
+      throw;
+    }
+    t[i] = &fs[i]->t;
+    b[i] = &fs[i]->b;
+    c[i] = &fs[i]->c;
+  }
+  levels_dev_batch(work.data(), count, comm, t.data(), b.data(), c.data());
+  for (int i = 0; i < count; ++i) fuse_order(*gs[i], range, limit[i], *out[i], *fs[i]);
 }
 
 void fuse_end(DevGraph& g, FuseOut& out, FuseStage& fs) {

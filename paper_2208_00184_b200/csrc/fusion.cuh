@@ -65,6 +65,9 @@ struct FuseStage {
   int64_t limit = 0;
 };
 void fuse_begin(DevGraph& g, dp_comm_t comm, int32_t range, int64_t limit, FuseOut& out, FuseStage& fs);
+// fuse_begin of several graphs (same comm model and range) with their levels batched.
+void fuse_begin_batch(DevGraph* const* gs, int count, dp_comm_t comm, int32_t range, const int64_t* limit,
+                      FuseOut* const* out, FuseStage* const* fs);
 void fuse_end(DevGraph& g, FuseOut& out, FuseStage& fs);
 
 // ClusterMap re-expressed over original ids (fusion.cpp:317-333) into host buffers.

@@ -531,10 +531,9 @@ __device__ __forceinline__ int ld_relaxed_i32(const int* p) {
 
 // forward (rev = false): in-CSC rows, val = tlevel + w, out = tlevel
 // backward (rev = true): out-CSR rows, val = out = blevel
-__global__ void __launch_bounds__(128) k_levels_flow(int32_t n, const int32_t* off, const int32_t* nbr,
-                                                    const int64_t* cost, const int64_t* w, int64_t* val,
-                                                    int64_t* out, bool rev, int* ctr, int32_t ahead,
-                                                    unsigned sleep_cap) {
+__device__ __forceinline__ void levels_flow_body(int32_t n, const int32_t* off, const int32_t* nbr,
+                                                 const int64_t* cost, const int64_t* w, int64_t* val, int64_t* out,
+                                                 bool rev, int* ctr, int32_t ahead, unsigned sleep_cap) {
   const int lane = threadIdx.x & 31;
   const int32_t nchunks = (n + 31) >> 5;
   for (;;) {
@@ -605,6 +604,39 @@ __global__ void __launch_bounds__(128) k_levels_flow(int32_t n, const int32_t* o
     }
     if (lane == 0) atomicAdd(&ctr[1], 1);
   }
+}
+
+__global__ void __launch_bounds__(128) k_levels_flow(int32_t n, const int32_t* off, const int32_t* nbr,
+                                                    const int64_t* cost, const int64_t* w, int64_t* val,
+                                                    int64_t* out, bool rev, int* ctr, int32_t ahead,
+                                                    unsigned sleep_cap) {
+  levels_flow_body(n, off, nbr, cost, w, val, out, rev, ctr, ahead, sleep_cap);
+}
+
+// Both directions of several graphs in one launch (blockIdx.y = pass): the t and b passes
+// are independent, and the graphs of a batched call stop waiting on each other's level
+// kernels (each pass keeps its own ticket counters and warp count).
+struct FlowPass {
+  int32_t n;
+  const int32_t* off;
+  const int32_t* nbr;
+  const int64_t* cost;
+  const int64_t* w;
+  int64_t* val;
+  int64_t* out;
+  bool rev;
+  int* ctr;
+  int32_t ahead, blocks;
+};
+constexpr int kFlowBatch = 16;
+struct FlowBatch {
+  FlowPass p[kFlowBatch];
+  unsigned sleep_cap;
+};
+__global__ void __launch_bounds__(128) k_levels_flow_batch(const __grid_constant__ FlowBatch b) {
+  const FlowPass& P = b.p[blockIdx.y];
+  if (static_cast<int32_t>(blockIdx.x) >= P.blocks) return;
+  levels_flow_body(P.n, P.off, P.nbr, P.cost, P.w, P.val, P.out, P.rev, P.ctr, P.ahead, b.sleep_cap);
 }
 
 __global__ void k_kahn_init(KahnArgs a) {
@@ -941,7 +973,7 @@ void levels_sweep_launch(DevGraph* const* gs, int64_t* const* tlevel, int64_t* c
 }
 
 // Index-order check of several graphs with one host sync; ok[i] = index order topological.
-std::vector<char> graphs_index_topological(DevGraph* const* gs, int count) {
+std::vector<char> graphs_index_topological(DevGraph* const* gs, int count, std::vector<unsigned long long>* spans) {
   dp_ctx* ctx = gs[0]->ctx;
   DevBuf<unsigned long long> chk(ctx, 2 * (size_t)count);
   std::vector<unsigned long long> init(2 * (size_t)count, 0ull);
@@ -956,6 +988,10 @@ std::vector<char> graphs_index_topological(DevGraph* const* gs, int count) {
   std::vector<unsigned long long> h = to_host(ctx, chk.p, 2 * (size_t)count);
   std::vector<char> ok(count);
   for (int i = 0; i < count; ++i) ok[i] = gs[i]->n > 0 && static_cast<int>(h[2 * i]) == 1;
+  if (spans) {
+    spans->resize(count);
+    for (int i = 0; i < count; ++i) (*spans)[i] = h[2 * i + 1];
+  }
   return ok;
 }
 
@@ -1008,6 +1044,70 @@ bool graph_levels_indexorder(DevGraph& g, int64_t* tlevel, int64_t* blevel, bool
             true, ctr.p + 2, ahead, sleep_cap);
   g.processed = n;
   return true;
+}
+
+// graph_levels_indexorder (chainlike = false) for several graphs: one index-order check (one
+// host round trip), one sweep launch per direction for the small ones, ONE launch for both
+// dataflow passes of all the others.  ok[i] = false: not topological in index order (the
+// caller runs graph_kahn).
+std::vector<char> graphs_levels_indexorder(DevGraph* const* gs, int count, int64_t* const* tlevel,
+                                           int64_t* const* blevel) {
+  std::vector<char> ok(count, 0);
+  if (count == 0 || getenv("DP_LEVELS_KAHN")) return ok;
+  dp_ctx* ctx = gs[0]->ctx;
+  std::vector<unsigned long long> spans;
+  ok = graphs_index_topological(gs, count, &spans);
+  std::vector<DevGraph*> sg;
+  std::vector<int64_t*> st, sb;
+  std::vector<int> flow;
+  for (int i = 0; i < count; ++i) {
+    if (!ok[i]) continue;
+    gs[i]->processed = gs[i]->n;
+    if (gs[i]->n <= kSeqMaxN && getenv("DP_LEVELS_FLOW") == nullptr) {
+      sg.push_back(gs[i]);
+      st.push_back(tlevel[i]);
+      sb.push_back(blevel[i]);
+    } else {
+      flow.push_back(i);
+    }
+  }
+  if (!sg.empty()) levels_sweep_launch(sg.data(), st.data(), sb.data(), static_cast<int>(sg.size()));
+  if (flow.empty()) return ok;
+  unsigned sleep_cap = 256;
+  if (const char* e = getenv("DP_FLOW_SLEEP")) sleep_cap = static_cast<unsigned>(atoi(e));
+  std::vector<DevBuf<int64_t>> fval(flow.size());
+  DevBuf<int> ctr(ctx, 4 * flow.size());
+  ctr.zero();
+  for (size_t q0 = 0; q0 < flow.size(); q0 += kFlowBatch / 2) {
+    const size_t k = std::min<size_t>(kFlowBatch / 2, flow.size() - q0);
+    FlowBatch b{};
+    b.sleep_cap = sleep_cap;
+    int gridx = 1;
+    for (size_t q = 0; q < k; ++q) {
+      const int i = flow[q0 + q];
+      DevGraph& g = *gs[i];
+      const int32_t n = g.n;
+      const double mean_span = g.m_ok > 0 ? static_cast<double>(spans[i]) / g.m_ok : 32.0;
+      int32_t ahead = static_cast<int32_t>(std::min(1.0e6, std::max(64.0, 2.0 * mean_span / 32.0)));
+      if (const char* e = getenv("DP_FLOW_AHEAD")) ahead = atoi(e);
+      const int32_t nchunks = (n + 31) / 32;
+      const int32_t warps = std::max(1, std::min({nchunks, ahead + 32, ctx->num_sms * 32}));
+      const int blocks = (warps + 3) / 4;
+      gridx = std::max(gridx, blocks);
+      fval[q0 + q].alloc(ctx, n);
+      fval[q0 + q].fill_bytes(0xff);
+      DP_CUDA(cudaMemsetAsync(blevel[i], 0xff, sizeof(int64_t) * n, ctx->stream));
+      int* c = ctr.p + 4 * (q0 + q);
+      b.p[2 * q] = FlowPass{n, g.in_off.p, g.in_src.p, g.in_cost.p, g.w.p, fval[q0 + q].p, tlevel[i], false, c, ahead,
+                            blocks};
+      b.p[2 * q + 1] = FlowPass{n, g.out_off.p, g.out_dst.p, g.out_cost.p, g.w.p, blevel[i], blevel[i], true, c + 2,
+                                ahead, blocks};
+    }
+    k_levels_flow_batch<<<dim3(gridx, 2 * static_cast<unsigned>(k)), 128, 0, ctx->stream>>>(b);
+    ++ctx->launches;
+    DP_CUDA(cudaGetLastError());
+  }
+  return ok;
 }
 
 void graph_kahn(DevGraph& g, int64_t* tlevel, int64_t* blevel, int32_t* level_of) {

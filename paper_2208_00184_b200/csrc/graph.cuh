@@ -71,7 +71,11 @@ bool graph_levels_indexorder(DevGraph& g, int64_t* tlevel, int64_t* blevel, bool
 void graph_kahn(DevGraph& g, int64_t* tlevel, int64_t* blevel, int32_t* level_of);
 // Batched building blocks of the chain-like (coarse) levels of several graphs.
 void levels_sweep_launch(DevGraph* const* gs, int64_t* const* tlevel, int64_t* const* blevel, int count);
-std::vector<char> graphs_index_topological(DevGraph* const* gs, int count);
+std::vector<char> graphs_index_topological(DevGraph* const* gs, int count,
+                                           std::vector<unsigned long long>* spans = nullptr);
+// graph_levels_indexorder(chainlike = false) of several graphs with shared launches.
+std::vector<char> graphs_levels_indexorder(DevGraph* const* gs, int count, int64_t* const* tlevel,
+                                           int64_t* const* blevel);
 // CycleDetected witness after an incomplete Kahn pass (graph.cpp:71-94).
 std::vector<int64_t> graph_cycle_witness(DevGraph& g);
 // Node index of an id (UnknownNode when absent); host lookup helper via device search.

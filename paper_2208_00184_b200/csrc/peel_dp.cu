@@ -1093,7 +1093,7 @@ constexpr int kLpMax = 256 + kCh + 1;
 constexpr int kE2Cap = 4096;
 constexpr int kE2CapShared = 1024;
 
-template <int E2>
+template <int E2, bool REC = false>
 struct DpBuf {
   int32_t lo[kCh];   // lo[j] for j = j0 + t + 1 (absolute position)
   int64_t out[kCh];
@@ -1105,6 +1105,13 @@ struct DpBuf {
   int64_t lp[kLpMax];
   int32_t node[kCh];
   int32_t cnt, n2;        // n2 > kE2Cap: the compute warp reads in-edges from HBM
+  // DP v5: per position the first four in-window in-edges {pos, cost << 8} (cost 0 past
+  // the count) and {lo, index of the fifth, number beyond four, 0}, read with broadcast
+  // loads; per 32-position block whether any position has more than four
+  int4 r01[REC ? kCh : 1];
+  int4 r23[REC ? kCh : 1];
+  int4 rz[REC ? kCh : 1];
+  int32_t bext[REC ? kCh / 32 : 1];
 };
 
 template <int E2>
@@ -1118,8 +1125,8 @@ struct DpSmem3 {
 
 __device__ __forceinline__ int ld_volatile_shared(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 
-template <int E2>
-__device__ void dp_stage(const DpArgs& a, DpBuf<E2>& B, int32_t j0, int32_t cnt, int lane) {
+template <int E2, bool REC>
+__device__ void dp_stage(const DpArgs& a, DpBuf<E2, REC>& B, int32_t j0, int32_t cnt, int lane) {
   for (int32_t t = lane; t < cnt; t += 32) {
     const int32_t v = a.seq[j0 + t];
     B.node[t] = v;
@@ -1237,6 +1244,27 @@ __device__ void dp_stage(const DpArgs& a, DpBuf<E2>& B, int32_t j0, int32_t cnt,
     B.cnt = cnt;
     B.n2 = n2;
   }
+  if constexpr (REC) {
+    __syncwarp();
+    if (n2 <= E2) {
+      for (int32_t t0 = 0; t0 < cnt; t0 += 32) {
+        const int32_t t = t0 + lane;
+        int32_t ex = 0;
+        if (t < cnt) {
+          const int32_t eb = B.off2[t], ee = B.off2[t + 1];
+          int2 x[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) x[q] = eb + q < ee ? B.e2[eb + q] : make_int2(0, 0);
+          B.r01[t] = make_int4(x[0].x, x[0].y, x[1].x, x[1].y);
+          B.r23[t] = make_int4(x[2].x, x[2].y, x[3].x, x[3].y);
+          ex = max(0, ee - eb - 4);
+          B.rz[t] = make_int4(B.lo[t], eb + 4, ex, 0);
+        }
+        const unsigned any = __ballot_sync(FULL, ex > 0);
+        if (lane == 0) B.bext[t0 >> 5] = any != 0;
+      }
+    }
+  }
 }
 
 template <typename SmemT>
@@ -1246,7 +1274,7 @@ __device__ void dp_producer(const DpArgs& a, SmemT& S, int k, int lane) {
     const int32_t j0 = c * kCh;
     if (j0 >= a.n) break;
     const int32_t j1 = min(a.n - 1, j0 + kCh - 1);
-    while (ld_volatile_shared(&S.consumed) < c - kDpProducers + 1) __nanosleep(100);
+    while (ld_volatile_shared(&S.consumed) < c - kDpProducers + 1) __nanosleep(1000);
     while (avail < j1 + 1) {
       avail = ld_acquire(a.progress);
       if (avail < j1 + 1) __nanosleep(200);
@@ -1375,178 +1403,247 @@ __device__ void dp_compute_v3(const DpArgs& a, DpSmem3<E2>& S) {
   }
 }
 
-// ---------------------------------------------------------------- DP v4 (order known)
-// The v3 recurrence with its eight candidate rows spread over kDp4Warps = 8 compute warps,
-// for graphs whose order is complete before the DP starts (tree peel, fixpoint.cu).  Rows
-// live in a ring of slots, one per warp: in block b (32 positions) slot b & 7 holds the
-// block's own candidates and slot s the old row r = (s - b - 1) & 7, so the v3 register
-// rotation becomes "+32 on every key" in each warp (the tie byte of a fixed candidate
-// grows by 32 per block) with no data moving between warps.  Per step every warp applies
-// the step's in-window in-edges to its slot and stores its per-lane minimum; per block each
-// warp reduces its 32 x 32 minima (lane = step), one warp runs v3's 31-step chain over the
-// block's own candidates, and the new slot takes the chain's values.  Bit-identical to v3.
-constexpr int kDp4Warps = 8;
+// ---------------------------------------------------------------- DP v5 (order known)
+// The v3 recurrence for graphs whose order is complete before the DP starts (tree peel,
+// fixpoint.cu), on kDp5Slots = 8 slot warps, one chain warp and the staging warps.
+//  * Slots.  v3's eight candidate rows (seven old rows + the block's own candidates) live
+//    in a ring, one slot per warp: in block b slot b & 7 holds the block's candidates and
+//    slot s the old row r = (s - b - 1) & 7, so v3's register rotation becomes "+32 on
+//    every key" in each warp (the tie byte of a fixed candidate grows by 32 per block).
+//    Lane l of row r holds candidate i = P - 224 + 32 r + l (P = block start; the new slot:
+//    i = P + l); an in-edge from position a lowers it iff a >= i, and it is eligible at a
+//    step iff i >= lo.  Per step a slot warp applies the step's in-window in-edges (the
+//    first four from staged records, broadcast loads) and stores its per-lane minimum; per
+//    block it reduces its 32 x 32 minima (lane = step) and arrives at the block's barrier.
+//  * Chain.  One warp runs v3's phase B for block b while the slot warps already work on
+//    block b + 1: it takes the slot minima, then the 32-step chain over the block's own
+//    candidates — candidate P included (k = 0, with the carried best[P]), so the new slot
+//    never needs a chain result to start — and publishes the block's best values.  Only
+//    the warp whose slot becomes row 6 at b + 1 waits for chain(b) (to add those values);
+//    all slot warps stay at most one block ahead.
+//  * Rebase.  Keys are 32-bit (value << 8 | tie byte) relative to a moving frame; when
+//    chain(b) sees the carried value leave +-2^20 it publishes a shift that every warp
+//    applies at the start of block b + 2, one block later than v3 (the slot warps are
+//    already in block b + 1), and the chain adjusts its carry accordingly.
+// Bit-identical to v3 (tests/test_gpu_paths.py, test_gpu_fixpoint.py).
+constexpr int kDp5Slots = 8;
 template <int E2>
-struct DpSmem4 {
-  DpBuf<E2> buf[kDpProducers];
-  int32_t mt[kDp4Warps][32][33];
-  int32_t ct[32][33];
-  int32_t rw[kDp4Warps][32];
-  int32_t bk[32];
-  int32_t bvr;
+struct DpSmem5 {
+  DpBuf<E2, true> buf[kDpProducers];
+  int32_t mt[kDp5Slots][32][33];  // per slot warp, private: minimum per step and lane
+  int32_t ct[2][32][33];          // new slot's keys per step (lanes <= step), by block parity
+  int32_t rw[2][kDp5Slots][32];   // per slot warp: minimum per step, by block parity
+  int32_t bk[2][32];              // chain: best values of the block's candidates
+  int32_t rebase[2];              // chain(b): frame shift applied from block b + 2 on
+  int chain_done;                 // chains completed
   int ready[kDpProducers];
   int consumed;
 };
+constexpr int kDp5Threads = (kDp5Slots + 1 + kDpProducers) * 32;
 
-__device__ __forceinline__ void dp4_sync() { asm volatile("bar.sync 2, %0;" ::"r"(kDp4Warps * 32) : "memory"); }
+__device__ __forceinline__ void dp5_arrive(int p) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(3 + p), "r"((kDp5Slots + 1) * 32) : "memory");
+}
+__device__ __forceinline__ void dp5_wait(int p) {
+  asm volatile("bar.sync %0, %1;" ::"r"(3 + p), "r"((kDp5Slots + 1) * 32) : "memory");
+}
+
+// One step of a slot warp (u: step in the block, t: position in the chunk).  NEW: the
+// block's own candidates (enter at their step, keys to ct); else an old row (minimum to mt).
+template <bool NEW, bool EXT, int E2>
+__device__ __forceinline__ void dp5_step(const DpBuf<E2, true>& B, DpSmem5<E2>& S, int32_t (*mtw)[33], int p,
+                                         int32_t u, int32_t t, int32_t il, int lane, int32_t& K) {
+  const int4 q = B.r01[t];
+  const int4 q2 = B.r23[t];
+  const int4 z = B.rz[t];
+  if (NEW && lane == u) K = 31 - u;  // enters with best = 0 (the chain adds it) + tie byte
+  K -= (q.x >= il ? q.y : 0) + (q.z >= il ? q.w : 0) + (q2.x >= il ? q2.y : 0) + (q2.z >= il ? q2.w : 0);
+  if (EXT && z.z) {
+    for (int32_t e = z.y; e < z.y + z.z; ++e) {
+      const int2 x = B.e2[e];
+      K -= x.x >= il ? x.y : 0;
+    }
+  }
+  if (NEW) {
+    if (lane <= u) S.ct[p][u][lane] = K;
+  } else {
+    mtw[u][lane] = il >= z.x ? K : INT32_MAX;
+  }
+}
+
+template <bool NEW, int E2>
+__device__ __forceinline__ void dp5_block(const DpArgs& a, const DpBuf<E2, true>& B, DpSmem5<E2>& S,
+                                          int32_t (*mtw)[33], int p, int32_t tb, int32_t nb, bool staged, int32_t P,
+                                          int32_t il, int lane, int32_t& K) {
+  if (staged && nb == 32 && !B.bext[tb >> 5]) {  // no position beyond four in-window in-edges
+#pragma unroll 8
+    for (int32_t u = 0; u < 32; ++u) dp5_step<NEW, false>(B, S, mtw, p, u, tb + u, il, lane, K);
+    return;
+  }
+  for (int32_t u = 0; u < nb; ++u) {
+    const int32_t t = tb + u;
+    if (staged) {
+      dp5_step<NEW, true>(B, S, mtw, p, u, t, il, lane, K);
+      continue;
+    }
+    if (NEW && lane == u) K = 31 - u;
+    const int32_t eb = B.off[t], ee = B.off[t + 1];
+    for (int32_t e = eb; e < ee; ++e) {
+      const int32_t k = B.ioff[t] + (e - eb);
+      const int32_t av = a.pos_of[a.in_src[k]];
+      if (av < P - 224) continue;
+      K -= av >= il ? static_cast<int32_t>(a.in_cost[k]) << 8 : 0;
+    }
+    if (NEW) {
+      if (lane <= u) S.ct[p][u][lane] = K;
+    } else {
+      mtw[u][lane] = il >= B.lo[t] ? K : INT32_MAX;
+    }
+  }
+}
 
 template <int E2>
-__device__ void dp_compute_v4(const DpArgs& a, DpSmem4<E2>& S, int w) {
+__device__ void dp_slot_v5(const DpArgs& a, DpSmem5<E2>& S, int w) {
   const int lane = threadIdx.x & 31;
   const int32_t n = a.n;
   constexpr int32_t kUnfilled = 0x3f000000;
   int32_t K = kUnfilled;
-  long long wait_cycles = 0;
-  const long long t_start = clock64();
-  if (w == 0 && lane == 0) S.bvr = 0;
-  dp4_sync();
+  long long cyc_wait = 0;
   int32_t blk = 0;
+  int32_t(*mtw)[33] = S.mt[w];
   for (int32_t c = 0;; ++c) {
     const int32_t j0 = c * kCh;
     if (j0 >= n) break;
     const int kb = c % kDpProducers;
-    const long long tw0 = clock64();
     while (ld_volatile_shared(&S.ready[kb]) != c) __nanosleep(32);
-    wait_cycles += clock64() - tw0;
     __threadfence_block();
-    const DpBuf<E2>& B = S.buf[kb];
+    const DpBuf<E2, true>& B = S.buf[kb];
     const int32_t cnt = B.cnt;
     const bool staged = B.n2 <= E2;
     for (int32_t tb = 0; tb < cnt; tb += 32, ++blk) {
       const int32_t P = j0 + tb;
       const int32_t nb = min(32, cnt - tb);
+      const int p = blk & 1;
       const int32_t r = (w - blk - 1) & 7;  // 7: this block's own candidates
-      const int32_t c0 = 224 - P - lane;
-      const int32_t kn_lim = -P - lane;
-      const int32_t bvr = S.bvr;
-      // lane u loads step u's inputs (first two in-window in-edges, the number of further
-      // ones, lo); the step loop takes them by shuffle, so no load sits on its critical path
-      int32_t X0 = 0, S0 = 0, X1 = 0, S1 = 0, LO = 0, EB = 0, EX = 0;
-      if (lane < nb) {
-        const int32_t t = tb + lane;
-        LO = B.lo[t];
-        if (staged) {
-          const int32_t eb = B.off2[t], ee = B.off2[t + 1];
-          const int2 x0 = B.e2[eb], x1 = B.e2[eb + 1];
-          X0 = x0.x;
-          S0 = eb < ee ? x0.y : 0;
-          X1 = x1.x;
-          S1 = eb + 1 < ee ? x1.y : 0;
-          EB = eb + 2;
-          EX = max(0, ee - eb - 2);
-        }
+      if (blk >= 2) {  // at most one block ahead of the chain; then the frame shift of chain(blk - 2)
+        const long long t0 = a.debug ? clock64() : 0;
+        while (ld_volatile_shared(&S.chain_done) < blk - 1) __nanosleep(20);
+        __threadfence_block();
+        if (a.debug) cyc_wait += clock64() - t0;
+        const int32_t d = S.rebase[p];
+        if (d != 0 && K < kUnfilled) K -= d * 256;
       }
-      const bool extra = !staged || __any_sync(FULL, EX > 0);
-      if (r == 7) {
-#pragma unroll 8
-        for (int32_t u = 0; u < nb; ++u) {
-          const int32_t x0 = __shfl_sync(FULL, X0, u), s0 = __shfl_sync(FULL, S0, u);
-          const int32_t x1 = __shfl_sync(FULL, X1, u), s1 = __shfl_sync(FULL, S1, u);
-          const int32_t lo = __shfl_sync(FULL, LO, u);
-          if (lane == u) K = (u == 0 ? bvr * 256 : 0) + 31 - u;
-          K -= (x0 + kn_lim >= 0 ? s0 : 0) + (x1 + kn_lim >= 0 ? s1 : 0);
-          if (extra) {
-            const int32_t t = tb + u;
-            if (staged) {
-              const int32_t eb = __shfl_sync(FULL, EB, u), ex = __shfl_sync(FULL, EX, u);
-              for (int32_t e = eb; e < eb + ex; ++e) {
-                const int2 x = B.e2[e];
-                K -= x.x + kn_lim >= 0 ? x.y : 0;
-              }
-            } else {
-              const int32_t eb = B.off[t], ee = B.off[t + 1];
-              for (int32_t e = eb; e < ee; ++e) {
-                const int32_t k = B.ioff[t] + (e - eb);
-                const int32_t av = a.pos_of[a.in_src[k]];
-                if (av < P - 224) continue;
-                K -= av + kn_lim >= 0 ? static_cast<int32_t>(a.in_cost[k]) << 8 : 0;
-              }
-            }
+      const int32_t il = r == 7 ? P + lane : P - 224 + 32 * r + lane;  // this lane's candidate
+      if (r == 7) dp5_block<true>(a, B, S, mtw, p, tb, nb, staged, P, il, lane, K);
+      else dp5_block<false>(a, B, S, mtw, p, tb, nb, staged, P, il, lane, K);
+      __syncwarp();
+      // row 6 holds the previous block's candidates: their best values (chain(blk - 1)) are
+      // added now — to the keys, and inside the reduction to the stored minima
+      const bool fix = r == 6 && blk >= 1;
+      if (fix) {
+        const long long t0 = a.debug ? clock64() : 0;
+        while (ld_volatile_shared(&S.chain_done) < blk) __nanosleep(20);
+        __threadfence_block();
+        if (a.debug) cyc_wait += clock64() - t0;
+        K += S.bk[(blk - 1) & 1][lane] * 256;
+      }
+      int32_t m = INT32_MAX;
+      if (r != 7 && lane < nb) {
+        int32_t r4[4] = {INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX};
+        if (fix) {
+          const int32_t* bkp = S.bk[(blk - 1) & 1];
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const int32_t x = mtw[lane][q];
+            r4[q & 3] = min(r4[q & 3], x == INT32_MAX ? INT32_MAX : x + bkp[q] * 256);
           }
-          S.mt[w][u][lane] = (lane == 0 && P >= lo) ? K : INT32_MAX;
-          if (lane >= 1 && lane <= u) S.ct[u][lane] = K;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) r4[q & 3] = min(r4[q & 3], mtw[lane][q]);
+        }
+        m = min(min(r4[0], r4[1]), min(r4[2], r4[3]));
+      }
+      S.rw[p][w][lane] = m;
+      K += 32;
+      __syncwarp();
+      dp5_arrive(p);
+    }
+  }
+  if (w == 0 && lane == 0 && a.debug) a.debug[5] = cyc_wait;
+}
+
+template <int E2>
+__device__ void dp_chain_v5(const DpArgs& a, DpSmem5<E2>& S) {
+  const int lane = threadIdx.x & 31;
+  const int32_t n = a.n;
+  const long long t_start = clock64();
+  long long cyc_chain = 0, cyc_wait = 0;
+  int32_t carry = 0;  // best[P] of the next block, in that block's frame
+  int32_t pend = 0;   // shift published by the previous chain
+  int32_t blk = 0;
+  for (int32_t c = 0;; ++c) {
+    const int32_t j0 = c * kCh;
+    if (j0 >= n) break;
+    const int kb = c % kDpProducers;
+    while (ld_volatile_shared(&S.ready[kb]) != c) __nanosleep(32);
+    __threadfence_block();
+    const DpBuf<E2, true>& B = S.buf[kb];
+    const int32_t cnt = B.cnt;
+    for (int32_t tb = 0; tb < cnt; tb += 32, ++blk) {
+      const int32_t P = j0 + tb;
+      const int32_t nb = min(32, cnt - tb);
+      const int p = blk & 1;
+      const long long t0 = a.debug ? clock64() : 0;
+      dp5_wait(p);
+      const long long t1 = a.debug ? clock64() : 0;
+      int32_t R = INT32_MAX, kmin = 0;
+      if (lane < nb) {
+#pragma unroll
+        for (int q = 0; q < kDp5Slots; ++q) R = min(R, S.rw[p][q][lane]);
+        kmin = B.lo[tb + lane] - P;
+      }
+      int32_t cc[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) cc[k] = S.ct[p][lane][k];
+      if (0 >= kmin) R = min(R, cc[0] + carry * 256);
+      if (nb == 32) {
+#pragma unroll
+        for (int k = 1; k < 32; ++k) {
+          const int32_t b = __shfl_sync(FULL, R, k - 1) & ~255;  // (R >> 8) * 256
+          if (lane >= k && k >= kmin) R = min(R, cc[k] + b);
         }
       } else {
-#pragma unroll 8
-        for (int32_t u = 0; u < nb; ++u) {
-          const int32_t x0 = __shfl_sync(FULL, X0, u), s0 = __shfl_sync(FULL, S0, u);
-          const int32_t x1 = __shfl_sync(FULL, X1, u), s1 = __shfl_sync(FULL, S1, u);
-          const int32_t lo = __shfl_sync(FULL, LO, u);
-          K -= (r <= (x0 + c0) >> 5 ? s0 : 0) + (r <= (x1 + c0) >> 5 ? s1 : 0);
-          if (extra) {
-            const int32_t t = tb + u;
-            if (staged) {
-              const int32_t eb = __shfl_sync(FULL, EB, u), ex = __shfl_sync(FULL, EX, u);
-              for (int32_t e = eb; e < eb + ex; ++e) {
-                const int2 x = B.e2[e];
-                K -= r <= (x.x + c0) >> 5 ? x.y : 0;
-              }
-            } else {
-              const int32_t eb = B.off[t], ee = B.off[t + 1];
-              for (int32_t e = eb; e < ee; ++e) {
-                const int32_t k = B.ioff[t] + (e - eb);
-                const int32_t av = a.pos_of[a.in_src[k]];
-                if (av < P - 224) continue;
-                K -= r <= (av + c0) >> 5 ? static_cast<int32_t>(a.in_cost[k]) << 8 : 0;
-              }
-            }
-          }
-          const int32_t rmin = (lo + c0 + 31) >> 5;
-          S.mt[w][u][lane] = r >= rmin ? K : INT32_MAX;
-        }
-      }
-      __syncwarp();
-      if (lane < nb) {
-        int32_t r4[4] = {INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX};
-#pragma unroll
-        for (int q = 0; q < 32; ++q) r4[q & 3] = min(r4[q & 3], S.mt[w][lane][q]);
-        S.rw[w][lane] = min(min(r4[0], r4[1]), min(r4[2], r4[3]));
-      }
-      dp4_sync();
-      if (w == 0) {  // the chain over the block's own candidates (v3 phase B)
-        int32_t R = INT32_MAX, kmin = 0;
-        if (lane < nb) {
-#pragma unroll
-          for (int q = 0; q < kDp4Warps; ++q) R = min(R, S.rw[q][lane]);
-          kmin = B.lo[tb + lane] - P;
-        }
         for (int k = 1; k < nb; ++k) {
-          const int32_t b = __shfl_sync(FULL, R, k - 1) >> 8;
-          const int32_t cc = S.ct[lane][k];
-          if (lane >= k && k >= kmin) R = min(R, cc + b * 256);
+          const int32_t b = __shfl_sync(FULL, R, k - 1) & ~255;
+          const int32_t ck = S.ct[p][lane][k];
+          if (lane >= k && k >= kmin) R = min(R, ck + b);
         }
-        if (lane < nb) a.prev_cut[P + lane + 1] = P + 31 - (R & 255);
-        S.bk[lane] = __shfl_up_sync(FULL, R, 1) >> 8;
-        const int32_t nb_bvr = __shfl_sync(FULL, R, nb - 1) >> 8;
-        if (lane == 0) S.bvr = nb_bvr;
       }
-      dp4_sync();
-      if (r == 7 && lane >= 1) K += S.bk[lane] * 256;
-      K += 32;
-      const int32_t nbvr = S.bvr;
-      if (nbvr > (1 << 20) || nbvr < -(1 << 20)) {
-        if (K < kUnfilled) K -= nbvr * 256;
-        dp4_sync();
-        if (w == 0 && lane == 0) S.bvr = 0;
+      if (lane < nb) a.prev_cut[P + lane + 1] = P + 31 - (R & 255);
+      const int32_t up = __shfl_up_sync(FULL, R, 1) >> 8;
+      S.bk[p][lane] = lane == 0 ? carry : up;
+      const int32_t cout = __shfl_sync(FULL, R, nb - 1) >> 8;
+      carry = cout - pend;  // into the next block's frame
+      const int32_t d = (carry > (1 << 20) || carry < -(1 << 20)) ? carry : 0;
+      if (lane == 0) S.rebase[p] = d;  // frame of block blk + 2 = frame of blk + 1 - d
+      pend = d;
+      __syncwarp();
+      __threadfence_block();
+      if (lane == 0) *reinterpret_cast<volatile int*>(&S.chain_done) = blk + 1;
+      if (a.debug) {
+        cyc_wait += t1 - t0;
+        cyc_chain += clock64() - t1;
       }
-      dp4_sync();
     }
-    if (w == 0 && lane == 0) *reinterpret_cast<volatile int*>(&S.consumed) = c + 1;
+    __syncwarp();
+    if (lane == 0) *reinterpret_cast<volatile int*>(&S.consumed) = c + 1;
   }
-  if (w == 0 && lane == 0 && a.debug) {
+  if (lane == 0 && a.debug) {
     a.debug[0] = clock64() - t_start;
-    a.debug[1] = wait_cycles;
+    a.debug[1] = 0;
     a.debug[2] = 0;
+    a.debug[4] = cyc_wait;
+    a.debug[6] = cyc_chain;
   }
 }
 
@@ -1620,21 +1717,24 @@ __global__ void __launch_bounds__(kPeelDpExclusive, 1) k_peel_dp_shared(const __
   }
 }
 
-// DP v4 alone on a finished order (tree peel): one CTA per graph, kDp4Warps compute warps
-// and kDpProducers staging warps.
-constexpr int kDp4Threads = (kDp4Warps + kDpProducers) * 32;
-constexpr size_t kSmemDp4 = sizeof(DpSmem4<kE2Cap>);
-static_assert(kSmemDp4 <= 227 * 1024, "DP v4 shared memory exceeds one SM");
-__global__ void __launch_bounds__(kDp4Threads, 1) k_dp_only(const __grid_constant__ PeelDpBatch b) {
+// DP v5 alone on a finished order (tree peel): one CTA per graph — kDp5Slots slot warps,
+// the chain warp, kDpProducers staging warps.
+constexpr size_t kSmemDp5 = sizeof(DpSmem5<kE2Cap>);
+static_assert(kSmemDp5 <= 227 * 1024, "DP v5 shared memory exceeds one SM");
+__global__ void __launch_bounds__(kDp5Threads, 1) k_dp_only(const __grid_constant__ PeelDpBatch b) {
   extern __shared__ int4 smem4[];
   const DpArgs& da = b.da[blockIdx.x];
-  DpSmem4<kE2Cap>& S = *reinterpret_cast<DpSmem4<kE2Cap>*>(smem4);
+  DpSmem5<kE2Cap>& S = *reinterpret_cast<DpSmem5<kE2Cap>*>(smem4);
   if (threadIdx.x < kDpProducers) S.ready[threadIdx.x] = -1;
-  if (threadIdx.x == 0) S.consumed = 0;
+  if (threadIdx.x == 0) {
+    S.consumed = 0;
+    S.chain_done = 0;
+  }
   __syncthreads();
   const int warp = threadIdx.x >> 5;
-  if (warp < kDp4Warps) dp_compute_v4(da, S, warp);
-  else dp_producer(da, S, warp - kDp4Warps, threadIdx.x & 31);
+  if (warp < kDp5Slots) dp_slot_v5(da, S, warp);
+  else if (warp == kDp5Slots) dp_chain_v5(da, S);
+  else dp_producer(da, S, warp - kDp5Slots - 1, threadIdx.x & 31);
 }
 
 __global__ void k_slot16(const int32_t* out_off, const int32_t* out_dst, const int32_t* rank, int32_t m, int4* slot) {
@@ -2044,7 +2144,7 @@ PeelDpJob* peel_dp_prepare(DevGraph& g, const int64_t* cpath, int32_t range, int
   da.in_cost = g.in_cost.p;
   da.prev_cut = prev_cut;
   da.first_exceed = first_exceed;
-  j->dbg.alloc(ctx, 4);
+  j->dbg.alloc(ctx, 8);
   j->dbg.zero();
   da.debug = getenv("DP_DEBUG_DP") ? j->dbg.p : nullptr;
   da.progress = j->st.counters.p;
@@ -2061,7 +2161,7 @@ void peel_dp_launch(dp_ctx* ctx, PeelDpJob* const* jobs, int count) {
     DP_CUDA(cudaFuncSetAttribute(k_peel_dp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemPair)));
     DP_CUDA(cudaFuncSetAttribute(k_peel_dp_shared, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(kSmemShared)));
-    DP_CUDA(cudaFuncSetAttribute(k_dp_only, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemDp4)));
+    DP_CUDA(cudaFuncSetAttribute(k_dp_only, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemDp5)));
     attr = true;
   }
   // tree peels of all graphs in one go; the one-warp peel's inputs where a proof failed
@@ -2093,7 +2193,7 @@ void peel_dp_launch(dp_ctx* ctx, PeelDpJob* const* jobs, int count) {
       bytes += 32.0 * dp4[b0 + q]->da.n + 12.0 * dp4[b0 + q]->g->m_ok;
     }
     StageScope s(ctx, "dp", bytes);
-    DP_LAUNCH(ctx, k_dp_only, k, kDp4Threads, kSmemDp4, batch);
+    DP_LAUNCH(ctx, k_dp_only, k, kDp5Threads, kSmemDp5, batch);
   }
   // one graph: pair mode (an SM each for peel and DP); several: shared mode (an SM per graph)
   const bool pair = count == 1 && rest.size() == 1 && getenv("DP_PEEL_DP_SHARED") == nullptr;
@@ -2120,12 +2220,15 @@ void peel_dp_launch(dp_ctx* ctx, PeelDpJob* const* jobs, int count) {
   for (int q = 0; q < count; ++q) {
     PeelDpJob* j = jobs[q];
     if (j->da.debug) {
-      long long h[4];
-      j->dbg.download(h, 4);
+      long long h[8];
+      j->dbg.download(h, 8);
       sync(ctx);
+      if (j->st.tree_ok && j->da.v3)
+        fprintf(stderr, "[peel_dp] dp v5: chain warp waiting %.1f ms, chaining %.1f ms; slot warp 0 waiting %.1f ms\n",
+                h[4] / 1.965e6, h[6] / 1.965e6, h[5] / 1.965e6);
       fprintf(stderr,
               "[peel_dp] dp %s: total %.1f ms, waiting %.1f ms, staging %.1f ms; peel warp %.1f ms (at 1.965 GHz)\n",
-              j->st.tree_ok && j->da.v3 ? "v4 (8 warps, tree-peeled order)" : "warp", h[0] / 1.965e6, h[1] / 1.965e6,
+              j->st.tree_ok && j->da.v3 ? "v5 (8 slot warps + chain warp, tree-peeled order)" : "warp", h[0] / 1.965e6, h[1] / 1.965e6,
               h[2] / 1.965e6, h[3] / 1.965e6);
     }
   }

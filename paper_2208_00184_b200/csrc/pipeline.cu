@@ -113,12 +113,31 @@ void generate_windows(Resident* const* rs, int count) {
   dp_ctx* ctx = rs[0]->ctx;
   std::vector<std::unique_ptr<FuseStage>> fs;
   std::vector<PeelDpJob*> jobs;
-  for (int i = 0; i < count; ++i) {
-    Resident& r = *rs[i];
-    fs.emplace_back(new FuseStage);
-    fuse_begin(r.g, r.comm, r.cfg.fusion_range, r.limit, r.f, *fs.back());
-    if (fs.back()->streamed) jobs.push_back(fs.back()->job.j);
+  // graphs sharing the comm model and a streamed range: their levels in shared launches
+  // (fuse_order cannot fail then, so errors keep the graph-by-graph order)
+  bool same = rs[0]->cfg.fusion_range >= 1 && rs[0]->cfg.fusion_range <= 256;
+  for (int i = 1; i < count; ++i)
+    same = same && rs[i]->comm.k_us_per_byte == rs[0]->comm.k_us_per_byte && rs[i]->comm.b_us == rs[0]->comm.b_us &&
+           rs[i]->cfg.fusion_range == rs[0]->cfg.fusion_range;
+  for (int i = 0; i < count; ++i) fs.emplace_back(new FuseStage);
+  if (same && count > 1) {
+    std::vector<DevGraph*> gs(count);
+    std::vector<int64_t> lim(count);
+    std::vector<FuseOut*> fo(count);
+    std::vector<FuseStage*> fp(count);
+    for (int i = 0; i < count; ++i) {
+      gs[i] = &rs[i]->g;
+      lim[i] = rs[i]->limit;
+      fo[i] = &rs[i]->f;
+      fp[i] = fs[i].get();
+    }
+    fuse_begin_batch(gs.data(), count, rs[0]->comm, rs[0]->cfg.fusion_range, lim.data(), fo.data(), fp.data());
+  } else {
+    for (int i = 0; i < count; ++i)
+      fuse_begin(rs[i]->g, rs[i]->comm, rs[i]->cfg.fusion_range, rs[i]->limit, rs[i]->f, *fs[i]);
   }
+  for (int i = 0; i < count; ++i)
+    if (fs[i]->streamed) jobs.push_back(fs[i]->job.j);
   if (!jobs.empty()) peel_dp_launch(ctx, jobs.data(), static_cast<int>(jobs.size()));
   for (int i = 0; i < count; ++i) fuse_end(rs[i]->g, rs[i]->f, *fs[i]);
   // coarse levels + cpd_topo of all graphs: one sweep launch per direction, one peel launch
@@ -162,13 +181,25 @@ void generate_windows(Resident* const* rs, int count) {
 void resident_generate(Resident* const* rs, int count, bool with_ccr) {
   dp_ctx* ctx = rs[0]->ctx;
   StageScope whole(ctx, "generate", 0.0);
+  const bool dbg = getenv("DP_DEBUG_SYNC") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  const int64_t s0 = ctx->sync_count;
   for (int i = 0; i < count; ++i) {
     Resident& r = *rs[i];
     resident_validate(r, false);
     graph_costs(r.g, r.comm);
     if (with_ccr) r.original_ccr = ccr_dev(r.g);
   }
+  const auto t1 = std::chrono::steady_clock::now();
+  const int64_t s1 = ctx->sync_count;
   generate_windows(rs, count);
+  if (dbg) {
+    sync(ctx);
+    const auto t2 = std::chrono::steady_clock::now();
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    fprintf(stderr, "[sync] %d graphs: validate %.1f ms (%lld syncs), windows %.1f ms (%lld syncs)\n", count, ms(t0, t1),
+            (long long)(s1 - s0), ms(t1, t2), (long long)(ctx->sync_count - s1));
+  }
 }
 
 void resident_init(Resident& r, dp_ctx* ctx, const dp_graph_t* h, const dp_devices_t* devices, dp_comm_t comm,

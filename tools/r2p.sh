@@ -1,0 +1,6 @@
+#!/bin/bash
+mkdir -p gpurun_out
+T=${1:-r2p}
+PYTHONUNBUFFERED=1 timeout 1200 python -u -m pytest tests/test_gpu_batch.py tests/test_gpu_resident.py tests/test_gpu_fixpoint.py tests/test_gpu_paths.py tests/test_gpu_configs.py tests/test_gpu_switches.py -q -x --timeout 300 -p no:cacheprovider > gpurun_out/${T}_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_pytest.log
+DP_DEBUG_DP=1 timeout 300 python tools/perf_stages.py deep > gpurun_out/${T}_stages_deep.txt 2>&1
+timeout 600 python bench.py --steps 3 --warmup 2 --no-cpu-baseline --candidates 0 --no-e2e --stages-under-load > gpurun_out/${T}_deep.json 2> gpurun_out/${T}_deep.err
