@@ -422,49 +422,60 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
   // stage registers: s (seq id), b (row), c (edge), d (edge with finish/device)
   int32_t s_v = -1;
   int32_t b_v = -1, b_ib = 0, b_ie = 0;
-  int64_t b_w = 0, b_mv = 0;
+  int64_t b_w = 0, b_mv = 0, b_bk = 0;
   int32_t c_v = -1, c_ib = 0, c_ie = 0, c_p = -1;
-  int64_t c_w = 0, c_mv = 0, c_c = 0;
+  int64_t c_w = 0, c_mv = 0, c_c = 0, c_bk = 0;
   int32_t d_v = -1, d_ib = 0, d_ie = 0, d_p = -1, d_dd = 0;
-  int64_t d_w = 0, d_mv = 0, d_c = 0, d_f = 0;
+  int64_t d_w = 0, d_mv = 0, d_c = 0, d_f = 0, d_bk = 0;
   if (tid == 0) s_prev_v = -1;
   // prime: the stages for k = 0 (edges + finish), 1 (edges), 2 (row), 3 (seq id)
   auto advance = [&](int32_t k) {  // loads issued at step k, consumed one step later
     // node k+1: finish / device of this thread's in-edge source (from stage c)
     int32_t nd_v = c_v, nd_ib = c_ib, nd_ie = c_ie, nd_p = c_p, nd_dd = 0;
-    int64_t nd_w = c_w, nd_mv = c_mv, nd_c = c_c, nd_f = 0;
+    int64_t nd_w = c_w, nd_mv = c_mv, nd_c = c_c, nd_f = 0, nd_bk = c_bk;
     if (nd_p >= 0) {
       nd_f = a.finish[nd_p];
       nd_dd = dev[nd_p];
     }
     // node k+2: this thread's in-edge (from stage b)
     int32_t nc_v = b_v, nc_ib = b_ib, nc_ie = b_ie, nc_p = -1;
-    int64_t nc_w = b_w, nc_mv = b_mv, nc_c = 0;
+    int64_t nc_w = b_w, nc_mv = b_mv, nc_c = 0, nc_bk = b_bk;
     if (nc_v >= 0 && nc_ib + tid < nc_ie) {
       nc_p = a.in_src[nc_ib + tid];
       nc_c = a.in_cost[nc_ib + tid];
     }
     // node k+3: row bounds, compute, memory (from stage s)
     int32_t nb_v = s_v, nb_ib = 0, nb_ie = 0;
-    int64_t nb_w = 0, nb_mv = 0;
+    int64_t nb_w = 0, nb_mv = 0, nb_bk = 0;
     if (nb_v >= 0) {
       nb_ib = a.in_off[nb_v];
       nb_ie = a.in_off[nb_v + 1];
       nb_w = a.w[nb_v];
       nb_mv = a.mem[nb_v];
+      if (tid == 0) nb_bk = a.back[nb_v];
     }
     // node k+4: id
     const int32_t ns_v = k + 4 < n ? a.seq[k + 4] : -1;
     d_v = nd_v; d_ib = nd_ib; d_ie = nd_ie; d_p = nd_p; d_dd = nd_dd; d_w = nd_w; d_mv = nd_mv; d_c = nd_c; d_f = nd_f;
-    c_v = nc_v; c_ib = nc_ib; c_ie = nc_ie; c_p = nc_p; c_w = nc_w; c_mv = nc_mv; c_c = nc_c;
-    b_v = nb_v; b_ib = nb_ib; b_ie = nb_ie; b_w = nb_w; b_mv = nb_mv;
+    d_bk = nd_bk;
+    c_v = nc_v; c_ib = nc_ib; c_ie = nc_ie; c_p = nc_p; c_w = nc_w; c_mv = nc_mv; c_c = nc_c; c_bk = nc_bk;
+    b_v = nb_v; b_ib = nb_ib; b_ie = nb_ie; b_w = nb_w; b_mv = nb_mv; b_bk = nb_bk;
     s_v = ns_v;
   };
   for (int32_t k = -4; k < 0; ++k) advance(k);  // after this: d = node 0, c = 1, b = 2, s = 3
   __syncthreads();
+  long long ph[6] = {0, 0, 0, 0, 0, 0}, tp = 0;
+  auto mark = [&](int i) {
+    if (a.debug && tid == 0) {
+      const long long t = clock64();
+      ph[i] += t - tp;
+      tp = t;
+    }
+  };
+  if (a.debug && tid == 0) tp = clock64();
   for (int32_t k = 0; k < n; ++k) {
     const int32_t v = d_v;
-    const int64_t w = d_w, mv = d_mv;
+    const int64_t w = d_w, mv = d_mv, back = d_bk;
     // this step's inputs, then the next steps' loads (consumed from step k+1 on)
     const int32_t my_p = d_p, my_dd0 = d_dd, ib = d_ib, ie = d_ie;
     const int64_t my_c = d_c, my_f0 = d_f;
@@ -476,12 +487,40 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
       sB[d] = LLONG_MIN;
     }
     __syncthreads();
-    if (my_p >= 0) {
-      const bool fresh = my_p == pv;  // placed in the previous step: loaded before its commit
+    mark(0);
+    {
+      // per-device maxima of the node's in-edges.  At most 32 (one warp): one device at a
+      // time (ballot over the lanes still unassigned, full-warp 64-bit max by two redux.sync
+      // on order-preserving words), one shared-memory update per device instead of a
+      // contended CAS per edge; more: a CAS per edge (spread over several warps)
+      const bool act = my_p >= 0;
+      const bool fresh = act && my_p == pv;  // placed in the previous step: loaded before its commit
       const int64_t f = fresh ? pf : my_f0;
       const int32_t dd = fresh ? prev : my_dd0;
-      atomicMax(&sA[dd], static_cast<long long>(f));
-      atomicMax(&sB[dd], static_cast<long long>(f + my_c));
+      auto wmax = [](int64_t x) {
+        const uint64_t u = static_cast<uint64_t>(x) ^ 0x8000000000000000ull;
+        const uint32_t hi = __reduce_max_sync(FULL, static_cast<uint32_t>(u >> 32));
+        const uint32_t lo = __reduce_max_sync(FULL, static_cast<uint32_t>(u >> 32) == hi ? static_cast<uint32_t>(u) : 0u);
+        return static_cast<long long>(((static_cast<uint64_t>(hi) << 32) | lo) ^ 0x8000000000000000ull);
+      };
+      if (ie - ib > 32) {  // in-edges over several warps (wide coarse graphs): per-edge updates
+        if (act) {
+          atomicMax(&sA[dd], static_cast<long long>(f));
+          atomicMax(&sB[dd], static_cast<long long>(f + my_c));
+        }
+      }
+      unsigned todo = ie - ib > 32 ? 0u : __ballot_sync(FULL, act);
+      while (todo) {
+        const int leader = __ffs(todo) - 1;
+        const int32_t d = __shfl_sync(FULL, dd, leader);
+        const bool mine = act && dd == d;
+        todo &= ~__ballot_sync(FULL, mine);
+        const long long ga = wmax(mine ? f : LLONG_MIN), gb = wmax(mine ? f + my_c : LLONG_MIN);
+        if (lane == leader) {
+          atomicMax(&sA[d], ga);
+          atomicMax(&sB[d], gb);
+        }
+      }
     }
     for (int32_t q = ib + T + tid; q < ie; q += T) {
       const int32_t p = a.in_src[q];
@@ -491,6 +530,7 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
       atomicMax(&sB[dd], static_cast<long long>(f + a.in_cost[q]));
     }
     __syncthreads();
+    mark(1);
     for (int32_t d = warp; d < D; d += nwarps) {
       long long mb = LLONG_MIN;
       for (int32_t x = lane; x < D; x += 32)
@@ -508,8 +548,8 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
       }
     }
     __syncthreads();
+    mark(2);
     if (tid == 0) {
-      const int64_t back = a.back[v];
       int32_t best = -1;
       for (int32_t d = 0; d < D; ++d)
         if (savail[d] >= mv && (best < 0 || sest[d] < sest[best])) best = d;
@@ -540,6 +580,7 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
       s_be = be;
     }
     __syncthreads();
+    mark(3);
     if (a.decisions)
       for (int d = tid; d < D; d += blockDim.x) a.dec_est[(int64_t)k * D + d] = sest[d];
     const int32_t chosen = s_chosen;
@@ -559,7 +600,10 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
     }
     prev = chosen;
     __syncthreads();
+    mark(4);
   }
+  if (a.debug && tid == 0)
+    for (int i = 0; i < 5; ++i) a.debug[2 + i] = ph[i];
   for (int d = tid; d < D; d += blockDim.x) a.pdm[1][d] = spdm[d];
   if (tid == 0) a.flags[1][0] = oom ? 1 : 0;
   if (tid == 0 && a.debug) a.debug[1] = clock64() - t0;
@@ -691,9 +735,9 @@ PlaceJob* place_prepare(DevGraph& g, const int32_t* seq, const Devices& devs, Pl
   }
   // block meta on chip when it fits: (5 x 8 + 2 x 4) bytes per block slot
   const size_t meta_bytes = static_cast<size_t>(48) * D * std::max(a.tl[0].maxb, a.tl[1].maxb);
-  a.meta_smem = meta_bytes <= 190 * 1024 && getenv("DP_PLACE_GLOBAL_META") == nullptr;
+  a.meta_smem = meta_bytes <= 186 * 1024 && getenv("DP_PLACE_GLOBAL_META") == nullptr;  // + ~38 KB static
   j->dyn = a.meta_smem ? meta_bytes : 0;
-  j->dbg.alloc(ctx, 2);
+  j->dbg.alloc(ctx, 8);
   a.debug = getenv("DP_DEBUG_PLACE") ? j->dbg.p : nullptr;
   if (a.debug) j->dbg.zero();
   guard.j = nullptr;
@@ -722,11 +766,13 @@ void place_launch(dp_ctx* ctx, PlaceJob* const* jobs, int count) {
   for (int q = 0; q < count; ++q) {
     PlaceJob* j = jobs[q];
     if (j->a.debug) {
-      long long h[2];
-      j->dbg.download(h, 2);
+      long long h[8];
+      j->dbg.download(h, 8);
       sync(ctx);
       fprintf(stderr, "[place] order_place %.2f ms, adjusting %.2f ms (n=%d, D=%d, meta %s)\n", h[0] / 1.965e6,
               h[1] / 1.965e6, j->a.n, j->a.D, j->a.meta_smem ? "smem" : "global");
+      fprintf(stderr, "[place] adjusting phases: loads %.2f, in-edges %.2f, find_slot %.2f, decide %.2f, commit %.2f ms\n",
+              h[2] / 1.965e6, h[3] / 1.965e6, h[4] / 1.965e6, h[5] / 1.965e6, h[6] / 1.965e6);
     }
   }
 }
