@@ -697,6 +697,12 @@ struct DpArgs {
   bool block32;             // ... with 32 steps of drift headroom: 32-step block recurrence
   bool v3;                  // block32 and R <= 225: multi-warp age-ordered recurrence
   long long* debug;         // optional: [total, waiting, staging] cycles of the DP warp
+  // DP v5: per-position records built by k_dp_records (order known before the DP)
+  const int4* rec01;        // first two in-window in-edges {pos, cost << 8, pos, cost << 8}
+  const int4* rec23;        // third and fourth
+  const int4* recz;         // {lo, index of the fifth in ovf, number beyond four, 0}
+  const int32_t* bext;      // per 32 positions: some position has more than four
+  const int2* ovf;          // in-window in-edges beyond the fourth
 };
 
 __device__ __forceinline__ void argmin_reduce(int64_t& v, int32_t& d) {
@@ -1403,6 +1409,65 @@ __device__ void dp_compute_v3(const DpArgs& a, DpSmem3<E2>& S) {
   }
 }
 
+// ---------------------------------------------------------------- DP v5 records
+// What the staging warps compute per chunk for v3 (dp_stage), computed once for every
+// position in parallel when the order is complete: lo (window start under the memory
+// limit, by binary search over the position-order memory prefix), the first-exceed check,
+// and the in-window in-edges (source position >= block start - 224) — the first four in
+// 16-byte records, the rest in an overflow list (order-free: they are summed).
+__global__ void k_mem_by_pos(const int32_t* seq, const int64_t* mem, int32_t n, int64_t* out) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p <= n; p += (int64_t)gridDim.x * blockDim.x)
+    out[p] = p < n ? mem[seq[p]] : 0;
+}
+
+__global__ void __launch_bounds__(256) k_dp_records(DpArgs a, const int64_t* mp, int4* rec01, int4* rec23, int4* recz,
+                                                    int32_t* bext, int2* ovf, int* ovf_count) {
+  const int lane = threadIdx.x & 31;
+  const int32_t n = a.n;
+  for (int64_t p0 = blockIdx.x * (int64_t)blockDim.x; p0 < n; p0 += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t p = static_cast<int32_t>(p0) + threadIdx.x;
+    int32_t cnt = 0;
+    if (p < n) {
+      const int32_t v = a.seq[p];
+      if (a.mem[v] > a.limit) atomicMin(a.first_exceed, p);
+      // lo: smallest i in [max(0, j - R), j - 1] with mp[j] - mp[i] <= limit, j = p + 1
+      const int32_t j = p + 1;
+      int32_t lo = max(0, j - a.range), hi = j - 1;
+      const int64_t pj = mp[j];
+      while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (pj - mp[mid] <= a.limit) hi = mid; else lo = mid + 1;
+      }
+      const int32_t P = p & ~31;
+      const int32_t kb = a.in_off[v], ke = a.in_off[v + 1];
+      int2 x[4] = {make_int2(0, 0), make_int2(0, 0), make_int2(0, 0), make_int2(0, 0)};
+      for (int32_t k = kb; k < ke; ++k) {
+        const int32_t av = a.pos_of[a.in_src[k]];
+        if (av < P - 224) continue;
+        const int2 e = make_int2(av, static_cast<int32_t>(a.in_cost[k]) << 8);
+        if (cnt < 4) x[cnt] = e;
+        ++cnt;
+      }
+      int32_t off = 0;
+      if (cnt > 4) {
+        off = atomicAdd(ovf_count, cnt - 4);
+        int32_t q = 0;
+        for (int32_t k = kb; k < ke; ++k) {
+          const int32_t av = a.pos_of[a.in_src[k]];
+          if (av < P - 224) continue;
+          if (q >= 4) ovf[off + q - 4] = make_int2(av, static_cast<int32_t>(a.in_cost[k]) << 8);
+          ++q;
+        }
+      }
+      rec01[p] = make_int4(x[0].x, x[0].y, x[1].x, x[1].y);
+      rec23[p] = make_int4(x[2].x, x[2].y, x[3].x, x[3].y);
+      recz[p] = make_int4(lo, off, max(0, cnt - 4), 0);
+    }
+    const unsigned any = __ballot_sync(FULL, cnt > 4);
+    if (lane == 0 && p < n + 31) bext[p >> 5] = any != 0;
+  }
+}
+
 // ---------------------------------------------------------------- DP v5 (order known)
 // The v3 recurrence for graphs whose order is complete before the DP starts (tree peel,
 // fixpoint.cu), on kDp5Slots = 8 slot warps, one chain warp and the staging warps.
@@ -1427,9 +1492,18 @@ __device__ void dp_compute_v3(const DpArgs& a, DpSmem3<E2>& S) {
 //    already in block b + 1), and the chain adjusts its carry accordingly.
 // Bit-identical to v3 (tests/test_gpu_paths.py, test_gpu_fixpoint.py).
 constexpr int kDp5Slots = 8;
+// A chunk's records (k_dp_records), copied by a staging warp.
+struct Dp5Buf {
+  int4 r01[kCh];
+  int4 r23[kCh];
+  int4 rz[kCh];
+  int32_t bext[kCh / 32];
+  int32_t cnt, n2;
+};
+
 template <int E2>
 struct DpSmem5 {
-  DpBuf<E2, true> buf[kDpProducers];
+  Dp5Buf buf[kDpProducers];
   int32_t mt[kDp5Slots][32][33];  // per slot warp, private: minimum per step and lane
   int32_t ct[2][32][33];          // new slot's keys per step (lanes <= step), by block parity
   int32_t rw[2][kDp5Slots][32];   // per slot warp: minimum per step, by block parity
@@ -1448,19 +1522,18 @@ __device__ __forceinline__ void dp5_wait(int p) {
   asm volatile("bar.sync %0, %1;" ::"r"(3 + p), "r"((kDp5Slots + 1) * 32) : "memory");
 }
 
-// One step of a slot warp (u: step in the block, t: position in the chunk).  NEW: the
-// block's own candidates (enter at their step, keys to ct); else an old row (minimum to mt).
+// One step of a slot warp (u: step in the block; q, q2, z: the position's staged records).
+// NEW: the block's own candidates (enter at their step, keys to ct); else an old row
+// (minimum to mt).
 template <bool NEW, bool EXT, int E2>
-__device__ __forceinline__ void dp5_step(const DpBuf<E2, true>& B, DpSmem5<E2>& S, int32_t (*mtw)[33], int p,
-                                         int32_t u, int32_t t, int32_t il, int lane, int32_t& K) {
-  const int4 q = B.r01[t];
-  const int4 q2 = B.r23[t];
-  const int4 z = B.rz[t];
+__device__ __forceinline__ void dp5_step(const Dp5Buf& B, DpSmem5<E2>& S, int32_t (*__restrict__ mtw)[33],
+                                         int p, int32_t u, const int4& q, const int4& q2, const int4& z, int32_t il,
+                                         int lane, int32_t& K, const int2* ovf) {
   if (NEW && lane == u) K = 31 - u;  // enters with best = 0 (the chain adds it) + tie byte
   K -= (q.x >= il ? q.y : 0) + (q.z >= il ? q.w : 0) + (q2.x >= il ? q2.y : 0) + (q2.z >= il ? q2.w : 0);
   if (EXT && z.z) {
     for (int32_t e = z.y; e < z.y + z.z; ++e) {
-      const int2 x = B.e2[e];
+      const int2 x = ovf[e];
       K -= x.x >= il ? x.y : 0;
     }
   }
@@ -1472,33 +1545,58 @@ __device__ __forceinline__ void dp5_step(const DpBuf<E2, true>& B, DpSmem5<E2>& 
 }
 
 template <bool NEW, int E2>
-__device__ __forceinline__ void dp5_block(const DpArgs& a, const DpBuf<E2, true>& B, DpSmem5<E2>& S,
+__device__ __forceinline__ void dp5_block(const DpArgs& a, const Dp5Buf& B, DpSmem5<E2>& S,
                                           int32_t (*mtw)[33], int p, int32_t tb, int32_t nb, bool staged, int32_t P,
                                           int32_t il, int lane, int32_t& K) {
+  const int4* __restrict__ r01 = B.r01;
+  const int4* __restrict__ r23 = B.r23;
+  const int4* __restrict__ rz = B.rz;
   if (staged && nb == 32 && !B.bext[tb >> 5]) {  // no position beyond four in-window in-edges
+    // records of step u + 2 load while step u computes
+    int4 qa = r01[tb], qa2 = r23[tb], za = rz[tb];
+    int4 qb = r01[tb + 1], qb2 = r23[tb + 1], zb = rz[tb + 1];
 #pragma unroll 8
-    for (int32_t u = 0; u < 32; ++u) dp5_step<NEW, false>(B, S, mtw, p, u, tb + u, il, lane, K);
+    for (int32_t u = 0; u < 32; ++u) {
+      const int32_t tn = tb + min(u + 2, 31);
+      const int4 qn = r01[tn], qn2 = r23[tn], zn = rz[tn];
+      dp5_step<NEW, false>(B, S, mtw, p, u, qa, qa2, za, il, lane, K, a.ovf);
+      qa = qb;
+      qa2 = qb2;
+      za = zb;
+      qb = qn;
+      qb2 = qn2;
+      zb = zn;
+    }
     return;
   }
   for (int32_t u = 0; u < nb; ++u) {
     const int32_t t = tb + u;
-    if (staged) {
-      dp5_step<NEW, true>(B, S, mtw, p, u, t, il, lane, K);
-      continue;
+    dp5_step<NEW, true>(B, S, mtw, p, u, r01[t], r23[t], rz[t], il, lane, K, a.ovf);
+  }
+}
+
+// DP v5 staging: copy a chunk's records (12 KB) into its buffer; one warp per buffer.
+template <int E2>
+__device__ void dp_producer_v5(const DpArgs& a, DpSmem5<E2>& S, int k, int lane) {
+  for (int32_t c = k;; c += kDpProducers) {
+    const int32_t j0 = c * kCh;
+    if (j0 >= a.n) break;
+    const int32_t cnt = min(kCh, a.n - j0);
+    while (ld_volatile_shared(&S.consumed) < c - kDpProducers + 1) __nanosleep(200);
+    Dp5Buf& B = S.buf[k];
+    for (int32_t t = lane; t < cnt; t += 32) {
+      B.r01[t] = a.rec01[j0 + t];
+      B.r23[t] = a.rec23[j0 + t];
+      B.rz[t] = a.recz[j0 + t];
     }
-    if (NEW && lane == u) K = 31 - u;
-    const int32_t eb = B.off[t], ee = B.off[t + 1];
-    for (int32_t e = eb; e < ee; ++e) {
-      const int32_t k = B.ioff[t] + (e - eb);
-      const int32_t av = a.pos_of[a.in_src[k]];
-      if (av < P - 224) continue;
-      K -= av >= il ? static_cast<int32_t>(a.in_cost[k]) << 8 : 0;
+    if (lane < kCh / 32) B.bext[lane] = lane * 32 < cnt ? a.bext[(j0 >> 5) + lane] : 0;
+    if (lane == 0) {
+      B.cnt = cnt;
+      B.n2 = 0;
     }
-    if (NEW) {
-      if (lane <= u) S.ct[p][u][lane] = K;
-    } else {
-      mtw[u][lane] = il >= B.lo[t] ? K : INT32_MAX;
-    }
+    __syncwarp();
+    __threadfence_block();
+    if (lane == 0) *reinterpret_cast<volatile int*>(&S.ready[k]) = c;
   }
 }
 
@@ -1517,7 +1615,7 @@ __device__ void dp_slot_v5(const DpArgs& a, DpSmem5<E2>& S, int w) {
     const int kb = c % kDpProducers;
     while (ld_volatile_shared(&S.ready[kb]) != c) __nanosleep(32);
     __threadfence_block();
-    const DpBuf<E2, true>& B = S.buf[kb];
+    const Dp5Buf& B = S.buf[kb];
     const int32_t cnt = B.cnt;
     const bool staged = B.n2 <= E2;
     for (int32_t tb = 0; tb < cnt; tb += 32, ++blk) {
@@ -1587,7 +1685,7 @@ __device__ void dp_chain_v5(const DpArgs& a, DpSmem5<E2>& S) {
     const int kb = c % kDpProducers;
     while (ld_volatile_shared(&S.ready[kb]) != c) __nanosleep(32);
     __threadfence_block();
-    const DpBuf<E2, true>& B = S.buf[kb];
+    const Dp5Buf& B = S.buf[kb];
     const int32_t cnt = B.cnt;
     for (int32_t tb = 0; tb < cnt; tb += 32, ++blk) {
       const int32_t P = j0 + tb;
@@ -1600,7 +1698,7 @@ __device__ void dp_chain_v5(const DpArgs& a, DpSmem5<E2>& S) {
       if (lane < nb) {
 #pragma unroll
         for (int q = 0; q < kDp5Slots; ++q) R = min(R, S.rw[p][q][lane]);
-        kmin = B.lo[tb + lane] - P;
+        kmin = B.rz[tb + lane].x - P;
       }
       int32_t cc[32];
 #pragma unroll
@@ -1734,7 +1832,7 @@ __global__ void __launch_bounds__(kDp5Threads, 1) k_dp_only(const __grid_constan
   const int warp = threadIdx.x >> 5;
   if (warp < kDp5Slots) dp_slot_v5(da, S, warp);
   else if (warp == kDp5Slots) dp_chain_v5(da, S);
-  else dp_producer(da, S, warp - kDp5Slots - 1, threadIdx.x & 31);
+  else dp_producer_v5(da, S, warp - kDp5Slots - 1, threadIdx.x & 31);
 }
 
 __global__ void k_slot16(const int32_t* out_off, const int32_t* out_dst, const int32_t* rank, int32_t m, int4* slot) {
@@ -2101,6 +2199,12 @@ struct PeelDpJob {
   PeelArgs pa{};
   DpArgs da{};
   double bytes = 0.0;  // algorithmic bytes (stage timing)
+  // DP v5 records (k_dp_records)
+  DevBuf<int64_t> mp;
+  DevBuf<int4> rec01, rec23, recz;
+  DevBuf<int32_t> bext;
+  DevBuf<int2> ovf;
+  DevBuf<int> ovfc;
 };
 
 PeelDpJob* peel_dp_prepare(DevGraph& g, const int64_t* cpath, int32_t range, int64_t limit, int32_t* seq,
@@ -2183,6 +2287,31 @@ void peel_dp_launch(dp_ctx* ctx, PeelDpJob* const* jobs, int count) {
   for (int q = 0; q < count; ++q) {
     if (jobs[q]->st.tree_ok && jobs[q]->da.v3 && getenv("DP_DP_V3") == nullptr) dp4.push_back(jobs[q]);
     else rest.push_back(jobs[q]);
+  }
+  if (!dp4.empty()) {  // the per-position records of every finished order
+    StageScope s(ctx, "dp records", 0.0);
+    for (PeelDpJob* j : dp4) {
+      const int32_t n = j->da.n;
+      const int32_t m = j->g->m_ok;
+      DevBuf<int64_t> tmp(ctx, (size_t)n + 1);
+      j->mp.alloc(ctx, (size_t)n + 1);
+      DP_LAUNCH(ctx, k_mem_by_pos, grid_for((int64_t)n + 1, 256), 256, 0, j->da.seq, j->da.mem, n, tmp.p);
+      exclusive_scan_i64(ctx, tmp.p, j->mp.p, (int64_t)n + 1);
+      j->rec01.alloc(ctx, n);
+      j->rec23.alloc(ctx, n);
+      j->recz.alloc(ctx, n);
+      j->bext.alloc(ctx, (size_t)n / 32 + 1);
+      j->ovf.alloc(ctx, m > 0 ? m : 1);
+      j->ovfc.alloc(ctx, 1);
+      j->ovfc.zero();
+      DP_LAUNCH(ctx, k_dp_records, grid_for(n, 256), 256, 0, j->da, j->mp.p, j->rec01.p, j->rec23.p, j->recz.p,
+                j->bext.p, j->ovf.p, j->ovfc.p);
+      j->da.rec01 = j->rec01.p;
+      j->da.rec23 = j->rec23.p;
+      j->da.recz = j->recz.p;
+      j->da.bext = j->bext.p;
+      j->da.ovf = j->ovf.p;
+    }
   }
   for (size_t b0 = 0; b0 < dp4.size(); b0 += kPeelDpBatch) {
     const int k = static_cast<int>(std::min<size_t>(kPeelDpBatch, dp4.size() - b0));
