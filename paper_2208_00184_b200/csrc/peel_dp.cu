@@ -1544,6 +1544,7 @@ __device__ __forceinline__ void dp5_step(const Dp5Buf& B, DpSmem5<E2>& S, int32_
   }
 }
 
+
 template <bool NEW, int E2>
 __device__ __forceinline__ void dp5_block(const DpArgs& a, const Dp5Buf& B, DpSmem5<E2>& S,
                                           int32_t (*mtw)[33], int p, int32_t tb, int32_t nb, bool staged, int32_t P,
@@ -1552,20 +1553,20 @@ __device__ __forceinline__ void dp5_block(const DpArgs& a, const Dp5Buf& B, DpSm
   const int4* __restrict__ r23 = B.r23;
   const int4* __restrict__ rz = B.rz;
   if (staged && nb == 32 && !B.bext[tb >> 5]) {  // no position beyond four in-window in-edges
-    // records of step u + 2 load while step u computes
-    int4 qa = r01[tb], qa2 = r23[tb], za = rz[tb];
-    int4 qb = r01[tb + 1], qb2 = r23[tb + 1], zb = rz[tb + 1];
+    // records of step u + 4 load while step u computes
+    int4 q0 = r01[tb], q02 = r23[tb], z0 = rz[tb];
+    int4 q1 = r01[tb + 1], q12 = r23[tb + 1], z1 = rz[tb + 1];
+    int4 q2 = r01[tb + 2], q22 = r23[tb + 2], z2 = rz[tb + 2];
+    int4 q3 = r01[tb + 3], q32 = r23[tb + 3], z3 = rz[tb + 3];
 #pragma unroll 8
     for (int32_t u = 0; u < 32; ++u) {
-      const int32_t tn = tb + min(u + 2, 31);
+      const int32_t tn = tb + min(u + 4, 31);
       const int4 qn = r01[tn], qn2 = r23[tn], zn = rz[tn];
-      dp5_step<NEW, false>(B, S, mtw, p, u, qa, qa2, za, il, lane, K, a.ovf);
-      qa = qb;
-      qa2 = qb2;
-      za = zb;
-      qb = qn;
-      qb2 = qn2;
-      zb = zn;
+      dp5_step<NEW, false>(B, S, mtw, p, u, q0, q02, z0, il, lane, K, a.ovf);
+      q0 = q1; q02 = q12; z0 = z1;
+      q1 = q2; q12 = q22; z1 = z2;
+      q2 = q3; q22 = q32; z2 = z3;
+      q3 = qn; q32 = qn2; z3 = zn;
     }
     return;
   }
@@ -1675,7 +1676,7 @@ __device__ void dp_chain_v5(const DpArgs& a, DpSmem5<E2>& S) {
   const int lane = threadIdx.x & 31;
   const int32_t n = a.n;
   const long long t_start = clock64();
-  long long cyc_chain = 0, cyc_wait = 0;
+  long long cyc_chain = 0, cyc_wait = 0, cyc_ld = 0, cyc_loop = 0;
   int32_t carry = 0;  // best[P] of the next block, in that block's frame
   int32_t pend = 0;   // shift published by the previous chain
   int32_t blk = 0;
@@ -1703,12 +1704,30 @@ __device__ void dp_chain_v5(const DpArgs& a, DpSmem5<E2>& S) {
       int32_t cc[32];
 #pragma unroll
       for (int k = 0; k < 32; ++k) cc[k] = S.ct[p][lane][k];
+      if (a.debug) {
+        const long long tl = clock64();
+        cyc_ld += tl - t1;
+      }
+      const long long t2 = a.debug ? clock64() : 0;
       if (0 >= kmin) R = min(R, cc[0] + carry * 256);
       if (nb == 32) {
+        // two candidates per shuffle round: with R_{k-1} (final) and lane k's partial R_k
+        // fetched together, every lane finishes R_k itself (candidate k is always eligible
+        // at its own step), so b_{k+1} needs no second round trip
+        int32_t ukk[32];
 #pragma unroll
-        for (int k = 1; k < 32; ++k) {
-          const int32_t b = __shfl_sync(FULL, R, k - 1) & ~255;  // (R >> 8) * 256
-          if (lane >= k && k >= kmin) R = min(R, cc[k] + b);
+        for (int k = 1; k < 32; k += 2) ukk[k] = S.ct[p][k][k];
+#pragma unroll
+        for (int k = 1; k < 32; k += 2) {
+          const int32_t x = __shfl_sync(FULL, R, k - 1), y = __shfl_sync(FULL, R, k);
+          const int32_t bk = x & ~255;  // (R_{k-1} >> 8) * 256
+          if (k + 1 < 32) {
+            const int32_t bk1 = min(y, ukk[k] + bk) & ~255;
+            if (lane >= k && k >= kmin) R = min(R, cc[k] + bk);
+            if (lane >= k + 1 && k + 1 >= kmin) R = min(R, cc[k + 1] + bk1);
+          } else {
+            if (lane >= k && k >= kmin) R = min(R, cc[k] + bk);
+          }
         }
       } else {
         for (int k = 1; k < nb; ++k) {
@@ -1717,7 +1736,7 @@ __device__ void dp_chain_v5(const DpArgs& a, DpSmem5<E2>& S) {
           if (lane >= k && k >= kmin) R = min(R, ck + b);
         }
       }
-      if (lane < nb) a.prev_cut[P + lane + 1] = P + 31 - (R & 255);
+      if (a.debug) cyc_loop += clock64() - t2;
       const int32_t up = __shfl_up_sync(FULL, R, 1) >> 8;
       S.bk[p][lane] = lane == 0 ? carry : up;
       const int32_t cout = __shfl_sync(FULL, R, nb - 1) >> 8;
@@ -1726,8 +1745,9 @@ __device__ void dp_chain_v5(const DpArgs& a, DpSmem5<E2>& S) {
       if (lane == 0) S.rebase[p] = d;  // frame of block blk + 2 = frame of blk + 1 - d
       pend = d;
       __syncwarp();
-      __threadfence_block();
+      __threadfence_block();  // shared-memory results before the flag (the global store follows it)
       if (lane == 0) *reinterpret_cast<volatile int*>(&S.chain_done) = blk + 1;
+      if (lane < nb) a.prev_cut[P + lane + 1] = P + 31 - (R & 255);
       if (a.debug) {
         cyc_wait += t1 - t0;
         cyc_chain += clock64() - t1;
@@ -1742,6 +1762,8 @@ __device__ void dp_chain_v5(const DpArgs& a, DpSmem5<E2>& S) {
     a.debug[2] = 0;
     a.debug[4] = cyc_wait;
     a.debug[6] = cyc_chain;
+    a.debug[2] = cyc_ld;
+    a.debug[7] = cyc_loop;
   }
 }
 
@@ -2353,8 +2375,10 @@ void peel_dp_launch(dp_ctx* ctx, PeelDpJob* const* jobs, int count) {
       j->dbg.download(h, 8);
       sync(ctx);
       if (j->st.tree_ok && j->da.v3)
-        fprintf(stderr, "[peel_dp] dp v5: chain warp waiting %.1f ms, chaining %.1f ms; slot warp 0 waiting %.1f ms\n",
-                h[4] / 1.965e6, h[6] / 1.965e6, h[5] / 1.965e6);
+        fprintf(stderr,
+                "[peel_dp] dp v5: chain warp waiting %.1f ms, chaining %.1f ms (loads %.1f, loop %.1f); slot warp 0 "
+                "waiting %.1f ms\n",
+                h[4] / 1.965e6, h[6] / 1.965e6, h[2] / 1.965e6, h[7] / 1.965e6, h[5] / 1.965e6);
       fprintf(stderr,
               "[peel_dp] dp %s: total %.1f ms, waiting %.1f ms, staging %.1f ms; peel warp %.1f ms (at 1.965 GHz)\n",
               j->st.tree_ok && j->da.v3 ? "v5 (8 slot warps + chain warp, tree-peeled order)" : "warp", h[0] / 1.965e6, h[1] / 1.965e6,
