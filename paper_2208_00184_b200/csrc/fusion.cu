@@ -310,6 +310,12 @@ __global__ void k_coarse_decode(const uint64_t* uniq, const int64_t* sums, int32
   }
 }
 
+// coarse edge count: reduce-by-key runs minus the sentinel run (dropped edges), if present
+__global__ void k_coarse_count(const int64_t* runs, const uint64_t* uniq, uint64_t sentinel, int32_t* mc) {
+  const int64_t nr = *runs;
+  *mc = static_cast<int32_t>(nr) - ((nr > 0 && uniq[nr - 1] == sentinel) ? 1 : 0);
+}
+
 __global__ void k_fill_dense_ids(int64_t* id, int32_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     id[i] = i;
@@ -679,7 +685,7 @@ DevGraph& fuse_contract(DevGraph& g, int64_t limit, FuseOut& out, FuseStage& fs)
   return work;
 }
 
-void fuse_order(DevGraph& g, int32_t range, int64_t limit, FuseOut& out, FuseStage& fs) {
+void fuse_order(DevGraph& g, int32_t range, int64_t limit, FuseOut& out, FuseStage& fs, bool defer = false) {
   dp_ctx* ctx = g.ctx;
   DevGraph& work = out.con.identity ? g : out.con.work;
   const int32_t n = work.n;
@@ -692,7 +698,10 @@ void fuse_order(DevGraph& g, int32_t range, int64_t limit, FuseOut& out, FuseSta
     fs.first.alloc(ctx, 1);
     int big = INT32_MAX;
     fs.first.upload(&big, 1);
-    fs.job.j = peel_dp_prepare(work, fs.c.p, range, limit, out.seq.p, out.pos_of.p, fs.prev_cut.p, fs.first.p);
+    // defer: the caller syncs once for several graphs, then runs peel_dp_prepare_finish
+    fs.job.j = defer ? peel_dp_prepare_begin(work, fs.c.p, range, limit, out.seq.p, out.pos_of.p, fs.prev_cut.p,
+                                             fs.first.p)
+                     : peel_dp_prepare(work, fs.c.p, range, limit, out.seq.p, out.pos_of.p, fs.prev_cut.p, fs.first.p);
   } else {
     topo_order(work, DP_TOPO_CPD, fs.c.p, out.seq.p, out.pos_of.p);
     if (range < 1) fail(DP_E_INVALID_VALUE, "exploration range must be >= 1");
@@ -725,7 +734,10 @@ void fuse_begin_batch(DevGraph* const* gs, int count, dp_comm_t comm, int32_t ra
     c[i] = &fs[i]->c;
   }
   levels_dev_batch(work.data(), count, comm, t.data(), b.data(), c.data());
-  for (int i = 0; i < count; ++i) fuse_order(*gs[i], range, limit[i], *out[i], *fs[i]);
+  for (int i = 0; i < count; ++i) fuse_order(*gs[i], range, limit[i], *out[i], *fs[i], true);
+  sync(gs[0]->ctx);  // one round trip for every graph's DP key width
+  for (int i = 0; i < count; ++i)
+    if (fs[i]->streamed) peel_dp_prepare_finish(fs[i]->job.j);
 }
 
 void fuse_end(DevGraph& g, FuseOut& out, FuseStage& fs) {
@@ -749,6 +761,125 @@ void fuse_end(DevGraph& g, FuseOut& out, FuseStage& fs) {
   out.node_cluster.alloc(ctx, g.n > 0 ? g.n : 1);
   DP_LAUNCH(ctx, k_node_cluster_orig, grid_for(g.n, B), B, 0, out.con.identity ? nullptr : out.con.cidx_of.p,
             cl_work.p, g.n, out.node_cluster.p);
+}
+
+// fuse_end of several streamed graphs with three host round trips in all (cut counts and
+// limit checks; coarse edge counts; coarse adjacency) instead of about six per graph.
+// Errors surface graph by graph in order, as from fuse_end.
+void fuse_end_batch(DevGraph* const* gs, int count, FuseOut* const* outs, FuseStage* const* fss) {
+  bool all = count > 1;
+  for (int i = 0; i < count; ++i) all = all && fss[i]->streamed;
+  if (!all) {
+    for (int i = 0; i < count; ++i) fuse_end(*gs[i], *outs[i], *fss[i]);
+    return;
+  }
+  dp_ctx* ctx = gs[0]->ctx;
+  const int B = 256;
+  struct Tmp {
+    DevBuf<uint8_t> is_cut;
+    DevBuf<int32_t> f, fx, cl_work, mcd;
+    DevBuf<uint64_t> keys, ko, uniq;
+    DevBuf<int64_t> vals, vo, sums, runs;
+    int h[2] = {0, 0};
+    int32_t mc = 0;
+    int bits = 1;
+    AdjState adj;
+  };
+  std::vector<std::unique_ptr<Tmp>> T(count);
+  auto work_of = [&](int i) -> DevGraph& { return outs[i]->con.identity ? *gs[i] : outs[i]->con.work; };
+  // 1: traceback and cut counts; the first-exceed flags ride along
+  for (int i = 0; i < count; ++i) {
+    T[i].reset(new Tmp);
+    Tmp& t = *T[i];
+    const int32_t n = work_of(i).n;
+    t.is_cut.alloc(ctx, (size_t)n + 1);
+    t.is_cut.zero();
+    DP_LAUNCH(ctx, k_traceback, 1, 256, 0, fss[i]->prev_cut.p, n, t.is_cut.p);
+    t.f.alloc(ctx, (size_t)n + 1);
+    t.fx.alloc(ctx, (size_t)n + 1);
+    t.f.zero();
+    DP_LAUNCH(ctx, k_cut_scan_in, grid_for(n, B), B, 0, t.is_cut.p, n, t.f.p);
+    exclusive_scan_i32(ctx, t.f.p, t.fx.p, (int64_t)n + 1);
+    download_bytes(ctx, &t.h[0], fss[i]->first.p, sizeof(int));
+    download_bytes(ctx, &t.h[1], t.fx.p + n, sizeof(int32_t));
+  }
+  sync(ctx);
+  // 2: limit checks in graph order (fusion.cpp:110-115), clusters, coarse edge aggregation
+  for (int i = 0; i < count; ++i) {
+    Tmp& t = *T[i];
+    DevGraph& work = work_of(i);
+    FuseOut& out = *outs[i];
+    const int32_t n = work.n;
+    if (t.h[0] != INT32_MAX) {
+      const int32_t v = scalar_to_host(ctx, out.seq.p + t.h[0]);
+      fail(DP_E_NODE_EXCEEDS_CLUSTER_LIMIT, "node %lld needs %lld bytes, cluster limit is %lld",
+           (long long)scalar_to_host(ctx, work.id.p + v), (long long)scalar_to_host(ctx, work.mem.p + v),
+           (long long)fss[i]->limit);
+    }
+    Clusters& cl = out.cl;
+    cl.n = n;
+    cl.k = t.h[1] + 1;
+    const int32_t k = cl.k;
+    cl.cl_of_pos.alloc(ctx, n);
+    cl.cut_pos.alloc(ctx, (size_t)k + 1);
+    cl.tot_w.alloc(ctx, k);
+    cl.tot_mem.alloc(ctx, k);
+    cl.tot_w.zero();
+    cl.tot_mem.zero();
+    DP_LAUNCH(ctx, k_clusters, grid_for(n, B), B, 0, t.fx.p, t.is_cut.p, out.seq.p, n, work.w.p, work.mem.p,
+              cl.cl_of_pos.p, cl.cut_pos.p, cl.tot_w.p, cl.tot_mem.p);
+    DP_CUDA(cudaMemcpyAsync(cl.cut_pos.p + k, &cl.n, sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+    t.cl_work.alloc(ctx, n > 0 ? n : 1);
+    DP_LAUNCH(ctx, k_cl_of_node, grid_for(n, B), B, 0, cl.cl_of_pos.p, out.pos_of.p, n, t.cl_work.p);
+    const int32_t m = work.m;
+    t.bits = bits_for(static_cast<uint64_t>(k));
+    t.keys.alloc(ctx, m > 0 ? m : 1);
+    t.ko.alloc(ctx, m > 0 ? m : 1);
+    t.uniq.alloc(ctx, m > 0 ? m : 1);
+    t.vals.alloc(ctx, m > 0 ? m : 1);
+    t.vo.alloc(ctx, m > 0 ? m : 1);
+    t.sums.alloc(ctx, m > 0 ? m : 1);
+    t.runs.alloc(ctx, 1);
+    t.mcd.alloc(ctx, 1);
+    DP_LAUNCH(ctx, k_coarse_keys, grid_for(m, B), B, 0, work.esrc.p, work.edst.p, work.bytes.p, m, t.cl_work.p,
+              t.bits, t.keys.p, t.vals.p);
+    {
+      StageScope st(ctx, "coarse_aggregate", 24.0 * m);
+      sort_pairs_u64_i64(ctx, t.keys.p, t.ko.p, t.vals.p, t.vo.p, m, 2 * t.bits);
+      reduce_by_key_u64(ctx, t.ko.p, t.uniq.p, t.vo.p, t.sums.p, t.runs.p, m);
+    }
+    const uint64_t sentinel = (t.bits >= 32) ? ~0ull : ((1ull << (2 * t.bits)) - 1);
+    DP_LAUNCH(ctx, k_coarse_count, 1, 1, 0, t.runs.p, t.uniq.p, sentinel, t.mcd.p);
+    download_bytes(ctx, &t.mc, t.mcd.p, sizeof(int32_t));
+  }
+  sync(ctx);
+  // 3: coarse graphs (cluster k: id k, summed compute / memory; fusion.cpp:173-229)
+  for (int i = 0; i < count; ++i) {
+    Tmp& t = *T[i];
+    FuseOut& out = *outs[i];
+    const int32_t k = out.cl.k, mc = t.mc;
+    DevBuf<int64_t> cw(ctx, k > 0 ? k : 1), cm(ctx, k > 0 ? k : 1), cb(ctx, mc > 0 ? mc : 1);
+    DevBuf<int32_t> cs(ctx, mc > 0 ? mc : 1), cd(ctx, mc > 0 ? mc : 1);
+    if (k) {
+      DP_CUDA(cudaMemcpyAsync(cw.p, out.cl.tot_w.p, sizeof(int64_t) * k, cudaMemcpyDeviceToDevice, ctx->stream));
+      DP_CUDA(cudaMemcpyAsync(cm.p, out.cl.tot_mem.p, sizeof(int64_t) * k, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    DP_LAUNCH(ctx, k_coarse_decode, grid_for(mc, B), B, 0, t.uniq.p, t.sums.p, mc, t.bits, cs.p, cd.p, cb.p);
+    graph_adopt_dense(out.coarse, ctx, k, mc, std::move(cw), std::move(cm), std::move(cs), std::move(cd),
+                      std::move(cb));
+    out.coarse.id.alloc(ctx, k > 0 ? k : 1);
+    DP_LAUNCH(ctx, k_fill_dense_ids, grid_for(k, B), B, 0, out.coarse.id.p, k);
+    graph_adjacency_begin(out.coarse, t.adj);
+  }
+  sync(ctx);
+  for (int i = 0; i < count; ++i) {
+    FuseOut& out = *outs[i];
+    graph_adjacency_end(out.coarse, T[i]->adj);
+    DevGraph& g = *gs[i];
+    out.node_cluster.alloc(ctx, g.n > 0 ? g.n : 1);
+    DP_LAUNCH(ctx, k_node_cluster_orig, grid_for(g.n, B), B, 0, out.con.identity ? nullptr : out.con.cidx_of.p,
+              T[i]->cl_work.p, g.n, out.node_cluster.p);
+  }
 }
 
 void fuse_dev(DevGraph& g, dp_comm_t comm, int32_t range, int64_t limit, FuseOut& out) {

@@ -69,6 +69,9 @@ void fuse_begin(DevGraph& g, dp_comm_t comm, int32_t range, int64_t limit, FuseO
 void fuse_begin_batch(DevGraph* const* gs, int count, dp_comm_t comm, int32_t range, const int64_t* limit,
                       FuseOut* const* out, FuseStage* const* fs);
 void fuse_end(DevGraph& g, FuseOut& out, FuseStage& fs);
+// fuse_end of several graphs sharing three host round trips (streamed graphs only; others
+// run fuse_end one by one).
+void fuse_end_batch(DevGraph* const* gs, int count, FuseOut* const* outs, FuseStage* const* fss);
 
 // ClusterMap re-expressed over original ids (fusion.cpp:317-333) into host buffers.
 dp_cluster_map_t* fuse_map_to_host(DevGraph& g, FuseOut& f);

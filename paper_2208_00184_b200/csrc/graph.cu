@@ -845,14 +845,27 @@ void graph_adopt_dense(DevGraph& g, dp_ctx* ctx, int32_t n, int32_t m, DevBuf<in
   g.has_group = false;
 }
 
-void graph_resolve(DevGraph& g) {
+void graph_resolve_begin(DevGraph& g, ResolveState& st) {
   dp_ctx* ctx = g.ctx;
   const int B = 256;
-  DevBuf<int> flag(ctx, 1);
-  int one = 1;
-  flag.upload(&one, 1);
-  DP_LAUNCH(ctx, k_dense_check, grid_for(g.n, B), B, 0, g.id.p, g.n, flag.p);
-  g.dense_ids = scalar_to_host(ctx, flag.p) == 1;
+  st.flag.alloc(ctx, 1);
+  const int one = 1;
+  st.flag.upload(&one, 1);
+  DP_LAUNCH(ctx, k_dense_check, grid_for(g.n, B), B, 0, g.id.p, g.n, st.flag.p);
+  download_bytes(ctx, &st.dense, st.flag.p, sizeof(int));
+}
+
+void graph_resolve(DevGraph& g) {
+  ResolveState st;
+  graph_resolve_begin(g, st);
+  sync(g.ctx);
+  graph_resolve_end(g, st);
+}
+
+void graph_resolve_end(DevGraph& g, ResolveState& st) {
+  dp_ctx* ctx = g.ctx;
+  const int B = 256;
+  g.dense_ids = st.dense == 1;
   if (!g.dense_ids) {
     DevBuf<uint64_t> keys(ctx, g.n);
     DevBuf<int32_t> vals(ctx, g.n);
@@ -880,7 +893,8 @@ int32_t graph_index_of(DevGraph& g, int64_t id) {
   return scalar_to_host(g.ctx, o.p);
 }
 
-void graph_adjacency(DevGraph& g) {
+// graph_adjacency split around its one host round trip, so several graphs share it.
+void graph_adjacency_begin(DevGraph& g, AdjState& st) {
   dp_ctx* ctx = g.ctx;
   const int B = 256;
   int32_t n = g.n, m = g.m;
@@ -888,46 +902,56 @@ void graph_adjacency(DevGraph& g) {
   g.in_off.alloc(ctx, (size_t)n + 1);
   g.out_eid.alloc(ctx, m);
   g.in_eid.alloc(ctx, m);
-  DevBuf<int32_t> cnt(ctx, (size_t)n + 1);
-  DevBuf<uint32_t> keys(ctx, m), keys_out(ctx, m);
-  DevBuf<int32_t> vals(ctx, m);
-  int endbit = bits_for(static_cast<uint64_t>(n));
+  st.cnt.alloc(ctx, (size_t)n + 1);
+  st.keys.alloc(ctx, m);
+  st.keys_out.alloc(ctx, m);
+  st.vals.alloc(ctx, m);
   // CSR by source
-  DevBuf<int> sorted(ctx, 1);
-  int one = 1;
-  sorted.upload(&one, 1);
-  DP_LAUNCH(ctx, k_sorted_check, grid_for(m, B), B, 0, g.esrc.p, g.edst.p, m, sorted.p);
-  cnt.zero();
-  DP_LAUNCH(ctx, k_row_keys, grid_for(m, B), B, 0, g.esrc.p, g.edst.p, m, n, true, keys.p, vals.p, cnt.p);
-  exclusive_scan_i32(ctx, cnt.p, g.out_off.p, (int64_t)n + 1);
-  // one host round trip for the three facts the host needs: already sorted by source,
-  // edges with resolved endpoints, some row longer than 64
-  DevBuf<int> big(ctx, 1);
-  big.zero();
-  DP_LAUNCH(ctx, k_big_rows, grid_for(n, B), B, 0, g.out_off.p, n, big.p);
-  int hs[3] = {0, 0, 0};
-  sorted.download(&hs[0], 1);
-  download_bytes(ctx, &hs[1], g.out_off.p + n, sizeof(int32_t));
-  big.download(&hs[2], 1);
-  sync(ctx);
-  g.m_ok = hs[1];
-  g.big_rows = hs[2] != 0;
-  if (hs[0] == 1) {
+  st.flags.alloc(ctx, 2);  // [0] sorted by source, [1] some row longer than 64
+  const int init[2] = {1, 0};
+  st.flags.upload(init, 2);
+  DP_LAUNCH(ctx, k_sorted_check, grid_for(m, B), B, 0, g.esrc.p, g.edst.p, m, st.flags.p);
+  st.cnt.zero();
+  DP_LAUNCH(ctx, k_row_keys, grid_for(m, B), B, 0, g.esrc.p, g.edst.p, m, n, true, st.keys.p, st.vals.p, st.cnt.p);
+  exclusive_scan_i32(ctx, st.cnt.p, g.out_off.p, (int64_t)n + 1);
+  DP_LAUNCH(ctx, k_big_rows, grid_for(n, B), B, 0, g.out_off.p, n, st.flags.p + 1);
+  // the three facts the host needs: already sorted by source, edges with resolved
+  // endpoints, some row longer than 64 (valid after the caller's sync)
+  download_bytes(ctx, &st.hs[0], st.flags.p, sizeof(int));
+  download_bytes(ctx, &st.hs[1], g.out_off.p + n, sizeof(int32_t));
+  download_bytes(ctx, &st.hs[2], st.flags.p + 1, sizeof(int));
+}
+
+void graph_adjacency_end(DevGraph& g, AdjState& st) {
+  dp_ctx* ctx = g.ctx;
+  const int B = 256;
+  int32_t n = g.n, m = g.m;
+  int endbit = bits_for(static_cast<uint64_t>(n));
+  g.m_ok = st.hs[1];
+  g.big_rows = st.hs[2] != 0;
+  if (st.hs[0] == 1) {
     DP_LAUNCH(ctx, k_iota, grid_for(m, B), B, 0, g.out_eid.p, (int64_t)m);
   } else {
-    sort_pairs_u32(ctx, keys.p, keys_out.p, vals.p, g.out_eid.p, m, endbit);
+    sort_pairs_u32(ctx, st.keys.p, st.keys_out.p, st.vals.p, g.out_eid.p, m, endbit);
   }
   // CSC by destination
-  cnt.zero();
-  DP_LAUNCH(ctx, k_row_keys, grid_for(m, B), B, 0, g.esrc.p, g.edst.p, m, n, false, keys.p, vals.p, cnt.p);
-  exclusive_scan_i32(ctx, cnt.p, g.in_off.p, (int64_t)n + 1);
-  sort_pairs_u32(ctx, keys.p, keys_out.p, vals.p, g.in_eid.p, m, endbit);
+  st.cnt.zero();
+  DP_LAUNCH(ctx, k_row_keys, grid_for(m, B), B, 0, g.esrc.p, g.edst.p, m, n, false, st.keys.p, st.vals.p, st.cnt.p);
+  exclusive_scan_i32(ctx, st.cnt.p, g.in_off.p, (int64_t)n + 1);
+  sort_pairs_u32(ctx, st.keys.p, st.keys_out.p, st.vals.p, g.in_eid.p, m, endbit);
   g.out_dst.alloc(ctx, g.m_ok);
   g.in_src.alloc(ctx, g.m_ok);
   DP_LAUNCH(ctx, k_gather_i32, grid_for(g.m_ok, B), B, 0, g.edst.p, g.out_eid.p, g.out_dst.p, (int64_t)g.m_ok);
   DP_LAUNCH(ctx, k_gather_i32, grid_for(g.m_ok, B), B, 0, g.esrc.p, g.in_eid.p, g.in_src.p, (int64_t)g.m_ok);
   g.has_adj = true;
   g.has_cost = false;  // CSR/CSC-ordered cost copies must follow the new permutation
+}
+
+void graph_adjacency(DevGraph& g) {
+  AdjState st;
+  graph_adjacency_begin(g, st);
+  sync(g.ctx);
+  graph_adjacency_end(g, st);
 }
 
 void graph_costs(DevGraph& g, dp_comm_t comm) {
@@ -1208,22 +1232,27 @@ std::vector<int64_t> graph_cycle_witness(DevGraph& g) {
   return out;
 }
 
-Validation graph_validate(DevGraph& g, const dp_graph_t* h, bool all, bool cycle_check) {
+void graph_validate_begin(DevGraph& g, ValState& vs) {
   dp_ctx* ctx = g.ctx;
   const int B = 256;
   int32_t n = g.n, m = g.m;
-  Validation out;
-  DevBuf<int32_t> dupcount;
+  DevBuf<int32_t>& dupcount = vs.dupcount;
   if (!g.dense_ids && n > 0) {
     dupcount.alloc(ctx, n);
     dupcount.zero();
     DP_LAUNCH(ctx, k_dup_runs, grid_for(n, B), B, 0, g.sorted_key.p, g.sorted_idx.p, n, dupcount.p);
   }
   if (!g.has_adj) graph_adjacency(g);
-  DevBuf<uint8_t> nflags(ctx, n > 0 ? n : 1), eflags(ctx, m > 0 ? m : 1), dupflag(ctx, m > 0 ? m : 1);
+  DevBuf<uint8_t>& nflags = vs.nflags;
+  DevBuf<uint8_t>& eflags = vs.eflags;
+  DevBuf<uint8_t>& dupflag = vs.dupflag;
+  DevBuf<int>& first = vs.first;
+  nflags.alloc(ctx, n > 0 ? n : 1);
+  eflags.alloc(ctx, m > 0 ? m : 1);
+  dupflag.alloc(ctx, m > 0 ? m : 1);
   dupflag.zero();
-  DevBuf<int> first(ctx, 3);
-  int init[3] = {INT32_MAX, INT32_MAX, 0};
+  first.alloc(ctx, 3);
+  const int init[3] = {INT32_MAX, INT32_MAX, 0};
   first.upload(init, 3);
   DP_LAUNCH(ctx, k_dup_edges, grid_for(n, B), B, 0, g.out_off.p, g.out_eid.p, g.out_dst.p, n, dupflag.p,
             first.p + 2);
@@ -1237,10 +1266,24 @@ Validation graph_validate(DevGraph& g, const dp_graph_t* h, bool all, bool cycle
   DP_LAUNCH(ctx, k_node_flags, grid_for(n, B), B, 0, g.w.p, g.mem.p, dupcount.p, n, nflags.p, first.p);
   DP_LAUNCH(ctx, k_edge_flags, grid_for(m, B), B, 0, g.src_id.p, g.dst_id.p, g.bytes.p, g.esrc.p, g.edst.p,
             dupflag.p, m, eflags.p, first.p + 1);
-  int fh[2];
-  first.download(fh, 2);
-  sync(ctx);
+  first.download(vs.fh, 2);  // read after the caller's sync
+}
 
+Validation graph_validate(DevGraph& g, const dp_graph_t* h, bool all, bool cycle_check) {
+  ValState vs;
+  graph_validate_begin(g, vs);
+  sync(g.ctx);
+  return graph_validate_end(g, h, vs, all, cycle_check);
+}
+
+Validation graph_validate_end(DevGraph& g, const dp_graph_t* h, ValState& vs, bool all, bool cycle_check) {
+  dp_ctx* ctx = g.ctx;
+  int32_t n = g.n, m = g.m;
+  Validation out;
+  const int* fh = vs.fh;
+  DevBuf<int32_t>& dupcount = vs.dupcount;
+  DevBuf<uint8_t>& nflags = vs.nflags;
+  DevBuf<uint8_t>& eflags = vs.eflags;
   auto add = [&](int code, std::string msg, std::vector<int64_t> nodes) {
     if (!out.code) {
       out.code = code;

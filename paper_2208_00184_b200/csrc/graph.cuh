@@ -57,14 +57,39 @@ void graph_adopt_dense(DevGraph& g, dp_ctx* ctx, int32_t n, int32_t m, DevBuf<in
                        DevBuf<int64_t>&& bytes);
 // id -> index map and edge endpoint resolution.
 void graph_resolve(DevGraph& g);
+struct ResolveState {
+  DevBuf<int> flag;
+  int dense = 0;
+};
+void graph_resolve_begin(DevGraph& g, ResolveState& st);  // caller syncs between
+void graph_resolve_end(DevGraph& g, ResolveState& st);
 // CSR/CSC over resolvable edges (stable in edge order).
 void graph_adjacency(DevGraph& g);
+// ... split around its one host round trip (the caller syncs between the two; several
+// graphs may share that sync).
+struct AdjState {
+  DevBuf<int32_t> cnt, vals;
+  DevBuf<uint32_t> keys, keys_out;
+  DevBuf<int> flags;
+  int hs[3] = {0, 0, 0};
+};
+void graph_adjacency_begin(DevGraph& g, AdjState& st);
+void graph_adjacency_end(DevGraph& g, AdjState& st);
 // Per-edge comm_time and the CSR/CSC-ordered copies.
 void graph_costs(DevGraph& g, dp_comm_t comm);
 // validate(): needs host arrays for message text.  all=false stops at the first.
 // cycle_check=false skips the Kahn pass (callers that run graph_kahn with levels right
 // after check g.processed themselves and call graph_cycle_witness).
 Validation graph_validate(DevGraph& g, const dp_graph_t* h, bool all, bool cycle_check = true);
+// ... split around its first host round trip (several graphs may share it).
+struct ValState {
+  DevBuf<int32_t> dupcount;
+  DevBuf<uint8_t> nflags, eflags, dupflag;
+  DevBuf<int> first;
+  int fh[2] = {0, 0};
+};
+void graph_validate_begin(DevGraph& g, ValState& vs);
+Validation graph_validate_end(DevGraph& g, const dp_graph_t* h, ValState& vs, bool all, bool cycle_check);
 // Kahn frontier (level-synchronous, persistent cooperative kernel): fills order /
 // level_off / processed, and when requested tlevel / blevel (graph.cpp:228-261).
 bool graph_levels_indexorder(DevGraph& g, int64_t* tlevel, int64_t* blevel, bool chainlike);

@@ -2227,15 +2227,25 @@ struct PeelDpJob {
   DevBuf<int32_t> bext;
   DevBuf<int2> ovf;
   DevBuf<int> ovfc;
+  // peel_dp_prepare_begin -> _finish
+  int32_t range = 0;
+  int64_t limit = 0;
+  int32_t* prev_cut = nullptr;
+  int* first_exceed = nullptr;
+  unsigned long long max_out = 0;
 };
 
-PeelDpJob* peel_dp_prepare(DevGraph& g, const int64_t* cpath, int32_t range, int64_t limit, int32_t* seq,
-                           int32_t* pos_of, int32_t* prev_cut, int* first_exceed) {
+PeelDpJob* peel_dp_prepare_begin(DevGraph& g, const int64_t* cpath, int32_t range, int64_t limit, int32_t* seq,
+                                 int32_t* pos_of, int32_t* prev_cut, int* first_exceed) {
   dp_ctx* ctx = g.ctx;
   const int32_t n = g.n;
   auto* j = new PeelDpJob;
   PeelDpHandle guard(j);
   j->ctx = ctx;
+  j->range = range;
+  j->limit = limit;
+  j->prev_cut = prev_cut;
+  j->first_exceed = first_exceed;
   j->out_sum.alloc(ctx, n);
   DP_LAUNCH(ctx, k_out_sum, grid_for(n, 256), 256, 0, g.out_off.p, g.out_cost.p, n, j->out_sum.p);
   // 32-bit keys need every window value within +-2^22 of the window minimum: bounded
@@ -2251,7 +2261,17 @@ PeelDpJob* peel_dp_prepare(DevGraph& g, const int64_t* cpath, int32_t range, int
   j->g = &g;
   j->seq = seq;
   j->pos_of = pos_of;
-  const unsigned long long max_out = scalar_to_host(ctx, j->mx.p);
+  download_bytes(ctx, &j->max_out, j->mx.p, sizeof(unsigned long long));  // read after the caller's sync
+  guard.j = nullptr;
+  return j;
+}
+
+void peel_dp_prepare_finish(PeelDpJob* j) {
+  dp_ctx* ctx = j->ctx;
+  DevGraph& g = *j->g;
+  const int32_t n = g.n;
+  const int32_t range = j->range;
+  const unsigned long long max_out = j->max_out;
   DpArgs& da = j->da;
   da.keys32 = static_cast<double>(max_out) * (range + 2) < static_cast<double>(1 << 21);
   // the block recurrence lets relative values drift for up to 2 x 32 steps before a rebase
@@ -2260,16 +2280,16 @@ PeelDpJob* peel_dp_prepare(DevGraph& g, const int64_t* cpath, int32_t range, int
   da.v3 = da.keys32 && da.block32 && range <= 225 && getenv("DP_DP_V2") == nullptr;
   da.n = n;
   da.range = range;
-  da.limit = limit;
-  da.seq = seq;
-  da.pos_of = pos_of;
+  da.seq = j->seq;
+  da.pos_of = j->pos_of;
   da.mem = g.mem.p;
   da.out_sum = j->out_sum.p;
   da.in_off = g.in_off.p;
   da.in_src = g.in_src.p;
   da.in_cost = g.in_cost.p;
-  da.prev_cut = prev_cut;
-  da.first_exceed = first_exceed;
+  da.limit = j->limit;
+  da.prev_cut = j->prev_cut;
+  da.first_exceed = j->first_exceed;
   j->dbg.alloc(ctx, 8);
   j->dbg.zero();
   da.debug = getenv("DP_DEBUG_DP") ? j->dbg.p : nullptr;
@@ -2277,6 +2297,14 @@ PeelDpJob* peel_dp_prepare(DevGraph& g, const int64_t* cpath, int32_t range, int
   // algorithmic bytes: peel 64 B row + 8 B seq/pos_of per node; DP 4+8+8+4 B per position
   // (node, memory, out-cost sum, cut) + 12 B per in-edge (source position, cost)
   j->bytes = 92.0 * n + 12.0 * g.m_ok;
+}
+
+PeelDpJob* peel_dp_prepare(DevGraph& g, const int64_t* cpath, int32_t range, int64_t limit, int32_t* seq,
+                           int32_t* pos_of, int32_t* prev_cut, int* first_exceed) {
+  PeelDpJob* j = peel_dp_prepare_begin(g, cpath, range, limit, seq, pos_of, prev_cut, first_exceed);
+  PeelDpHandle guard(j);
+  sync(g.ctx);
+  peel_dp_prepare_finish(j);
   guard.j = nullptr;
   return j;
 }

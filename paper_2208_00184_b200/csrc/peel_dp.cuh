@@ -51,6 +51,11 @@ int32_t peel_dp_stream(DevGraph& g, const int64_t* cpath, int32_t range, int64_t
 struct PeelDpJob;
 PeelDpJob* peel_dp_prepare(DevGraph& g, const int64_t* cpath, int32_t range, int64_t limit, int32_t* seq,
                            int32_t* pos_of, int32_t* prev_cut, int* first_exceed);
+// ... split around its one host round trip (several graphs may share it): begin enqueues,
+// finish runs after a sync of the context stream.
+PeelDpJob* peel_dp_prepare_begin(DevGraph& g, const int64_t* cpath, int32_t range, int64_t limit, int32_t* seq,
+                                 int32_t* pos_of, int32_t* prev_cut, int* first_exceed);
+void peel_dp_prepare_finish(PeelDpJob* j);
 void peel_dp_launch(dp_ctx* ctx, PeelDpJob* const* jobs, int count);
 void peel_dp_release(PeelDpJob* j);
 struct PeelDpHandle {

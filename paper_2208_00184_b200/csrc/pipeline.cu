@@ -91,6 +91,40 @@ void resident_validate(Resident& r, bool cycle_check) {
   if (v.code) fail(v.code, "%s", v.message.c_str());
 }
 
+// resident_validate(r, false) of several graphs with three host round trips in all (id
+// density; adjacency facts; first violations) instead of three per graph.  Violations are
+// reported graph by graph in order.
+void resident_validate_batch(Resident* const* rs, int count, std::vector<Validation>* found = nullptr) {
+  if (count == 1 && !found) {
+    resident_validate(*rs[0], false);
+    return;
+  }
+  dp_ctx* ctx = rs[0]->ctx;
+  double bytes = 0.0;
+  for (int i = 0; i < count; ++i) bytes += 16.0 * rs[i]->g.m + 8.0 * rs[i]->g.n;
+  StageScope st(ctx, "index+validate", bytes);
+  std::vector<ResolveState> R(count);
+  std::vector<AdjState> A(count);
+  std::vector<ValState> V(count);
+  for (int i = 0; i < count; ++i) graph_resolve_begin(rs[i]->g, R[i]);
+  sync(ctx);
+  for (int i = 0; i < count; ++i) {
+    graph_resolve_end(rs[i]->g, R[i]);
+    graph_adjacency_begin(rs[i]->g, A[i]);
+  }
+  sync(ctx);
+  for (int i = 0; i < count; ++i) {
+    graph_adjacency_end(rs[i]->g, A[i]);
+    graph_validate_begin(rs[i]->g, V[i]);
+  }
+  sync(ctx);
+  for (int i = 0; i < count; ++i) {
+    Validation v = graph_validate_end(rs[i]->g, rs[i]->host, V[i], false, false);
+    if (found) found->push_back(std::move(v));
+    else if (v.code) fail(v.code, "%s", v.message.c_str());
+  }
+}
+
 // The end of the generation window (pipeline.cpp:67-79): 2x expand.
 void generate_tail(Resident& r) {
   dp_ctx* ctx = r.ctx;
@@ -139,7 +173,17 @@ void generate_windows(Resident* const* rs, int count) {
   for (int i = 0; i < count; ++i)
     if (fs[i]->streamed) jobs.push_back(fs[i]->job.j);
   if (!jobs.empty()) peel_dp_launch(ctx, jobs.data(), static_cast<int>(jobs.size()));
-  for (int i = 0; i < count; ++i) fuse_end(rs[i]->g, rs[i]->f, *fs[i]);
+  {
+    std::vector<DevGraph*> gs(count);
+    std::vector<FuseOut*> fo(count);
+    std::vector<FuseStage*> fp(count);
+    for (int i = 0; i < count; ++i) {
+      gs[i] = &rs[i]->g;
+      fo[i] = &rs[i]->f;
+      fp[i] = fs[i].get();
+    }
+    fuse_end_batch(gs.data(), count, fo.data(), fp.data());
+  }
   // coarse levels + cpd_topo of all graphs: one sweep launch per direction, one peel launch
   std::vector<DevGraph*> cg(count);
   std::vector<DevBuf<int64_t>*> ct(count), cb(count), cc(count);
@@ -184,11 +228,32 @@ void resident_generate(Resident* const* rs, int count, bool with_ccr) {
   const bool dbg = getenv("DP_DEBUG_SYNC") != nullptr;
   const auto t0 = std::chrono::steady_clock::now();
   const int64_t s0 = ctx->sync_count;
-  for (int i = 0; i < count; ++i) {
-    Resident& r = *rs[i];
-    resident_validate(r, false);
-    graph_costs(r.g, r.comm);
-    if (with_ccr) r.original_ccr = ccr_dev(r.g);
+  if (!with_ccr) {
+    resident_validate_batch(rs, count);
+    for (int i = 0; i < count; ++i) graph_costs(rs[i]->g, rs[i]->comm);
+  } else {  // validation (pipeline.cpp:33) and ccr (:58), one round trip each for all the graphs
+    std::vector<Validation> found;
+    resident_validate_batch(rs, count, &found);
+    for (int i = 0; i < count; ++i)
+      if (!found[i].code) graph_costs(rs[i]->g, rs[i]->comm);
+    std::vector<DevBuf<unsigned long long>> sums(count);
+    std::vector<unsigned long long> h(2 * (size_t)count, 0ull);
+    for (int i = 0; i < count; ++i) {
+      if (found[i].code) continue;
+      DevGraph& g = rs[i]->g;
+      sums[i].alloc(ctx, 2);
+      sums[i].zero();
+      DP_LAUNCH(ctx, k_ccr, grid_for(std::max(g.n, g.m), 256, 4 * ctx->num_sms), 256, 0, g.w.p, g.n, g.cost.p, g.m,
+                sums[i].p);
+      sums[i].download(h.data() + 2 * i, 2);
+    }
+    sync(ctx);
+    for (int i = 0; i < count; ++i) {  // errors graph by graph: its violation, then its ccr
+      if (found[i].code) fail(found[i].code, "%s", found[i].message.c_str());
+      const int64_t tc = static_cast<int64_t>(h[2 * i]);
+      if (tc <= 0) fail(DP_E_ZERO_COMPUTE_TIME, "total compute time is zero");
+      rs[i]->original_ccr = static_cast<double>(static_cast<int64_t>(h[2 * i + 1])) / static_cast<double>(tc);
+    }
   }
   const auto t1 = std::chrono::steady_clock::now();
   const int64_t s1 = ctx->sync_count;
