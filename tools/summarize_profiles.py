@@ -76,7 +76,10 @@ def stalls(rep: str, top: int = 25) -> str:
     for nm in names:
         short = nm.split("(")[0].split("::")[-1]
         r = ncu_csv(rep, "source", ["-k", f"regex:{short}", "--print-source", "sass"])
-        hi = next(i for i, row in enumerate(r) if row and row[0] == "Address")
+        hi = next((i for i, row in enumerate(r) if row and row[0] == "Address"), None)
+        if hi is None:
+            out.append(f"## {short}: no source page")
+            continue
         h = r[hi]
         nxt = next((i for i in range(hi + 1, len(r)) if r[i] and r[i][0] == "Address"), len(r))
         rows = [x for x in r[hi + 1:nxt] if len(x) == len(h) and x[0].startswith("0x")]  # first launch only
