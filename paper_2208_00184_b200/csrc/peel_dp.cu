@@ -1583,7 +1583,7 @@ __device__ void dp_producer_v5(const DpArgs& a, DpSmem5<E2>& S, int k, int lane)
     const int32_t j0 = c * kCh;
     if (j0 >= a.n) break;
     const int32_t cnt = min(kCh, a.n - j0);
-    while (ld_volatile_shared(&S.consumed) < c - kDpProducers + 1) __nanosleep(200);
+    while (ld_volatile_shared(&S.consumed) < c - kDpProducers + 1) __nanosleep(2000);  // a chunk lasts ~10 us
     Dp5Buf& B = S.buf[k];
     for (int32_t t = lane; t < cnt; t += 32) {
       B.r01[t] = a.rec01[j0 + t];
