@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(
     for (int32_t i0 = lb; i0 < le; i0 += TT::kThreads) {
       const int32_t i = i0 + tid;
       int32_t kb = 0, ke = 0, cnt = 0;
+      // (the T0 children of position i will be positions [cs[i], cs[i + 1]) of s0)
       unsigned hit = 0;
       int32_t cc[8];
       if (i < le) {
@@ -154,6 +155,7 @@ __global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(
       }
       int32_t tot;
       const int32_t ex = block_scan<TT>(cnt, &tot, ws);
+      if (i < le) a.cs[i] = le + carry + ex;
       if (cnt) {
         int32_t o = le + carry + ex;
         if (ke - kb <= 8) {
@@ -178,38 +180,47 @@ __global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(
     if (tid == 0) a.info[0] = 3;
     return;
   }
-  // ---- 2: subtree sizes of T0 (a child's parent position is best[child])
+  if (tid == 0) a.cs[n] = n;
+  __syncthreads();
+  // ---- 2: subtree sizes of T0, by s0 position: position i's children are the contiguous
+  // positions [cs[i], cs[i + 1]) of the next level (phase 1 numbered them so)
+  int32_t* psize = a.psize;
+  int32_t* ppre = a.ppre;
   for (int32_t l = L - 1; l >= 0; --l) {
     const int32_t b = a.lvl_off[l], e = a.lvl_off[l + 1];
     for (int32_t i = b + tid; i < e; i += TT::kThreads) {
-      const int32_t v = a.seq0[i];
       int32_t s = 1;
-      for (int32_t k = a.out_off[v]; k < a.out_off[v + 1]; ++k) {
-        const int32_t c = a.rowc[k];
-        if (ldcg(a.best + c) == i) s += a.size[c];
-      }
-      a.size[v] = s;
+      for (int32_t q = a.cs[i]; q < a.cs[i + 1]; ++q) s += psize[q];
+      psize[i] = s;
     }
     __syncthreads();
   }
-  // ---- 3: preorder positions of T0
-  roots_scan<TT>(a, nsrc, a.size, a.pre, ws);
+  // ---- 3: preorder positions of T0 (roots: level 0 in rank order)
+  {
+    int32_t carry = 0;
+    for (int32_t i0 = 0; i0 < nsrc; i0 += TT::kThreads) {
+      const int32_t i = i0 + tid;
+      const int32_t sz = i < nsrc ? psize[i] : 0;
+      int32_t tot;
+      const int32_t ex = block_scan<TT>(sz, &tot, ws);
+      if (i < nsrc) ppre[i] = carry + ex;
+      carry += tot;
+    }
+  }
   __syncthreads();
   for (int32_t l = 0; l + 1 < L; ++l) {
     const int32_t b = a.lvl_off[l], e = a.lvl_off[l + 1];
     for (int32_t i = b + tid; i < e; i += TT::kThreads) {
-      const int32_t v = a.seq0[i];
-      int32_t acc = a.pre[v] + 1;
-      for (int32_t k = a.out_off[v]; k < a.out_off[v + 1]; ++k) {
-        const int32_t c = a.rowc[k];
-        if (ldcg(a.best + c) == i) {
-          a.pre[c] = acc;
-          acc += a.size[c];
-        }
+      int32_t acc = ppre[i] + 1;
+      for (int32_t q = a.cs[i]; q < a.cs[i + 1]; ++q) {
+        ppre[q] = acc;
+        acc += psize[q];
       }
     }
     __syncthreads();
   }
+  for (int32_t i = tid; i < n; i += TT::kThreads) a.pre[a.seq0[i]] = ppre[i];
+  __syncthreads();
   // ---- 4: proof T(preorder(T0)) = T0
   bool bad = false;
   for (int32_t v = tid; v < n; v += TT::kThreads) {
@@ -217,7 +228,7 @@ __global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(
     if (b == e) continue;
     int32_t mx = -1;
     for (int32_t k = b; k < e; ++k) mx = max(mx, a.pre[a.in_src[k]]);
-    bad |= mx != a.pre[a.seq0[ldcg(a.best + v)]];
+    bad |= mx != ppre[ldcg(a.best + v)];
   }
   int32_t* pos = a.pre;
   int rounds = 1;
@@ -379,6 +390,9 @@ std::unique_ptr<TreeJob> fixpoint_prepare(DevGraph& g, const int32_t* by_rank, c
   j->pre2.alloc(ctx, n);
   j->par.alloc(ctx, n);
   j->lvl_off.alloc(ctx, (size_t)n + 1);
+  j->cs.alloc(ctx, (size_t)n + 1);
+  j->psize.alloc(ctx, n);
+  j->ppre.alloc(ctx, n);
   j->info.alloc(ctx, 3);
   j->info.zero();
   TreeArgs& a = j->a;
@@ -397,6 +411,9 @@ std::unique_ptr<TreeJob> fixpoint_prepare(DevGraph& g, const int32_t* by_rank, c
   a.pre2 = j->pre2.p;
   a.par = j->par.p;
   a.lvl_off = j->lvl_off.p;
+  a.cs = j->cs.p;
+  a.psize = j->psize.p;
+  a.ppre = j->ppre.p;
   // ~8 us per level (all phases) against ~0.4 us per node for the one-warp peel
   a.max_levels = getenv("DP_PEEL_FIXPOINT") ? n + 1 : std::max(64, n / 40);
   a.max_rounds = getenv("DP_PEEL_FIXPOINT") ? 4096 : -1;

@@ -22,6 +22,9 @@ struct TreeArgs {
   int32_t* pre2;         // general rounds: second buffer
   int32_t* par;          // general rounds: T(s) parent
   int32_t* lvl_off;      // [n + 1]
+  int32_t* cs;           // [n + 1] s0 position of each position's first T0 child (cs[n] = n)
+  int32_t* psize;        // T0 subtree size by s0 position
+  int32_t* ppre;         // T0 preorder position by s0 position
   int32_t max_levels;    // more levels than this: give up (chain-like graph)
   int32_t max_rounds;    // general rounds after a failed proof (-1: from the cost model)
   int32_t* seq;
@@ -36,7 +39,7 @@ constexpr int kTreeBatch = 8;
 
 struct TreeJob {
   dp_ctx* ctx = nullptr;
-  DevBuf<int32_t> rowc, roots, seq0, best, indeg, size, pre, pre2, par, lvl_off;
+  DevBuf<int32_t> rowc, roots, seq0, best, indeg, size, pre, pre2, par, lvl_off, cs, psize, ppre;
   DevBuf<int> info;
   TreeArgs a{};
   double bytes = 0.0;  // algorithmic bytes (stage timing)

@@ -74,7 +74,9 @@ def stalls(rep: str, top: int = 25) -> str:
     names = sorted({row[h_i] for r in [ncu_csv(rep, "raw")] for h_i in [r[0].index("Kernel Name")] for row in r[2:]})
     out = []
     for nm in names:
-        short = nm.split("(")[0].split("::")[-1]
+        import re
+        mk = re.search(r"\bk_\w+", nm)
+        short = mk.group(0) if mk else nm.split("(")[0].split("::")[-1]
         r = ncu_csv(rep, "source", ["-k", f"regex:{short}", "--print-source", "sass"])
         hi = next((i for i, row in enumerate(r) if row and row[0] == "Address"), None)
         if hi is None:
