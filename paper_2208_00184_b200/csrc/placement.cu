@@ -335,11 +335,9 @@ struct PlaceBatch {
 __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatch batch) {
   const PlaceArgs& a = batch.a[blockIdx.x >> 1];
   __shared__ int32_t sK[kMaxD], snb[kMaxD];
-  __shared__ int64_t sg[kMaxD], sl[kMaxD], savail[kMaxD], spdm[kMaxD];
+  __shared__ int64_t sg[kMaxD], sl[kMaxD], savail[kMaxD], spdm[kMaxD], savail2[kMaxD];
   __shared__ long long sA[kMaxD], sB[kMaxD];
   __shared__ int64_t sest[kMaxD], spre[kMaxD];
-  __shared__ int32_t s_chosen, s_be;
-  __shared__ int64_t s_start;
   const int which = blockIdx.x & 1;  // 0 order_place, 1 adjusting_placement
   const long long t0 = clock64();
   if (!a.run[which]) return;
@@ -364,6 +362,8 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
     sg[d] = -1;
     sl[d] = 0;
     savail[d] = a.cap[d];
+    sA[d] = LLONG_MIN;
+    sB[d] = LLONG_MIN;
     spdm[d] = 0;
   }
   __syncthreads();
@@ -429,40 +429,54 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
   int64_t d_w = 0, d_mv = 0, d_c = 0, d_f = 0, d_bk = 0;
   if (tid == 0) s_prev_v = -1;
   // prime: the stages for k = 0 (edges + finish), 1 (edges), 2 (row), 3 (seq id)
-  auto advance = [&](int32_t k) {  // loads issued at step k, consumed one step later
+  // next-stage registers: loaded at step k (issue), moved into the stages only after the
+  // step's work (shift), so no register move waits on a load in flight
+  int32_t nd_v = -1, nd_ib = 0, nd_ie = 0, nd_p = -1, nd_dd = 0;
+  int64_t nd_w = 0, nd_mv = 0, nd_c = 0, nd_f = 0, nd_bk = 0;
+  int32_t nc_v = -1, nc_ib = 0, nc_ie = 0, nc_p = -1;
+  int64_t nc_w = 0, nc_mv = 0, nc_c = 0, nc_bk = 0;
+  int32_t nb_v = -1, nb_ib = 0, nb_ie = 0;
+  int64_t nb_w = 0, nb_mv = 0, nb_bk = 0;
+  int32_t ns_v = -1;
+  auto issue = [&](int32_t k) {  // loads issued at step k, consumed one step later
     // node k+1: finish / device of this thread's in-edge source (from stage c)
-    int32_t nd_v = c_v, nd_ib = c_ib, nd_ie = c_ie, nd_p = c_p, nd_dd = 0;
-    int64_t nd_w = c_w, nd_mv = c_mv, nd_c = c_c, nd_f = 0, nd_bk = c_bk;
+    nd_v = c_v; nd_ib = c_ib; nd_ie = c_ie; nd_p = c_p; nd_dd = 0;
+    nd_w = c_w; nd_mv = c_mv; nd_c = c_c; nd_f = 0; nd_bk = c_bk;
     if (nd_p >= 0) {
       nd_f = a.finish[nd_p];
       nd_dd = dev[nd_p];
     }
     // node k+2: this thread's in-edge (from stage b)
-    int32_t nc_v = b_v, nc_ib = b_ib, nc_ie = b_ie, nc_p = -1;
-    int64_t nc_w = b_w, nc_mv = b_mv, nc_c = 0, nc_bk = b_bk;
+    nc_v = b_v; nc_ib = b_ib; nc_ie = b_ie; nc_p = -1;
+    nc_w = b_w; nc_mv = b_mv; nc_c = 0; nc_bk = b_bk;
     if (nc_v >= 0 && nc_ib + tid < nc_ie) {
       nc_p = a.in_src[nc_ib + tid];
       nc_c = a.in_cost[nc_ib + tid];
     }
     // node k+3: row bounds, compute, memory (from stage s)
-    int32_t nb_v = s_v, nb_ib = 0, nb_ie = 0;
-    int64_t nb_w = 0, nb_mv = 0, nb_bk = 0;
+    nb_v = s_v; nb_ib = 0; nb_ie = 0;
+    nb_w = 0; nb_mv = 0; nb_bk = 0;
     if (nb_v >= 0) {
       nb_ib = a.in_off[nb_v];
       nb_ie = a.in_off[nb_v + 1];
       nb_w = a.w[nb_v];
       nb_mv = a.mem[nb_v];
-      if (tid == 0) nb_bk = a.back[nb_v];
+      if (lane == 0) nb_bk = a.back[nb_v];  // every warp decides (below)
     }
     // node k+4: id
-    const int32_t ns_v = k + 4 < n ? a.seq[k + 4] : -1;
+    ns_v = k + 4 < n ? a.seq[k + 4] : -1;
+  };
+  auto shift = [&] {
     d_v = nd_v; d_ib = nd_ib; d_ie = nd_ie; d_p = nd_p; d_dd = nd_dd; d_w = nd_w; d_mv = nd_mv; d_c = nd_c; d_f = nd_f;
     d_bk = nd_bk;
     c_v = nc_v; c_ib = nc_ib; c_ie = nc_ie; c_p = nc_p; c_w = nc_w; c_mv = nc_mv; c_c = nc_c; c_bk = nc_bk;
     b_v = nb_v; b_ib = nb_ib; b_ie = nb_ie; b_w = nb_w; b_mv = nb_mv; b_bk = nb_bk;
     s_v = ns_v;
   };
-  for (int32_t k = -4; k < 0; ++k) advance(k);  // after this: d = node 0, c = 1, b = 2, s = 3
+  for (int32_t k = -4; k < 0; ++k) {  // after this: d = node 0, c = 1, b = 2, s = 3
+    issue(k);
+    shift();
+  }
   __syncthreads();
   long long ph[6] = {0, 0, 0, 0, 0, 0}, tp = 0;
   auto mark = [&](int i) {
@@ -481,12 +495,11 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
     const int64_t my_c = d_c, my_f0 = d_f;
     const int32_t pv = s_prev_v;
     const int64_t pf = s_prev_finish;
-    advance(k);
-    for (int d = tid; d < D; d += blockDim.x) {
-      sA[d] = LLONG_MIN;
-      sB[d] = LLONG_MIN;
-    }
-    __syncthreads();
+    issue(k);
+    // available memory double-buffered by node parity: this node's decision reads one copy
+    // while its commit writes the other (no barrier between decision and commit)
+    int64_t* const avail = (k & 1) ? savail2 : savail;
+    int64_t* const avail_next = (k & 1) ? savail : savail2;
     mark(0);
     {
       // per-device maxima of the node's in-edges.  At most 32 (one warp): one device at a
@@ -541,7 +554,7 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
       if (sA[d] > pre) pre = sA[d];
       if (mb > pre) pre = mb;
       int64_t est = kNever;
-      if (savail[d] >= mv) est = tl_query(tl.view(d), sK[d], sg[d], sl[d], pre, w);
+      if (avail[d] >= mv) est = tl_query(tl.view(d), sK[d], sg[d], sl[d], pre, w);
       if (lane == 0) {
         sest[d] = est;
         spre[d] = pre;
@@ -549,13 +562,16 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
     }
     __syncthreads();
     mark(2);
-    if (tid == 0) {
+    // every warp takes the decision (placement.cpp:185-210) itself, so the chosen device's
+    // warp commits without another barrier
+    int32_t chosen = 0;
+    int64_t start = 0;
+    int be = 0;
+    if (lane == 0) {
       int32_t best = -1;
       for (int32_t d = 0; d < D; ++d)
-        if (savail[d] >= mv && (best < 0 || sest[d] < sest[best])) best = d;
-      int32_t chosen;
-      int64_t start = 0;
-      bool reloc = false, be = false;
+        if (avail[d] >= mv && (best < 0 || sest[d] < sest[best])) best = d;
+      bool reloc = false;
       if (best >= 0 && (sest[prev] == kNever || sest[prev] - sest[best] > back)) {
         chosen = best;
         start = sest[best];
@@ -564,43 +580,44 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
         chosen = prev;
         start = sest[prev];
       } else {
-        chosen = most_free(savail, D);
-        be = true;
+        chosen = most_free(avail, D);
+        be = 1;
         oom = true;
       }
-      if (a.decisions) {
+      if (a.decisions && warp == 0) {
         a.dec_prev[k] = prev;
         a.dec_back[k] = back;
         a.dec_chosen[k] = chosen;
         a.dec_reloc[k] = reloc;
-        a.dec_be[k] = be;
+        a.dec_be[k] = be != 0;
       }
-      s_chosen = chosen;
-      s_start = start;
-      s_be = be;
     }
-    __syncthreads();
-    mark(3);
+    chosen = __shfl_sync(FULL, chosen, 0);
+    start = __shfl_sync(FULL, start, 0);
+    be = __shfl_sync(FULL, be, 0);
+    for (int d = tid; d < D; d += blockDim.x) {  // the queries are done with this node's maxima
+      sA[d] = LLONG_MIN;
+      sB[d] = LLONG_MIN;
+    }
     if (a.decisions)
       for (int d = tid; d < D; d += blockDim.x) a.dec_est[(int64_t)k * D + d] = sest[d];
-    const int32_t chosen = s_chosen;
     if (warp == (chosen % nwarps)) {
       const TLView t = tl.view(chosen);
-      int64_t start = s_start;
-      if (s_be) start = tl_query(t, sK[chosen], sg[chosen], sl[chosen], spre[chosen], w);
+      if (be) start = tl_query(t, sK[chosen], sg[chosen], sl[chosen], spre[chosen], w);
       tl_insert(t, &sK[chosen], &sg[chosen], &sl[chosen], start, w);
+      for (int d = lane; d < D; d += 32) avail_next[d] = avail[d] - (d == chosen ? mv : 0);
       if (lane == 0) {
         a.finish[v] = start + w;
         dev[v] = chosen;
-        savail[chosen] -= mv;
         spdm[chosen] += mv;
         s_prev_finish = start + w;
         s_prev_v = v;
       }
     }
     prev = chosen;
+    shift();  // this step's loads have had the whole step to arrive
     __syncthreads();
-    mark(4);
+    mark(3);
   }
   if (a.debug && tid == 0)
     for (int i = 0; i < 5; ++i) a.debug[2 + i] = ph[i];
@@ -771,8 +788,8 @@ void place_launch(dp_ctx* ctx, PlaceJob* const* jobs, int count) {
       sync(ctx);
       fprintf(stderr, "[place] order_place %.2f ms, adjusting %.2f ms (n=%d, D=%d, meta %s)\n", h[0] / 1.965e6,
               h[1] / 1.965e6, j->a.n, j->a.D, j->a.meta_smem ? "smem" : "global");
-      fprintf(stderr, "[place] adjusting phases: loads %.2f, in-edges %.2f, find_slot %.2f, decide %.2f, commit %.2f ms\n",
-              h[2] / 1.965e6, h[3] / 1.965e6, h[4] / 1.965e6, h[5] / 1.965e6, h[6] / 1.965e6);
+      fprintf(stderr, "[place] adjusting phases: loads %.2f, in-edges %.2f, find_slot %.2f, decide+commit %.2f ms\n",
+              h[2] / 1.965e6, h[3] / 1.965e6, h[4] / 1.965e6, h[5] / 1.965e6);
     }
   }
 }
