@@ -94,3 +94,24 @@ def test_pipeline_batch_chunks_beyond_launch_width(gpu, ref):
     got = gpu.evaluate_pipeline_batch(gs, devs, GEN)
     for i, (g, r) in enumerate(zip(gs, got)):
         same_pipeline(r, ref.evaluate_pipeline(g, devs, GEN), f"batch12[{i}]")
+
+
+def test_batch_errors_in_order(gpu, ref):
+    """Validation and the generation windows are batched (one host sync per phase for the
+    whole call), yet the call fails with the error of the FIRST failing graph in call
+    order, as a loop of single calls would: a window-stage failure (NodeExceedsClusterLimit
+    in fuse) in graph 1 wins over a validation failure (CycleDetected) in graph 2, and vice
+    versa when the order is swapped."""
+    from paper_2208_00184_b200._abi import Graph
+    good = layered(62, 3000, 40)
+    heavy = layered(63, 2000, 40)
+    heavy.memory_bytes = heavy.memory_bytes.copy()
+    heavy.memory_bytes[5] = 10 ** 15
+    cyc = Graph(np.array([1, 2, 3]), np.array([5, 5, 5]), np.array([1, 1, 1]), np.array([1, 2, 3]),
+                np.array([2, 3, 1]), np.array([10, 10, 10]))
+    devs = devices(4, capacity_for(good, 4, 1.25))
+    for order, first in (([good, heavy, cyc], heavy), ([good, cyc, heavy], cyc), ([cyc, good, heavy], cyc)):
+        a = outcome(gpu.evaluate_pipeline_batch, order, devs, GEN)
+        b = outcome(ref.evaluate_pipeline, first, devs, GEN)
+        assert a[0] == b[0] == "err" and a[1:] == b[1:], (a, b)
+    same_pipeline(gpu.evaluate_pipeline_batch([good], devs, GEN)[0], ref.evaluate_pipeline(good, devs, GEN))
