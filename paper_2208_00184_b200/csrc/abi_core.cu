@@ -157,10 +157,21 @@ void levels_dev_chainlike_batch(DevGraph* const* gs, int count, dp_comm_t comm, 
   {
     StageScope st(ctx, "levels", bytes);
     std::vector<char> ok(count, 0);
-    if (!getenv("DP_LEVELS_KAHN")) ok = graphs_index_topological(gs, count);
+    bool flow = getenv("DP_LEVELS_FLOW") != nullptr;
+    for (int i = 0; i < count; ++i) flow = flow || coarse_flow_wanted(gs[i]->n);
     std::vector<DevGraph*> sg;
     std::vector<int64_t*> st_, sb;
-    for (int i = 0; i < count; ++i) {
+    if (flow) {  // the small ones still take the sweep (graphs_levels_indexorder decides)
+      std::vector<int64_t*> tp(count), bp(count);
+      for (int i = 0; i < count; ++i) {
+        tp[i] = t[i]->p;
+        bp[i] = b[i]->p;
+      }
+      ok = graphs_levels_indexorder(gs, count, tp.data(), bp.data());
+    } else if (!getenv("DP_LEVELS_KAHN")) {
+      ok = graphs_index_topological(gs, count);
+    }
+    for (int i = 0; i < count && !flow; ++i) {
       if (!ok[i]) continue;
       sg.push_back(gs[i]);
       st_.push_back(t[i]->p);

@@ -1019,6 +1019,8 @@ std::vector<char> graphs_index_topological(DevGraph* const* gs, int count, std::
   return ok;
 }
 
+bool coarse_flow_wanted(int32_t n) { return n > kSeqMaxN && getenv("DP_COARSE_FLOW") != nullptr; }
+
 // Levels when the node index order is topological (every edge u->v has u < v): the
 // one-CTA sweep for small or chain-like graphs (the coarse graph of fuse), the dataflow
 // kernel otherwise.  Returns false when the index order is not topological (caller uses
@@ -1036,7 +1038,7 @@ bool graph_levels_indexorder(DevGraph& g, int64_t* tlevel, int64_t* blevel, bool
   chk.download(h, 2);
   sync(ctx);
   if (static_cast<int>(h[0]) != 1) return false;
-  const bool sweep = (n <= kSeqMaxN || chainlike) && getenv("DP_LEVELS_FLOW") == nullptr;
+  const bool sweep = (n <= kSeqMaxN || (chainlike && !coarse_flow_wanted(n))) && getenv("DP_LEVELS_FLOW") == nullptr;
 
   if (sweep) {
     DevGraph* gs[1] = {&g};

@@ -93,6 +93,8 @@ Validation graph_validate_end(DevGraph& g, const dp_graph_t* h, ValState& vs, bo
 // Kahn frontier (level-synchronous, persistent cooperative kernel): fills order /
 // level_off / processed, and when requested tlevel / blevel (graph.cpp:228-261).
 bool graph_levels_indexorder(DevGraph& g, int64_t* tlevel, int64_t* blevel, bool chainlike);
+// a coarse (chain-like) graph of n nodes takes the dataflow kernel instead of the sweep
+bool coarse_flow_wanted(int32_t n);
 void graph_kahn(DevGraph& g, int64_t* tlevel, int64_t* blevel, int32_t* level_of);
 // Batched building blocks of the chain-like (coarse) levels of several graphs.
 void levels_sweep_launch(DevGraph* const* gs, int64_t* const* tlevel, int64_t* const* blevel, int count);

@@ -228,9 +228,19 @@ void resident_generate(Resident* const* rs, int count, bool with_ccr) {
   const bool dbg = getenv("DP_DEBUG_SYNC") != nullptr;
   const auto t0 = std::chrono::steady_clock::now();
   const int64_t s0 = ctx->sync_count;
-  if (!with_ccr) {
+  if (!with_ccr && count == 1) {
     resident_validate_batch(rs, count);
-    for (int i = 0; i < count; ++i) graph_costs(rs[i]->g, rs[i]->comm);
+    graph_costs(rs[0]->g, rs[0]->comm);
+  } else if (!with_ccr) {
+    std::vector<Validation> found;
+    resident_validate_batch(rs, count, &found);
+    for (int i = 0; i < count; ++i) {
+      if (found[i].code) {  // the earlier graphs' windows come first
+        if (i > 0) generate_windows(rs, i);
+        fail(found[i].code, "%s", found[i].message.c_str());
+      }
+      graph_costs(rs[i]->g, rs[i]->comm);
+    }
   } else {  // validation (pipeline.cpp:33) and ccr (:58), one round trip each for all the graphs
     std::vector<Validation> found;
     resident_validate_batch(rs, count, &found);
@@ -249,9 +259,13 @@ void resident_generate(Resident* const* rs, int count, bool with_ccr) {
     }
     sync(ctx);
     for (int i = 0; i < count; ++i) {  // errors graph by graph: its violation, then its ccr
-      if (found[i].code) fail(found[i].code, "%s", found[i].message.c_str());
       const int64_t tc = static_cast<int64_t>(h[2 * i]);
-      if (tc <= 0) fail(DP_E_ZERO_COMPUTE_TIME, "total compute time is zero");
+      if (found[i].code || tc <= 0) {
+        // the earlier graphs' windows come first (as in a loop of single calls)
+        if (i > 0) generate_windows(rs, i);
+        if (found[i].code) fail(found[i].code, "%s", found[i].message.c_str());
+        fail(DP_E_ZERO_COMPUTE_TIME, "total compute time is zero");
+      }
       rs[i]->original_ccr = static_cast<double>(static_cast<int64_t>(h[2 * i + 1])) / static_cast<double>(tc);
     }
   }
@@ -388,9 +402,16 @@ int dp_pipeline_batch(dp_ctx_t* ctx, int32_t count, const dp_graph_t* const* gra
   for (int32_t i = 0; i < count; ++i) {
     Resident* r = rp[i];
     if (!up.empty()) DP_CUDA(cudaStreamWaitEvent(ctx->stream, up[i], 0));
-    resident_validate(*r, true);
-    graph_costs(r->g, comm);
-    r->original_ccr = ccr_dev(r->g);
+    try {
+      resident_validate(*r, true);
+      graph_costs(r->g, comm);
+      r->original_ccr = ccr_dev(r->g);
+    } catch (const DpFail&) {
+      // a loop of single calls would have run the earlier graphs' windows first: their
+      // errors take precedence over this graph's
+      if (i > 0) generate_windows(rp.data(), i);
+      throw;
+    }
   }
   if (dbg) sync(ctx);
   const auto h2 = now();

@@ -93,6 +93,22 @@ __device__ __forceinline__ int64_t warp_incl_max(int64_t v) {
   return v;
 }
 
+// Full-warp 64-bit max / min: redux.sync on the high and low words of order-preserving
+// (sign-biased) values.  (Partial-mask redux is emulated in software on sm_100a.)
+__device__ __forceinline__ long long warp_max_i64(long long x) {
+  const uint64_t u = static_cast<uint64_t>(x) ^ 0x8000000000000000ull;
+  const uint32_t hi = __reduce_max_sync(FULL, static_cast<uint32_t>(u >> 32));
+  const uint32_t lo = __reduce_max_sync(FULL, static_cast<uint32_t>(u >> 32) == hi ? static_cast<uint32_t>(u) : 0u);
+  return static_cast<long long>(((static_cast<uint64_t>(hi) << 32) | lo) ^ 0x8000000000000000ull);
+}
+__device__ __forceinline__ long long warp_min_i64(long long x) {
+  const uint64_t u = static_cast<uint64_t>(x) ^ 0x8000000000000000ull;
+  const uint32_t hi = __reduce_min_sync(FULL, static_cast<uint32_t>(u >> 32));
+  const uint32_t lo =
+      __reduce_min_sync(FULL, static_cast<uint32_t>(u >> 32) == hi ? static_cast<uint32_t>(u) : 0xffffffffu);
+  return static_cast<long long>(((static_cast<uint64_t>(hi) << 32) | lo) ^ 0x8000000000000000ull);
+}
+
 struct BlockLoad {
   int64_t s, e, pm, pmprev;  // this lane's entry, PM at it, PM before it (with carry)
   int32_t c;
@@ -114,14 +130,80 @@ __device__ __forceinline__ BlockLoad tl_load(const TLView t, int32_t pos) {
   return r;
 }
 
+// Block at position pos whose id, count and carried-in PM are already known: one load.
+__device__ __forceinline__ BlockLoad tl_load_known(const TLView t, int32_t b, int32_t c, int64_t carry) {
+  const int lane = threadIdx.x & 31;
+  BlockLoad r;
+  r.c = c;
+  r.s = lane < c ? t.S[(int64_t)b * kTB + lane] : INT64_MAX;
+  r.e = lane < c ? t.E[(int64_t)b * kTB + lane] : INT64_MIN;
+  const int64_t inc = warp_incl_max(r.e);
+  r.pm = inc > carry ? inc : carry;
+  const int64_t up = __shfl_up_sync(FULL, r.pm, 1);
+  r.pmprev = lane == 0 ? carry : up;
+  return r;
+}
+
 // DeviceTimeline::find_slot(earliest, dur) (placement.cpp:13-21); warp-collective.
+// Nodes arrive in topological order, so `earliest` is nearly always inside the last 32
+// block positions: their meta comes in one round of independent loads (lane = position),
+// the block holding the first PM > earliest in a second, and the gap candidates after it
+// need only their entries.  Otherwise: a 32-ary search over all positions.
 __device__ int64_t tl_query(const TLView t, int32_t K, int64_t gmax, int64_t last, int64_t earliest, int64_t dur) {
   const int lane = threadIdx.x & 31;
   if (K == 0 || last <= earliest) return earliest;
   const int32_t nb = *t.nb;
-  // first interval with PM > earliest: its block is the first position with pmEnd > earliest
-  const int32_t j = warp_first_true(0, nb - 1, [&](int32_t q) { return t.pmEnd[q] > earliest; });
-  BlockLoad L = tl_load(t, j);
+  const int32_t lo = nb > 32 ? nb - 32 : 0;
+  const int32_t p = lo + lane;
+  const bool in = p < nb;
+  int64_t wpm = INT64_MAX, wgu = -1, wfe = 0, wfs = 0;
+  int32_t wid = 0, wc = 0;
+  if (in) {
+    wpm = t.pmEnd[p];
+    wgu = t.gub[p];
+    wfe = t.fE[p];
+    wfs = t.fS[p];
+    wid = t.id[p];
+    wc = t.cnt[p];
+  }
+  const int64_t pm_lo = lo > 0 ? t.pmEnd[lo - 1] : INT64_MIN;
+  if (pm_lo > earliest) {
+    // first interval with PM > earliest: its block is the first position with pmEnd > earliest
+    const int32_t j = warp_first_true(0, lo - 1, [&](int32_t q) { return t.pmEnd[q] > earliest; });
+    BlockLoad L = tl_load(t, j);
+    const int k0 = __ffs(__ballot_sync(FULL, lane < L.c && L.pm > earliest)) - 1;
+    const int64_t s0 = __shfl_sync(FULL, L.s, k0);
+    if (s0 >= earliest && s0 - earliest >= dur) return earliest;
+    if (gmax < dur) return last;
+    {
+      const bool fit = lane > k0 && lane < L.c && L.e > L.pmprev && L.s - L.pmprev >= dur;
+      const unsigned bal = __ballot_sync(FULL, fit);
+      if (bal) return __shfl_sync(FULL, L.pmprev, __ffs(bal) - 1);
+    }
+    for (int32_t p0 = j + 1; p0 < nb; p0 += 32) {
+      const int32_t q = p0 + lane;
+      bool cand = false;
+      if (q < nb) {
+        const int64_t pe = t.pmEnd[q - 1];
+        cand = t.gub[q] >= dur || (t.fE[q] > pe && t.fS[q] - pe >= dur);
+      }
+      unsigned bal = __ballot_sync(FULL, cand);
+      while (bal) {
+        const int32_t pos = p0 + __ffs(bal) - 1;
+        bal &= bal - 1;
+        L = tl_load(t, pos);
+        const bool fit = lane < L.c && L.e > L.pmprev && L.s - L.pmprev >= dur;
+        const unsigned b2 = __ballot_sync(FULL, fit);
+        if (b2) return __shfl_sync(FULL, L.pmprev, __ffs(b2) - 1);
+      }
+    }
+    return last;
+  }
+  // inside the window (pmEnd[nb - 1] = last > earliest)
+  const int64_t wup = __shfl_up_sync(FULL, wpm, 1);  // (every lane shuffles)
+  const int64_t wprev = lane == 0 ? pm_lo : wup;      // pmEnd[p - 1]
+  const int jl = __ffs(__ballot_sync(FULL, in && wpm > earliest)) - 1;
+  BlockLoad L = tl_load_known(t, __shfl_sync(FULL, wid, jl), __shfl_sync(FULL, wc, jl), __shfl_sync(FULL, wprev, jl));
   const int k0 = __ffs(__ballot_sync(FULL, lane < L.c && L.pm > earliest)) - 1;
   const int64_t s0 = __shfl_sync(FULL, L.s, k0);
   if (s0 >= earliest && s0 - earliest >= dur) return earliest;
@@ -131,22 +213,14 @@ __device__ int64_t tl_query(const TLView t, int32_t K, int64_t gmax, int64_t las
     const unsigned bal = __ballot_sync(FULL, fit);
     if (bal) return __shfl_sync(FULL, L.pmprev, __ffs(bal) - 1);
   }
-  for (int32_t p0 = j + 1; p0 < nb; p0 += 32) {
-    const int32_t p = p0 + lane;
-    bool cand = false;
-    if (p < nb) {
-      const int64_t pe = t.pmEnd[p - 1];
-      cand = t.gub[p] >= dur || (t.fE[p] > pe && t.fS[p] - pe >= dur);
-    }
-    unsigned bal = __ballot_sync(FULL, cand);
-    while (bal) {
-      const int32_t pos = p0 + __ffs(bal) - 1;
-      bal &= bal - 1;
-      L = tl_load(t, pos);
-      const bool fit = lane < L.c && L.e > L.pmprev && L.s - L.pmprev >= dur;
-      const unsigned b2 = __ballot_sync(FULL, fit);
-      if (b2) return __shfl_sync(FULL, L.pmprev, __ffs(b2) - 1);
-    }
+  unsigned bal = __ballot_sync(FULL, in && lane > jl && (wgu >= dur || (wfe > wprev && wfs - wprev >= dur)));
+  while (bal) {
+    const int q = __ffs(bal) - 1;
+    bal &= bal - 1;
+    L = tl_load_known(t, __shfl_sync(FULL, wid, q), __shfl_sync(FULL, wc, q), __shfl_sync(FULL, wprev, q));
+    const bool fit = lane < L.c && L.e > L.pmprev && L.s - L.pmprev >= dur;
+    const unsigned b2 = __ballot_sync(FULL, fit);
+    if (b2) return __shfl_sync(FULL, L.pmprev, __ffs(b2) - 1);
   }
   return last;
 }
@@ -210,6 +284,53 @@ __device__ void tl_insert(const TLView t, int32_t* Kp, int64_t* gmaxp, int64_t* 
     }
     __syncwarp();
     return;
+  }
+  {
+    // common case: s goes into the last block and it has room.  Its meta is rebuilt from
+    // registers (two dependent rounds of global accesses instead of a reload per step).
+    const int32_t jt = nb - 1;
+    const int64_t fst = t.fS[jt];
+    const int32_t b = t.id[jt], c = t.cnt[jt];
+    const int64_t carry = jt > 0 ? t.pmEnd[jt - 1] : INT64_MIN;
+    if (fst <= s && c < kTB) {
+      const int64_t vs = lane < c ? t.S[(int64_t)b * kTB + lane] : INT64_MAX;
+      const int64_t ve = lane < c ? t.E[(int64_t)b * kTB + lane] : INT64_MIN;
+      const int q = __popc(__ballot_sync(FULL, lane < c && vs <= s));
+      const int64_t us = __shfl_up_sync(FULL, vs, 1), ue = __shfl_up_sync(FULL, ve, 1);
+      const int64_t ns = lane < q ? vs : lane == q ? s : us;  // lanes > c: unused
+      const int64_t ne = lane < q ? ve : lane == q ? e : ue;
+      if (lane >= q && lane <= c) {
+        t.S[(int64_t)b * kTB + lane] = ns;
+        t.E[(int64_t)b * kTB + lane] = ne;
+      }
+      const int32_t c1 = c + 1;
+      const int64_t em = lane < c1 ? ne : INT64_MIN;
+      const int64_t inc = warp_incl_max(em);
+      const int64_t pv = __shfl_up_sync(FULL, inc, 1);
+      int64_t g = (lane >= 1 && lane < c1 && em > pv) ? ns - pv : -1;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const int64_t y = __shfl_xor_sync(FULL, g, o);
+        g = y > g ? y : g;
+      }
+      const int64_t mx = __shfl_sync(FULL, inc, 31);
+      const int64_t fs = __shfl_sync(FULL, ns, 0), fe = __shfl_sync(FULL, ne, 0);
+      int64_t gnew = g;  // + the block's first gap against its carry (tl_insert below)
+      if (jt > 0 && fe > carry && fs - carry > gnew) gnew = fs - carry;
+      if (lane == 0) {
+        t.cnt[jt] = c1;
+        t.maxE[jt] = mx;
+        t.fS[jt] = fs;
+        t.fE[jt] = fe;
+        t.gub[jt] = g;  // block-local, as tl_meta
+        t.pmEnd[jt] = carry > mx ? carry : mx;
+        if (gnew > *gmaxp) *gmaxp = gnew;
+        *lastp = last > e ? last : e;
+        *Kp = *Kp + 1;
+      }
+      __syncwarp();
+      return;
+    }
   }
   // target block: the last position whose first start <= s (entries with S <= s precede)
   int32_t j;
@@ -336,7 +457,7 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
   const PlaceArgs& a = batch.a[blockIdx.x >> 1];
   __shared__ int32_t sK[kMaxD], snb[kMaxD];
   __shared__ int64_t sg[kMaxD], sl[kMaxD], savail[kMaxD], spdm[kMaxD], savail2[kMaxD];
-  __shared__ long long sA[kMaxD], sB[kMaxD];
+  __shared__ long long sA[kMaxD], sB[kMaxD], sA2[kMaxD], sB2[kMaxD];
   __shared__ int64_t sest[kMaxD], spre[kMaxD];
   const int which = blockIdx.x & 1;  // 0 order_place, 1 adjusting_placement
   const long long t0 = clock64();
@@ -364,6 +485,8 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
     savail[d] = a.cap[d];
     sA[d] = LLONG_MIN;
     sB[d] = LLONG_MIN;
+    sA2[d] = LLONG_MIN;
+    sB2[d] = LLONG_MIN;
     spdm[d] = 0;
   }
   __syncthreads();
@@ -409,16 +532,23 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
   // adjusting_placement (placement.cpp:172-216)
   // The static inputs of a step are loaded in a software pipeline over the order, one
   // dependent stage per step, so no step waits on a chain of global loads: during step k
-  // the CTA loads node k+3's id, node k+2's row bounds / compute / memory, this thread's
-  // in-edge of node k+1 (source, cost) and the finish time / device of node k+1's source
-  // (final unless that source is node k, which is patched from shared memory at step k+1).
-  // In-edges beyond blockDim.x per node are read in the step itself.
-  __shared__ int64_t s_prev_finish;
-  __shared__ int32_t s_prev_v;
+  // the CTA loads node k+4's id, node k+3's row bounds / compute / memory / back cost, this
+  // thread's in-edge of node k+2 (source, cost) and the finish time / device of node
+  // k+1's source.  Two block barriers per node: X (in-edge maxima ready; the previous
+  // node's commit done) and Y (the per-device queries done).  Every warp takes the
+  // decision itself, then the commit warp inserts the node into its device's timeline
+  // while the other warps already reduce the next node's in-edges.  So a finish time /
+  // device loaded for node k+1 may predate the commits of nodes k-1 and k: every thread
+  // keeps those two (it took their decisions) and patches them in.  In-edges beyond
+  // blockDim.x per node are read in the step itself (node k-1 committed by then).
+  __shared__ int64_t s_be_start;
   int32_t prev = 0;
   bool oom = false;
   const int32_t n = a.n;
   const int T = blockDim.x;
+  const int cw = nwarps - 1;  // the commit warp (warp 0 holds the in-edges of small rows)
+  int32_t v1 = -1, dv1 = 0, v2 = -1, dv2 = 0;  // nodes k-1, k-2: index, device, finish
+  int64_t f1 = 0, f2 = 0;
   // stage registers: s (seq id), b (row), c (edge), d (edge with finish/device)
   int32_t s_v = -1;
   int32_t b_v = -1, b_ib = 0, b_ie = 0;
@@ -427,8 +557,6 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
   int64_t c_w = 0, c_mv = 0, c_c = 0, c_bk = 0;
   int32_t d_v = -1, d_ib = 0, d_ie = 0, d_p = -1, d_dd = 0;
   int64_t d_w = 0, d_mv = 0, d_c = 0, d_f = 0, d_bk = 0;
-  if (tid == 0) s_prev_v = -1;
-  // prime: the stages for k = 0 (edges + finish), 1 (edges), 2 (row), 3 (seq id)
   // next-stage registers: loaded at step k (issue), moved into the stages only after the
   // step's work (shift), so no register move waits on a load in flight
   int32_t nd_v = -1, nd_ib = 0, nd_ie = 0, nd_p = -1, nd_dd = 0;
@@ -438,6 +566,12 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
   int32_t nb_v = -1, nb_ib = 0, nb_ie = 0;
   int64_t nb_w = 0, nb_mv = 0, nb_bk = 0;
   int32_t ns_v = -1;
+  // 0, but opaque to the compiler's uniformity analysis: the pipelined node loads then
+  // count as per-thread values and stay in vector registers.  With a provably uniform
+  // address the loaded row / weight / memory go to uniform registers, and the R2UR that
+  // moves them there waits for the load right where it is issued (~1.5 us per node).
+  // (threadIdx.x < blockDim.x <= 1024 < n + 4096, which ptxas cannot fold: n is a parameter)
+  const int32_t divz = static_cast<uint32_t>(tid) >= static_cast<uint32_t>(a.n) + 4096u ? 1 : 0;
   auto issue = [&](int32_t k) {  // loads issued at step k, consumed one step later
     // node k+1: finish / device of this thread's in-edge source (from stage c)
     nd_v = c_v; nd_ib = c_ib; nd_ie = c_ie; nd_p = c_p; nd_dd = 0;
@@ -453,7 +587,7 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
       nc_p = a.in_src[nc_ib + tid];
       nc_c = a.in_cost[nc_ib + tid];
     }
-    // node k+3: row bounds, compute, memory (from stage s)
+    // node k+3: row bounds, compute, memory, back cost (from stage s)
     nb_v = s_v; nb_ib = 0; nb_ie = 0;
     nb_w = 0; nb_mv = 0; nb_bk = 0;
     if (nb_v >= 0) {
@@ -461,10 +595,10 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
       nb_ie = a.in_off[nb_v + 1];
       nb_w = a.w[nb_v];
       nb_mv = a.mem[nb_v];
-      if (lane == 0) nb_bk = a.back[nb_v];  // every warp decides (below)
+      nb_bk = a.back[nb_v];
     }
     // node k+4: id
-    ns_v = k + 4 < n ? a.seq[k + 4] : -1;
+    ns_v = k + 4 < n ? a.seq[k + 4 + divz] : -1;
   };
   auto shift = [&] {
     d_v = nd_v; d_ib = nd_ib; d_ie = nd_ie; d_p = nd_p; d_dd = nd_dd; d_w = nd_w; d_mv = nd_mv; d_c = nd_c; d_f = nd_f;
@@ -493,13 +627,14 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
     // this step's inputs, then the next steps' loads (consumed from step k+1 on)
     const int32_t my_p = d_p, my_dd0 = d_dd, ib = d_ib, ie = d_ie;
     const int64_t my_c = d_c, my_f0 = d_f;
-    const int32_t pv = s_prev_v;
-    const int64_t pf = s_prev_finish;
     issue(k);
-    // available memory double-buffered by node parity: this node's decision reads one copy
-    // while its commit writes the other (no barrier between decision and commit)
+    // available memory and the in-edge maxima double-buffered by node parity: the commit of
+    // node k-1 writes one copy while node k's decision reads the other, and node k's in-edge
+    // reduction fills one pair of maxima while the other is reset after node k-1's queries
     int64_t* const avail = (k & 1) ? savail2 : savail;
     int64_t* const avail_next = (k & 1) ? savail : savail2;
+    long long* const cA = (k & 1) ? sA2 : sA;
+    long long* const cB = (k & 1) ? sB2 : sB;
     mark(0);
     {
       // per-device maxima of the node's in-edges.  At most 32 (one warp): one device at a
@@ -507,19 +642,19 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
       // on order-preserving words), one shared-memory update per device instead of a
       // contended CAS per edge; more: a CAS per edge (spread over several warps)
       const bool act = my_p >= 0;
-      const bool fresh = act && my_p == pv;  // placed in the previous step: loaded before its commit
-      const int64_t f = fresh ? pf : my_f0;
-      const int32_t dd = fresh ? prev : my_dd0;
-      auto wmax = [](int64_t x) {
-        const uint64_t u = static_cast<uint64_t>(x) ^ 0x8000000000000000ull;
-        const uint32_t hi = __reduce_max_sync(FULL, static_cast<uint32_t>(u >> 32));
-        const uint32_t lo = __reduce_max_sync(FULL, static_cast<uint32_t>(u >> 32) == hi ? static_cast<uint32_t>(u) : 0u);
-        return static_cast<long long>(((static_cast<uint64_t>(hi) << 32) | lo) ^ 0x8000000000000000ull);
-      };
+      int64_t f = my_f0;
+      int32_t dd = my_dd0;
+      if (my_p == v1) {
+        f = f1;
+        dd = dv1;
+      } else if (my_p == v2) {
+        f = f2;
+        dd = dv2;
+      }
       if (ie - ib > 32) {  // in-edges over several warps (wide coarse graphs): per-edge updates
         if (act) {
-          atomicMax(&sA[dd], static_cast<long long>(f));
-          atomicMax(&sB[dd], static_cast<long long>(f + my_c));
+          atomicMax(&cA[dd], static_cast<long long>(f));
+          atomicMax(&cB[dd], static_cast<long long>(f + my_c));
         }
       }
       unsigned todo = ie - ib > 32 ? 0u : __ballot_sync(FULL, act);
@@ -528,30 +663,34 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
         const int32_t d = __shfl_sync(FULL, dd, leader);
         const bool mine = act && dd == d;
         todo &= ~__ballot_sync(FULL, mine);
-        const long long ga = wmax(mine ? f : LLONG_MIN), gb = wmax(mine ? f + my_c : LLONG_MIN);
+        const long long ga = warp_max_i64(mine ? f : LLONG_MIN), gb = warp_max_i64(mine ? f + my_c : LLONG_MIN);
         if (lane == leader) {
-          atomicMax(&sA[d], ga);
-          atomicMax(&sB[d], gb);
+          atomicMax(&cA[d], ga);
+          atomicMax(&cB[d], gb);
         }
       }
     }
     for (int32_t q = ib + T + tid; q < ie; q += T) {
       const int32_t p = a.in_src[q];
-      const int64_t f = a.finish[p];
-      const int32_t dd = dev[p];
-      atomicMax(&sA[dd], static_cast<long long>(f));
-      atomicMax(&sB[dd], static_cast<long long>(f + a.in_cost[q]));
+      int64_t f = a.finish[p];
+      int32_t dd = dev[p];
+      if (p == v1) {
+        f = f1;
+        dd = dv1;
+      }
+      atomicMax(&cA[dd], static_cast<long long>(f));
+      atomicMax(&cB[dd], static_cast<long long>(f + a.in_cost[q]));
     }
-    __syncthreads();
+    __syncthreads();  // X
     mark(1);
     for (int32_t d = warp; d < D; d += nwarps) {
       long long mb = LLONG_MIN;
       for (int32_t x = lane; x < D; x += 32)
-        if (x != d) mb = max(mb, sB[x]);
+        if (x != d) mb = max(mb, cB[x]);
 #pragma unroll
       for (int o = 16; o; o >>= 1) mb = max(mb, __shfl_xor_sync(FULL, mb, o));
       int64_t pre = 0;
-      if (sA[d] > pre) pre = sA[d];
+      if (cA[d] > pre) pre = cA[d];
       if (mb > pre) pre = mb;
       int64_t est = kNever;
       if (avail[d] >= mv) est = tl_query(tl.view(d), sK[d], sg[d], sl[d], pre, w);
@@ -560,65 +699,81 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
         spre[d] = pre;
       }
     }
-    __syncthreads();
+    __syncthreads();  // Y
     mark(2);
-    // every warp takes the decision (placement.cpp:185-210) itself, so the chosen device's
-    // warp commits without another barrier
-    int32_t chosen = 0;
-    int64_t start = 0;
-    int be = 0;
-    if (lane == 0) {
-      int32_t best = -1;
-      for (int32_t d = 0; d < D; ++d)
-        if (avail[d] >= mv && (best < 0 || sest[d] < sest[best])) best = d;
-      bool reloc = false;
-      if (best >= 0 && (sest[prev] == kNever || sest[prev] - sest[best] > back)) {
-        chosen = best;
-        start = sest[best];
-        reloc = chosen != prev;
-      } else if (sest[prev] != kNever) {
-        chosen = prev;
-        start = sest[prev];
-      } else {
-        chosen = most_free(avail, D);
-        be = 1;
-        oom = true;
-      }
-      if (a.decisions && warp == 0) {
-        a.dec_prev[k] = prev;
-        a.dec_back[k] = back;
-        a.dec_chosen[k] = chosen;
-        a.dec_reloc[k] = reloc;
-        a.dec_be[k] = be != 0;
+    // the decision (placement.cpp:185-210), by every warp (lanes = devices): best = the
+    // lowest position among the feasible devices with the least est
+    int32_t best = -1;
+    int64_t bestv = kNever;
+    for (int32_t d0 = 0; d0 < D; d0 += 32) {
+      const int32_t d = d0 + lane;
+      const bool ok = d < D && avail[d] >= mv;
+      const int64_t e = ok ? sest[d] : kNever;
+      const int64_t m = warp_min_i64(e);
+      const unsigned hit = __ballot_sync(FULL, ok && e == m);
+      if (hit && (best < 0 || m < bestv)) {
+        best = d0 + __ffs(hit) - 1;
+        bestv = m;
       }
     }
-    chosen = __shfl_sync(FULL, chosen, 0);
-    start = __shfl_sync(FULL, start, 0);
-    be = __shfl_sync(FULL, be, 0);
+    const int64_t ep = sest[prev];
+    int32_t chosen;
+    int64_t start = 0;
+    bool be = false, reloc = false;
+    if (best >= 0 && (ep == kNever || ep - bestv > back)) {
+      chosen = best;
+      start = bestv;
+      reloc = chosen != prev;
+    } else if (ep != kNever) {
+      chosen = prev;
+      start = ep;
+    } else {
+      chosen = most_free(avail, D);
+      be = true;
+      oom = true;
+    }
+    if (a.decisions && tid == 0) {
+      a.dec_prev[k] = prev;
+      a.dec_back[k] = back;
+      a.dec_chosen[k] = chosen;
+      a.dec_reloc[k] = reloc;
+      a.dec_be[k] = be;
+    }
     for (int d = tid; d < D; d += blockDim.x) {  // the queries are done with this node's maxima
-      sA[d] = LLONG_MIN;
-      sB[d] = LLONG_MIN;
+      cA[d] = LLONG_MIN;
+      cB[d] = LLONG_MIN;
     }
     if (a.decisions)
       for (int d = tid; d < D; d += blockDim.x) a.dec_est[(int64_t)k * D + d] = sest[d];
-    if (warp == (chosen % nwarps)) {
+    if (be) {  // block-uniform: the start needs a query on the most free device
+      if (warp == cw) {
+        start = tl_query(tl.view(chosen), sK[chosen], sg[chosen], sl[chosen], spre[chosen], w);
+        if (lane == 0) s_be_start = start;
+      }
+      __syncthreads();
+      start = s_be_start;
+    }
+    if (warp == cw) {
       const TLView t = tl.view(chosen);
-      if (be) start = tl_query(t, sK[chosen], sg[chosen], sl[chosen], spre[chosen], w);
       tl_insert(t, &sK[chosen], &sg[chosen], &sl[chosen], start, w);
       for (int d = lane; d < D; d += 32) avail_next[d] = avail[d] - (d == chosen ? mv : 0);
       if (lane == 0) {
         a.finish[v] = start + w;
         dev[v] = chosen;
         spdm[chosen] += mv;
-        s_prev_finish = start + w;
-        s_prev_v = v;
       }
     }
+    v2 = v1;
+    dv2 = dv1;
+    f2 = f1;
+    v1 = v;
+    dv1 = chosen;
+    f1 = start + w;
     prev = chosen;
     shift();  // this step's loads have had the whole step to arrive
-    __syncthreads();
     mark(3);
   }
+  __syncthreads();  // the last commit
   if (a.debug && tid == 0)
     for (int i = 0; i < 5; ++i) a.debug[2 + i] = ph[i];
   for (int d = tid; d < D; d += blockDim.x) a.pdm[1][d] = spdm[d];
