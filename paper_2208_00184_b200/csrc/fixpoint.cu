@@ -111,6 +111,14 @@ __global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(
   if (tid == 0) a.lvl_off[0] = 0;
   __syncthreads();
   // ---- 1: breadth-first order s0 and the freeing forest T0
+  long long clk = clock64();  // phase clocks (DP_DEBUG_FIXPOINT): info[3..6], in 1,024 cycles
+  auto phase = [&](int i) {
+    if (tid == 0) {
+      const long long c = clock64();
+      a.info[3 + i] = static_cast<int>((c - clk) >> 10);
+      clk = c;
+    }
+  };
   int32_t lb = 0, le = nsrc, L = 0;
   while (lb < le) {
     if (tid == 0) a.lvl_off[L + 1] = le;
@@ -182,6 +190,7 @@ __global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(
   }
   if (tid == 0) a.cs[n] = n;
   __syncthreads();
+  phase(0);
   // ---- 2: subtree sizes of T0, by s0 position: position i's children are the contiguous
   // positions [cs[i], cs[i + 1]) of the next level (phase 1 numbered them so)
   int32_t* psize = a.psize;
@@ -221,6 +230,7 @@ __global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(
   }
   for (int32_t i = tid; i < n; i += TT::kThreads) a.pre[a.seq0[i]] = ppre[i];
   __syncthreads();
+  phase(1);
   // ---- 4: proof T(preorder(T0)) = T0
   bool bad = false;
   for (int32_t v = tid; v < n; v += TT::kThreads) {
@@ -232,7 +242,9 @@ __global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(
   }
   int32_t* pos = a.pre;
   int rounds = 1;
-  if (__syncthreads_or(bad)) {
+  const bool any_bad = __syncthreads_or(bad);
+  phase(2);
+  if (any_bad) {
     // general rounds s <- preorder(T(s)) on the same levels (a T(s) parent is a
     // predecessor, so it sits on a shallower level)
     int32_t budget = a.max_rounds;
@@ -306,6 +318,7 @@ __global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(
     a.pos_of[v] = p;
   }
   __syncthreads();
+  phase(3);
   if (tid == 0) {
     __threadfence();
     a.info[0] = 1;
@@ -393,7 +406,7 @@ std::unique_ptr<TreeJob> fixpoint_prepare(DevGraph& g, const int32_t* by_rank, c
   j->cs.alloc(ctx, (size_t)n + 1);
   j->psize.alloc(ctx, n);
   j->ppre.alloc(ctx, n);
-  j->info.alloc(ctx, 3);
+  j->info.alloc(ctx, 8);
   j->info.zero();
   TreeArgs& a = j->a;
   a.n = n;
@@ -442,13 +455,17 @@ void fixpoint_launch_batch(dp_ctx* ctx, TreeJob* const* jobs, int count) {
     else DP_LAUNCH(ctx, k_treepeel<TreeCfg<512>>, k, 512, 0, b);
   }
   if (getenv("DP_DEBUG_FIXPOINT")) {
-    std::vector<int> h(3 * (size_t)count);
-    for (int q = 0; q < count; ++q) jobs[q]->info.download(h.data() + 3 * q, 3);
+    std::vector<int> h(8 * (size_t)count);
+    for (int q = 0; q < count; ++q) jobs[q]->info.download(h.data() + 8 * q, 8);
     sync(ctx);
     for (int q = 0; q < count; ++q) {
-      fprintf(stderr, "[treepeel] n=%d status=%d levels=%d rounds=%d\n", jobs[q]->a.n, h[3 * q], h[3 * q + 1],
-              h[3 * q + 2]);
-      const int slot = h[3 * q] == 1 ? (h[3 * q + 2] == 1 ? 0 : 1) : h[3 * q];
+      const int* x = h.data() + 8 * q;
+      fprintf(stderr,
+              "[treepeel] n=%d status=%d levels=%d rounds=%d; ms: kahn %.2f, sizes+preorder %.2f, proof %.2f, "
+              "rounds+emit %.2f (at 1.965 GHz)\n",
+              jobs[q]->a.n, x[0], x[1], x[2], x[3] * 1024 / 1.965e6, x[4] * 1024 / 1.965e6, x[5] * 1024 / 1.965e6,
+              x[6] * 1024 / 1.965e6);
+      const int slot = x[0] == 1 ? (x[2] == 1 ? 0 : 1) : x[0];
       if (slot >= 0 && slot < 5) ++ctx->tree_stats[slot];
     }
   }

@@ -43,23 +43,51 @@ constexpr unsigned FULL = 0xffffffffu;
 // overall max end (zero-length intervals included).
 constexpr int kTB = 32;
 
+// With the meta in global memory (large coarse graphs) the gap scan of find_slot reads
+// G[p] = an upper bound of every gap of block p including its first one against the carry
+// (max(gub[p], fS[p] - pmEnd[p-1] when fE[p] > pmEnd[p-1])) and SG[P] = max G over the
+// 32 positions of super-block P, so a scan costs at most three dependent rounds; with the
+// meta in shared memory the scan reads gub / fS / fE directly (G, SG null).
 struct TLView {
   int64_t *S, *E;                                 // [maxb][kTB] by physical block id
   int32_t *id, *cnt;                              // [maxb] by position
   int64_t *maxE, *pmEnd, *fS, *fE, *gub;          // [maxb] by position
+  int64_t *G, *SG;                                // [maxb], [maxb / 32 + 1] (global meta only)
   int32_t* nb;                                    // blocks in use (shared memory)
 };
 
 struct TLArrays {
-  int64_t *S, *E, *maxE, *pmEnd, *fS, *fE, *gub;
+  int64_t *S, *E, *maxE, *pmEnd, *fS, *fE, *gub, *G, *SG;
   int32_t *id, *cnt;
   int32_t maxb;
   int32_t* nb;  // shared memory, set by the kernel
   __device__ TLView view(int d) const {
-    const int64_t eo = (int64_t)d * maxb * kTB, mo = (int64_t)d * maxb;
-    return TLView{S + eo, E + eo, id + mo, cnt + mo, maxE + mo, pmEnd + mo, fS + mo, fE + mo, gub + mo, nb + d};
+    const int64_t eo = (int64_t)d * maxb * kTB, mo = (int64_t)d * maxb, so = (int64_t)d * (maxb / 32 + 1);
+    return TLView{S + eo, E + eo, id + mo, cnt + mo, maxE + mo, pmEnd + mo, fS + mo, fE + mo, gub + mo,
+                  G ? G + mo : nullptr, SG ? SG + so : nullptr, nb + d};
   }
 };
+
+// G of position p >= 1 from its meta and the carry pmEnd[p - 1] (position 0 has no carry)
+__device__ __forceinline__ int64_t tl_gbound(int32_t p, int64_t gub, int64_t fs, int64_t fe, int64_t carry) {
+  return (p > 0 && fe > carry && fs - carry > gub) ? fs - carry : gub;
+}
+
+// SG of the super-blocks P0..P1 from G (warp-collective)
+__device__ void tl_sg(const TLView t, int32_t P0, int32_t P1, int32_t nb) {
+  const int lane = threadIdx.x & 31;
+  for (int32_t P = P0; P <= P1; ++P) {
+    const int32_t p = P * 32 + lane;
+    int64_t x = p < nb ? t.G[p] : -1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const int64_t y = __shfl_xor_sync(FULL, x, o);
+      x = y > x ? y : x;
+    }
+    if (lane == 0) t.SG[P] = x;
+  }
+  __syncwarp();
+}
 
 // First index in [lo, hi] whose predicate holds (monotone false...true; pred(hi) true).
 template <typename Pred>
@@ -149,10 +177,12 @@ __device__ __forceinline__ BlockLoad tl_load_known(const TLView t, int32_t b, in
 // block positions: their meta comes in one round of independent loads (lane = position),
 // the block holding the first PM > earliest in a second, and the gap candidates after it
 // need only their entries.  Otherwise: a 32-ary search over all positions.
-__device__ int64_t tl_query(const TLView t, int32_t K, int64_t gmax, int64_t last, int64_t earliest, int64_t dur) {
+__device__ int64_t tl_query(const TLView t, int32_t K, int64_t gmax, int64_t last, int64_t earliest, int64_t dur,
+                           int32_t* hint) {
   const int lane = threadIdx.x & 31;
-  if (K == 0 || last <= earliest) return earliest;
   const int32_t nb = *t.nb;
+  *hint = nb - 1;  // the block reserve() will insert into (a guess tl_insert checks)
+  if (K == 0 || last <= earliest) return earliest;
   const int32_t lo = nb > 32 ? nb - 32 : 0;
   const int32_t p = lo + lane;
   const bool in = p < nb;
@@ -173,12 +203,44 @@ __device__ int64_t tl_query(const TLView t, int32_t K, int64_t gmax, int64_t las
     BlockLoad L = tl_load(t, j);
     const int k0 = __ffs(__ballot_sync(FULL, lane < L.c && L.pm > earliest)) - 1;
     const int64_t s0 = __shfl_sync(FULL, L.s, k0);
-    if (s0 >= earliest && s0 - earliest >= dur) return earliest;
+    if (s0 >= earliest && s0 - earliest >= dur) {
+      *hint = k0 > 0 || j == 0 ? j : j - 1;
+      return earliest;
+    }
     if (gmax < dur) return last;
     {
       const bool fit = lane > k0 && lane < L.c && L.e > L.pmprev && L.s - L.pmprev >= dur;
       const unsigned bal = __ballot_sync(FULL, fit);
-      if (bal) return __shfl_sync(FULL, L.pmprev, __ffs(bal) - 1);
+      if (bal) {
+        *hint = j;
+        return __shfl_sync(FULL, L.pmprev, __ffs(bal) - 1);
+      }
+    }
+    if (t.G) {  // candidates by G, super-blocks by SG
+      int32_t P = j >> 5;
+      const int32_t Pn = (nb - 1) >> 5;
+      unsigned bal = __ballot_sync(FULL, P * 32 + lane > j && P * 32 + lane < nb && t.G[P * 32 + lane] >= dur);
+      for (;;) {
+        while (bal) {
+          const int32_t pos = P * 32 + __ffs(bal) - 1;
+          bal &= bal - 1;
+          L = tl_load(t, pos);
+          const bool fit = lane < L.c && L.e > L.pmprev && L.s - L.pmprev >= dur;
+          const unsigned b2 = __ballot_sync(FULL, fit);
+          if (b2) {
+            *hint = b2 & 1u ? pos - 1 : pos;
+            return __shfl_sync(FULL, L.pmprev, __ffs(b2) - 1);
+          }
+        }
+        int32_t nP = -1;
+        for (int32_t P0 = P + 1; P0 <= Pn && nP < 0; P0 += 32) {
+          const unsigned sb = __ballot_sync(FULL, P0 + lane <= Pn && t.SG[P0 + lane] >= dur);
+          if (sb) nP = P0 + __ffs(sb) - 1;
+        }
+        if (nP < 0) return last;
+        P = nP;
+        bal = __ballot_sync(FULL, P * 32 + lane < nb && t.G[P * 32 + lane] >= dur);
+      }
     }
     for (int32_t p0 = j + 1; p0 < nb; p0 += 32) {
       const int32_t q = p0 + lane;
@@ -194,7 +256,10 @@ __device__ int64_t tl_query(const TLView t, int32_t K, int64_t gmax, int64_t las
         L = tl_load(t, pos);
         const bool fit = lane < L.c && L.e > L.pmprev && L.s - L.pmprev >= dur;
         const unsigned b2 = __ballot_sync(FULL, fit);
-        if (b2) return __shfl_sync(FULL, L.pmprev, __ffs(b2) - 1);
+        if (b2) {
+          *hint = b2 & 1u ? pos - 1 : pos;
+          return __shfl_sync(FULL, L.pmprev, __ffs(b2) - 1);
+        }
       }
     }
     return last;
@@ -206,12 +271,19 @@ __device__ int64_t tl_query(const TLView t, int32_t K, int64_t gmax, int64_t las
   BlockLoad L = tl_load_known(t, __shfl_sync(FULL, wid, jl), __shfl_sync(FULL, wc, jl), __shfl_sync(FULL, wprev, jl));
   const int k0 = __ffs(__ballot_sync(FULL, lane < L.c && L.pm > earliest)) - 1;
   const int64_t s0 = __shfl_sync(FULL, L.s, k0);
-  if (s0 >= earliest && s0 - earliest >= dur) return earliest;
+  const int32_t jw = lo + jl;
+  if (s0 >= earliest && s0 - earliest >= dur) {
+    *hint = k0 > 0 || jw == 0 ? jw : jw - 1;
+    return earliest;
+  }
   if (gmax < dur) return last;
   {
     const bool fit = lane > k0 && lane < L.c && L.e > L.pmprev && L.s - L.pmprev >= dur;
     const unsigned bal = __ballot_sync(FULL, fit);
-    if (bal) return __shfl_sync(FULL, L.pmprev, __ffs(bal) - 1);
+    if (bal) {
+      *hint = jw;
+      return __shfl_sync(FULL, L.pmprev, __ffs(bal) - 1);
+    }
   }
   unsigned bal = __ballot_sync(FULL, in && lane > jl && (wgu >= dur || (wfe > wprev && wfs - wprev >= dur)));
   while (bal) {
@@ -220,14 +292,18 @@ __device__ int64_t tl_query(const TLView t, int32_t K, int64_t gmax, int64_t las
     L = tl_load_known(t, __shfl_sync(FULL, wid, q), __shfl_sync(FULL, wc, q), __shfl_sync(FULL, wprev, q));
     const bool fit = lane < L.c && L.e > L.pmprev && L.s - L.pmprev >= dur;
     const unsigned b2 = __ballot_sync(FULL, fit);
-    if (b2) return __shfl_sync(FULL, L.pmprev, __ffs(b2) - 1);
+    if (b2) {
+      *hint = b2 & 1u ? lo + q - 1 : lo + q;
+      return __shfl_sync(FULL, L.pmprev, __ffs(b2) - 1);
+    }
   }
   return last;
 }
 
 // Recomputes the meta of the block at position pos from its entries (warp-collective)
 // and propagates pmEnd forward while it changes.  Returns the block's gap upper bound.
-__device__ int64_t tl_meta(const TLView t, int32_t pos, int32_t nb, bool propagate = true) {
+// *ghi (optional): the last position whose G was rewritten.
+__device__ int64_t tl_meta(const TLView t, int32_t pos, int32_t nb, bool propagate = true, int32_t* ghi = nullptr) {
   const int lane = threadIdx.x & 31;
   const int32_t b = t.id[pos], c = t.cnt[pos];
   const int64_t s = lane < c ? t.S[(int64_t)b * kTB + lane] : INT64_MAX;
@@ -242,104 +318,51 @@ __device__ int64_t tl_meta(const TLView t, int32_t pos, int32_t nb, bool propaga
   }
   const int64_t mx = __shfl_sync(FULL, inc, 31);
   const int64_t fs = __shfl_sync(FULL, s, 0), fe = __shfl_sync(FULL, e, 0);
+  int32_t last_g = pos;
   if (lane == 0) {
     t.maxE[pos] = mx;
     t.fS[pos] = fs;
     t.fE[pos] = fe;
     t.gub[pos] = g;
-    int64_t pm = pos > 0 && t.pmEnd[pos - 1] > mx ? t.pmEnd[pos - 1] : mx;
+    const int64_t carry = pos > 0 ? t.pmEnd[pos - 1] : INT64_MIN;
+    int64_t pm = carry > mx ? carry : mx;
     t.pmEnd[pos] = pm;
+    int32_t lc = pos;  // the last position whose pmEnd was rewritten
     for (int32_t q = pos + 1; propagate && q < nb; ++q) {  // forward while it changes
       const int64_t np = t.maxE[q] > pm ? t.maxE[q] : pm;
       if (np == t.pmEnd[q]) break;
       t.pmEnd[q] = np;
       pm = np;
+      lc = q;
+    }
+    if (t.G) {  // G depends on the block and its carry: pos, and every q whose carry changed
+      t.G[pos] = tl_gbound(pos, g, fs, fe, carry);
+      if (propagate) {
+        last_g = min(lc + 1, nb - 1);
+        for (int32_t q = pos + 1; q <= last_g; ++q)
+          t.G[q] = tl_gbound(q, t.gub[q], t.fS[q], t.fE[q], t.pmEnd[q - 1]);
+      }
     }
   }
+  last_g = __shfl_sync(FULL, last_g, 0);
+  if (ghi) *ghi = last_g;
   __syncwarp();
   return g;
 }
 
-// DeviceTimeline::reserve(start, dur) (placement.cpp:23-32): upper_bound insert.
-__device__ void tl_insert(const TLView t, int32_t* Kp, int64_t* gmaxp, int64_t* lastp, int64_t s, int64_t dur) {
+// DeviceTimeline::reserve(start, dur) (placement.cpp:23-32): upper_bound insert into the
+// last block whose first start <= s.  Block splits (a full target block) take
+// tl_insert_split; every other insert is done from registers: one round of meta loads at
+// the target (guessed by the query: `hint`, checked here), one for the block's entries,
+// then the stores (the block's meta rebuilt from the entries in registers, the prefix
+// maxima propagated only when the block's own changed).
+__device__ void tl_insert_split(const TLView t, int32_t* Kp, int64_t* gmaxp, int64_t* lastp, int64_t s, int64_t dur,
+                                int32_t nb, int32_t j0) {
   const int lane = threadIdx.x & 31;
   const int64_t e = s + dur;
-  int32_t nb = *t.nb;
   const int64_t last = *lastp;
   int64_t gnew = -1;  // gaps this insert may create (upper bound bookkeeping)
-  if (nb == 0) {
-    if (lane == 0) {
-      t.id[0] = 0;
-      t.cnt[0] = 1;
-      t.S[0] = s;
-      t.E[0] = e;
-      t.maxE[0] = e;
-      t.pmEnd[0] = e;
-      t.fS[0] = s;
-      t.fE[0] = e;
-      t.gub[0] = -1;
-      *t.nb = 1;
-      *Kp = 1;
-      *lastp = e;
-    }
-    __syncwarp();
-    return;
-  }
-  {
-    // common case: s goes into the last block and it has room.  Its meta is rebuilt from
-    // registers (two dependent rounds of global accesses instead of a reload per step).
-    const int32_t jt = nb - 1;
-    const int64_t fst = t.fS[jt];
-    const int32_t b = t.id[jt], c = t.cnt[jt];
-    const int64_t carry = jt > 0 ? t.pmEnd[jt - 1] : INT64_MIN;
-    if (fst <= s && c < kTB) {
-      const int64_t vs = lane < c ? t.S[(int64_t)b * kTB + lane] : INT64_MAX;
-      const int64_t ve = lane < c ? t.E[(int64_t)b * kTB + lane] : INT64_MIN;
-      const int q = __popc(__ballot_sync(FULL, lane < c && vs <= s));
-      const int64_t us = __shfl_up_sync(FULL, vs, 1), ue = __shfl_up_sync(FULL, ve, 1);
-      const int64_t ns = lane < q ? vs : lane == q ? s : us;  // lanes > c: unused
-      const int64_t ne = lane < q ? ve : lane == q ? e : ue;
-      if (lane >= q && lane <= c) {
-        t.S[(int64_t)b * kTB + lane] = ns;
-        t.E[(int64_t)b * kTB + lane] = ne;
-      }
-      const int32_t c1 = c + 1;
-      const int64_t em = lane < c1 ? ne : INT64_MIN;
-      const int64_t inc = warp_incl_max(em);
-      const int64_t pv = __shfl_up_sync(FULL, inc, 1);
-      int64_t g = (lane >= 1 && lane < c1 && em > pv) ? ns - pv : -1;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const int64_t y = __shfl_xor_sync(FULL, g, o);
-        g = y > g ? y : g;
-      }
-      const int64_t mx = __shfl_sync(FULL, inc, 31);
-      const int64_t fs = __shfl_sync(FULL, ns, 0), fe = __shfl_sync(FULL, ne, 0);
-      int64_t gnew = g;  // + the block's first gap against its carry (tl_insert below)
-      if (jt > 0 && fe > carry && fs - carry > gnew) gnew = fs - carry;
-      if (lane == 0) {
-        t.cnt[jt] = c1;
-        t.maxE[jt] = mx;
-        t.fS[jt] = fs;
-        t.fE[jt] = fe;
-        t.gub[jt] = g;  // block-local, as tl_meta
-        t.pmEnd[jt] = carry > mx ? carry : mx;
-        if (gnew > *gmaxp) *gmaxp = gnew;
-        *lastp = last > e ? last : e;
-        *Kp = *Kp + 1;
-      }
-      __syncwarp();
-      return;
-    }
-  }
-  // target block: the last position whose first start <= s (entries with S <= s precede)
-  int32_t j;
-  if (t.fS[nb - 1] <= s) {
-    j = nb - 1;
-  } else {
-    j = warp_first_true(0, nb - 1, [&](int32_t q) { return t.fS[q] > s; }) - 1;
-    if (j < 0) j = 0;
-  }
+  int32_t j = j0, sg_lo = j0, sg_hi = -1;
   if (t.cnt[j] == kTB) {  // split in halves: the upper half moves to a new block after j
     const int32_t nbid = nb;  // ids are allocated densely: the next free id is nb
     const int32_t b = t.id[j];
@@ -352,15 +375,17 @@ __device__ void tl_insert(const TLView t, int32_t* Kp, int64_t* gmaxp, int64_t* 
       const int32_t lo = max(j + 1, top - 32);
       const int32_t q = lo + lane;
       int32_t vi = 0, vc = 0;
-      int64_t m1 = 0, m2 = 0, m3 = 0, m4 = 0, m5 = 0;
+      int64_t m1 = 0, m2 = 0, m3 = 0, m4 = 0, m5 = 0, m6 = 0;
       const bool act = q < top;
       if (act) {
         vi = t.id[q]; vc = t.cnt[q]; m1 = t.maxE[q]; m2 = t.pmEnd[q]; m3 = t.fS[q]; m4 = t.fE[q]; m5 = t.gub[q];
+        if (t.G) m6 = t.G[q];
       }
       __syncwarp();
       if (act) {
         t.id[q + 1] = vi; t.cnt[q + 1] = vc; t.maxE[q + 1] = m1; t.pmEnd[q + 1] = m2; t.fS[q + 1] = m3;
         t.fE[q + 1] = m4; t.gub[q + 1] = m5;
+        if (t.G) t.G[q + 1] = m6;
       }
       __syncwarp();
     }
@@ -371,9 +396,10 @@ __device__ void tl_insert(const TLView t, int32_t* Kp, int64_t* gmaxp, int64_t* 
       t.pmEnd[j + 1] = t.pmEnd[j];  // placeholder until tl_meta below
       *t.nb = ++nb;
     }
-    __syncwarp();
+    nb = __shfl_sync(FULL, nb, 0);  // every lane's bound (tl_sg loops over it)
     tl_meta(t, j, nb, false);  // position j + 1 is not valid yet: no propagation
     tl_meta(t, j + 1, nb);
+    sg_hi = nb - 1;  // every later position moved
     if (t.fS[j + 1] <= s) ++j;
   }
   // insert into block j at the upper_bound position
@@ -392,7 +418,9 @@ __device__ void tl_insert(const TLView t, int32_t* Kp, int64_t* gmaxp, int64_t* 
   }
   if (lane == 0) t.cnt[j] = c + 1;
   __syncwarp();
-  gnew = tl_meta(t, j, nb);
+  int32_t ghi;
+  gnew = tl_meta(t, j, nb, true, &ghi);
+  if (t.G) tl_sg(t, sg_lo >> 5, max(sg_hi, ghi) >> 5, nb);
   // the next block's first gap may have changed (its carry in); count it in the bound
   if (j + 1 < nb) {
     const int64_t pe = t.pmEnd[j];
@@ -411,6 +439,144 @@ __device__ void tl_insert(const TLView t, int32_t* Kp, int64_t* gmaxp, int64_t* 
     if (gnew > *gmaxp) *gmaxp = gnew;
     *lastp = last > e ? last : e;
     *Kp = *Kp + 1;
+  }
+  __syncwarp();
+}
+
+
+__device__ void tl_insert(const TLView t, int32_t* Kp, int64_t* gmaxp, int64_t* lastp, int64_t s, int64_t dur,
+                          int32_t hint) {
+  const int lane = threadIdx.x & 31;
+  const int64_t e = s + dur;
+  const int32_t nb = *t.nb;
+  const int64_t last = *lastp;
+  if (nb == 0) {
+    if (lane == 0) {
+      t.id[0] = 0;
+      t.cnt[0] = 1;
+      t.S[0] = s;
+      t.E[0] = e;
+      t.maxE[0] = e;
+      t.pmEnd[0] = e;
+      t.fS[0] = s;
+      t.fE[0] = e;
+      t.gub[0] = -1;
+      if (t.G) {
+        t.G[0] = -1;
+        t.SG[0] = -1;
+      }
+      *t.nb = 1;
+      *Kp = 1;
+      *lastp = e;
+    }
+    __syncwarp();
+    return;
+  }
+  // target j: the last position with fS <= s (position 0 when s precedes everything)
+  int32_t j = hint >= 0 && hint < nb ? hint : nb - 1;
+  struct Row {
+    int64_t fs, fs1, fe1, carry, pm;
+    int32_t id, c;
+  };
+  auto load = [&](int32_t q) {
+    Row r;
+    r.fs = t.fS[q];
+    r.fs1 = q + 1 < nb ? t.fS[q + 1] : INT64_MAX;
+    r.fe1 = q + 1 < nb ? t.fE[q + 1] : 0;
+    r.carry = q > 0 ? t.pmEnd[q - 1] : INT64_MIN;
+    r.pm = t.pmEnd[q];
+    r.id = t.id[q];
+    r.c = t.cnt[q];
+    return r;
+  };
+  Row r = load(j);
+  if (!((j == 0 || r.fs <= s) && r.fs1 > s)) {
+    if (t.fS[nb - 1] <= s) {
+      j = nb - 1;
+    } else {
+      j = warp_first_true(0, nb - 1, [&](int32_t q) { return t.fS[q] > s; }) - 1;
+      if (j < 0) j = 0;
+    }
+    r = load(j);
+  }
+  if (r.c == kTB) {
+    tl_insert_split(t, Kp, gmaxp, lastp, s, dur, nb, j);
+    return;
+  }
+  const int32_t gp = (j & ~31) + lane;
+  const int64_t gsb = t.G && gp < nb ? t.G[gp] : -1;  // G of j's super-block
+  const int32_t b = r.id, c = r.c;
+  const int64_t vs = lane < c ? t.S[(int64_t)b * kTB + lane] : INT64_MAX;
+  const int64_t ve = lane < c ? t.E[(int64_t)b * kTB + lane] : INT64_MIN;
+  const int q = __popc(__ballot_sync(FULL, lane < c && vs <= s));
+  const int64_t us = __shfl_up_sync(FULL, vs, 1), ue = __shfl_up_sync(FULL, ve, 1);
+  const int64_t ns = lane < q ? vs : lane == q ? s : us;  // lanes > c: unused
+  const int64_t ne = lane < q ? ve : lane == q ? e : ue;
+  if (lane >= q && lane <= c) {
+    t.S[(int64_t)b * kTB + lane] = ns;
+    t.E[(int64_t)b * kTB + lane] = ne;
+  }
+  const int32_t c1 = c + 1;
+  const int64_t em = lane < c1 ? ne : INT64_MIN;
+  const int64_t inc = warp_incl_max(em);
+  const int64_t pv = __shfl_up_sync(FULL, inc, 1);
+  int64_t g = (lane >= 1 && lane < c1 && em > pv) ? ns - pv : -1;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const int64_t y = __shfl_xor_sync(FULL, g, o);
+    g = y > g ? y : g;
+  }
+  const int64_t mx = __shfl_sync(FULL, inc, 31);
+  const int64_t fs = __shfl_sync(FULL, ns, 0), fe = __shfl_sync(FULL, ne, 0);
+  const int64_t pmn = r.carry > mx ? r.carry : mx;
+  const int64_t gj = tl_gbound(j, g, fs, fe, r.carry);  // the block's gaps + its first one
+  // + the next block's first gap (its carry is this block's prefix max)
+  int64_t gnew = gj;
+  if (j + 1 < nb && r.fe1 > pmn && r.fs1 - pmn > gnew) gnew = r.fs1 - pmn;
+  int32_t lc = j;  // the last position whose prefix max changed
+  if (lane == 0) {
+    t.cnt[j] = c1;
+    t.maxE[j] = mx;
+    t.fS[j] = fs;
+    t.fE[j] = fe;
+    t.gub[j] = g;  // block-local, as tl_meta
+    t.pmEnd[j] = pmn;
+    if (pmn != r.pm) {  // forward while it changes
+      int64_t pm = pmn;
+      for (int32_t x = j + 1; x < nb; ++x) {
+        const int64_t np = t.maxE[x] > pm ? t.maxE[x] : pm;
+        if (np == t.pmEnd[x]) break;
+        t.pmEnd[x] = np;
+        pm = np;
+        lc = x;
+      }
+    }
+    if (gnew > *gmaxp) *gmaxp = gnew;
+    *lastp = last > e ? last : e;
+    *Kp = *Kp + 1;
+  }
+  if (t.G) {
+    lc = __shfl_sync(FULL, lc, 0);
+    if (pmn == r.pm) {  // only G[j] changed: its super-block's max from the loaded values
+      int64_t x = gp == j ? gj : gsb;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const int64_t y = __shfl_xor_sync(FULL, x, o);
+        x = y > x ? y : x;
+      }
+      if (lane == 0) {
+        t.G[j] = gj;
+        t.SG[j >> 5] = x;
+      }
+    } else {  // the carries of j+1 .. lc+1 changed too
+      const int32_t hi = min(lc + 1, nb - 1);
+      if (lane == 0) {
+        t.G[j] = gj;
+        for (int32_t x = j + 1; x <= hi; ++x) t.G[x] = tl_gbound(x, t.gub[x], t.fS[x], t.fE[x], t.pmEnd[x - 1]);
+      }
+      __syncwarp();
+      tl_sg(t, j >> 5, hi >> 5, nb);
+    }
   }
   __syncwarp();
 }
@@ -459,6 +625,7 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
   __shared__ int64_t sg[kMaxD], sl[kMaxD], savail[kMaxD], spdm[kMaxD], savail2[kMaxD];
   __shared__ long long sA[kMaxD], sB[kMaxD], sA2[kMaxD], sB2[kMaxD];
   __shared__ int64_t sest[kMaxD], spre[kMaxD];
+  __shared__ int32_t shint[kMaxD];
   const int which = blockIdx.x & 1;  // 0 order_place, 1 adjusting_placement
   const long long t0 = clock64();
   if (!a.run[which]) return;
@@ -476,6 +643,8 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
     tl.gub = dyn + 4 * mc;
     tl.id = reinterpret_cast<int32_t*>(dyn + 5 * mc);
     tl.cnt = tl.id + mc;
+    tl.G = nullptr;  // the scan reads the on-chip meta directly
+    tl.SG = nullptr;
   }
   for (int d = tid; d < D; d += blockDim.x) {
     sK[d] = 0;
@@ -515,8 +684,9 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
         oom = true;
       }
       const TLView t = tl.view(target);
-      const int64_t start = tl_query(t, sK[target], sg[target], sl[target], 0, w);
-      tl_insert(t, &sK[target], &sg[target], &sl[target], start, w);
+      int32_t hint;
+      const int64_t start = tl_query(t, sK[target], sg[target], sl[target], 0, w, &hint);
+      tl_insert(t, &sK[target], &sg[target], &sl[target], start, w, hint);
       if (lane == 0) {
         dev[v] = target;
         savail[target] -= mv;
@@ -637,10 +807,10 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
     long long* const cB = (k & 1) ? sB2 : sB;
     mark(0);
     {
-      // per-device maxima of the node's in-edges.  At most 32 (one warp): one device at a
-      // time (ballot over the lanes still unassigned, full-warp 64-bit max by two redux.sync
-      // on order-preserving words), one shared-memory update per device instead of a
-      // contended CAS per edge; more: a CAS per edge (spread over several warps)
+      // per-device maxima of the node's in-edges, warp by warp: one device at a time (ballot
+      // over the lanes still unassigned, full-warp 64-bit max by two redux.sync on
+      // order-preserving words), then one shared-memory update per (warp, device) instead of
+      // a contended CAS per edge (64-bit shared atomicMax is a CAS loop on sm_100a)
       const bool act = my_p >= 0;
       int64_t f = my_f0;
       int32_t dd = my_dd0;
@@ -651,13 +821,7 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
         f = f2;
         dd = dv2;
       }
-      if (ie - ib > 32) {  // in-edges over several warps (wide coarse graphs): per-edge updates
-        if (act) {
-          atomicMax(&cA[dd], static_cast<long long>(f));
-          atomicMax(&cB[dd], static_cast<long long>(f + my_c));
-        }
-      }
-      unsigned todo = ie - ib > 32 ? 0u : __ballot_sync(FULL, act);
+      unsigned todo = __ballot_sync(FULL, act);  // (rows over 32 in-edges: every warp with edges)
       while (todo) {
         const int leader = __ffs(todo) - 1;
         const int32_t d = __shfl_sync(FULL, dd, leader);
@@ -693,10 +857,12 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
       if (cA[d] > pre) pre = cA[d];
       if (mb > pre) pre = mb;
       int64_t est = kNever;
-      if (avail[d] >= mv) est = tl_query(tl.view(d), sK[d], sg[d], sl[d], pre, w);
+      int32_t hint = -1;
+      if (avail[d] >= mv) est = tl_query(tl.view(d), sK[d], sg[d], sl[d], pre, w, &hint);
       if (lane == 0) {
         sest[d] = est;
         spre[d] = pre;
+        shint[d] = hint;
       }
     }
     __syncthreads();  // Y
@@ -745,9 +911,10 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
     }
     if (a.decisions)
       for (int d = tid; d < D; d += blockDim.x) a.dec_est[(int64_t)k * D + d] = sest[d];
+    int32_t hint = shint[chosen];  // (read before the next node's queries rewrite it)
     if (be) {  // block-uniform: the start needs a query on the most free device
       if (warp == cw) {
-        start = tl_query(tl.view(chosen), sK[chosen], sg[chosen], sl[chosen], spre[chosen], w);
+        start = tl_query(tl.view(chosen), sK[chosen], sg[chosen], sl[chosen], spre[chosen], w, &hint);
         if (lane == 0) s_be_start = start;
       }
       __syncthreads();
@@ -755,7 +922,7 @@ __global__ void __launch_bounds__(256) k_place(const __grid_constant__ PlaceBatc
     }
     if (warp == cw) {
       const TLView t = tl.view(chosen);
-      tl_insert(t, &sK[chosen], &sg[chosen], &sl[chosen], start, w);
+      tl_insert(t, &sK[chosen], &sg[chosen], &sl[chosen], start, w, hint);
       for (int d = lane; d < D; d += 32) avail_next[d] = avail[d] - (d == chosen ? mv : 0);
       if (lane == 0) {
         a.finish[v] = start + w;
@@ -808,8 +975,8 @@ __global__ void k_expand(const int32_t* cl, const int32_t* cdev, const int64_t* 
 void alloc_tl(dp_ctx* ctx, int32_t D, int32_t n, DevBuf<int64_t>& store, DevBuf<int32_t>& store32, TLArrays& t) {
   // a device holding K intervals uses at most K/16 + 1 blocks (splits leave halves of 16)
   const int64_t maxb = n / (kTB / 2) + 2;
-  const int64_t ent = (int64_t)D * maxb * kTB, meta = (int64_t)D * maxb;
-  store.alloc(ctx, static_cast<size_t>(2 * ent + 5 * meta));
+  const int64_t ent = (int64_t)D * maxb * kTB, meta = (int64_t)D * maxb, sg = (int64_t)D * (maxb / 32 + 1);
+  store.alloc(ctx, static_cast<size_t>(2 * ent + 6 * meta + sg));
   store32.alloc(ctx, static_cast<size_t>(2 * meta));
   t.S = store.p;
   t.E = store.p + ent;
@@ -818,6 +985,8 @@ void alloc_tl(dp_ctx* ctx, int32_t D, int32_t n, DevBuf<int64_t>& store, DevBuf<
   t.fS = t.pmEnd + meta;
   t.fE = t.fS + meta;
   t.gub = t.fE + meta;
+  t.G = t.gub + meta;
+  t.SG = t.G + meta;
   t.id = store32.p;
   t.cnt = store32.p + meta;
   t.maxb = static_cast<int32_t>(maxb);
