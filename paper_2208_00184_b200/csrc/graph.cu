@@ -87,11 +87,23 @@ __global__ void k_row_keys(const int32_t* esrc, const int32_t* edst, int32_t m, 
 
 // 1 when every edge resolves and esrc is non-decreasing (generator output order), so the
 // CSR permutation is the identity and the sort can be skipped.
-__global__ void k_sorted_check(const int32_t* esrc, const int32_t* edst, int32_t m, int* flag) {
+// flag[0]: edges sorted by source with both endpoints resolved; flag[2]: every resolved
+// edge u -> v has u < v (the index order is topological), *span += v - u over them (the
+// dataflow level kernel's launch plan) -- the level pass needs no host round trip of its own.
+__global__ void k_sorted_check(const int32_t* esrc, const int32_t* edst, int32_t m, int* flag,
+                               unsigned long long* span) {
+  unsigned long long sp = 0;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
-    bool ok = esrc[e] >= 0 && edst[e] >= 0 && (e == 0 || esrc[e - 1] <= esrc[e]);
+    const int32_t s = esrc[e], d = edst[e];
+    bool ok = s >= 0 && d >= 0 && (e == 0 || esrc[e - 1] <= s);
     if (!ok) atomicExch(flag, 0);
+    if (s >= 0 && d >= 0) {
+      if (s >= d) atomicExch(flag + 2, 0);
+      else sp += static_cast<unsigned long long>(d - s);
+    }
   }
+  for (int o = 16; o; o >>= 1) sp += __shfl_xor_sync(0xffffffffu, sp, o);
+  if ((threadIdx.x & 31) == 0 && sp) atomicAdd(span, sp);
 }
 
 __global__ void k_iota(int32_t* a, int64_t n) {
@@ -529,32 +541,55 @@ __device__ __forceinline__ int ld_relaxed_i32(const int* p) {
   return x;
 }
 
+constexpr int kFlowFin = 32;  // finished counter one L2 line (128 B) away from the ticket
+constexpr int kFlowCtr = 64;  // ints of counters per pass
+
 // forward (rev = false): in-CSC rows, val = tlevel + w, out = tlevel
 // backward (rev = true): out-CSR rows, val = out = blevel
 __device__ __forceinline__ void levels_flow_body(int32_t n, const int32_t* off, const int32_t* nbr,
                                                  const int64_t* cost, const int64_t* w, int64_t* val, int64_t* out,
-                                                 bool rev, int* ctr, int32_t ahead, unsigned sleep_cap) {
+                                                 bool rev, int* ctr, int32_t ahead, int32_t grain,
+                                                 unsigned sleep_cap) {
   const int lane = threadIdx.x & 31;
   const int32_t nchunks = (n + 31) >> 5;
-  for (;;) {
-    int c = 0;
-    if (lane == 0) {
-      c = atomicAdd(&ctr[0], 1);
-      if (c < nchunks)
-        while (ld_relaxed_i32(&ctr[1]) < c - ahead) __nanosleep(128);
-    }
-    c = __shfl_sync(0xffffffffu, c, 0);
-    if (c >= nchunks) break;
+  // Software pipeline over a warp's chunks: the next ticket is taken when the current chunk
+  // starts and its row bounds / weight are loaded while the current chunk waits on its
+  // inputs, so a chunk's chain is rows -> inputs -> publish instead of ticket -> bounds ->
+  // rows -> inputs -> publish.  A warp's current chunk is always its lowest ticket, so the
+  // lowest unfinished chunk is always being worked on (no deadlock).  A ticket is `grain`
+  // consecutive chunks (one atomic per grain: on a wide graph thousands of warps share the
+  // ticket counter, whose same-address atomics serialise in L2); ctr[0] = next ticket,
+  // ctr[kFlowFin] = chunks finished (the lookahead throttle; skipped when unthrottled).
+  int c = 0;
+  if (lane == 0) c = atomicAdd(&ctr[0], grain);
+  c = __shfl_sync(0xffffffffu, c, 0);
+  int rem = grain - 1;  // chunks of the current ticket after c
+  const bool throttled = ahead < nchunks;
+  int fin_seen = 0;  // lane 0: last value read from ctr[kFlowFin] (re-read only when needed)
+  int32_t k = 0, e = 0;
+  int64_t wv = 0;
+  if (c < nchunks) {
     const int32_t i = c * 32 + lane;
-    const bool valid = i < n;
-    const int32_t v = valid ? (rev ? n - 1 - i : i) : 0;
-    int32_t k = 0, e = 0;
-    int64_t wv = 0;
-    if (valid) {
+    if (i < n) {
+      const int32_t v = rev ? n - 1 - i : i;
       k = off[v];
       e = off[v + 1];
       wv = w[v];
     }
+  }
+  while (c < nchunks) {
+    int cn = 0;
+    if (lane == 0) {
+      if (rem == 0) cn = atomicAdd(&ctr[0], grain);
+      if (c - ahead > fin_seen)
+        while ((fin_seen = ld_relaxed_i32(&ctr[kFlowFin])) < c - ahead) __nanosleep(128);
+    }
+    const int32_t i = c * 32 + lane;
+    const bool valid = i < n;
+    const int32_t v = valid ? (rev ? n - 1 - i : i) : 0;
+    int32_t kn = 0, en = 0;
+    int64_t wvn = 0;
+    bool fetched = false;  // next chunk's bounds requested
     int64_t mx = 0;
     bool done = !valid;
     unsigned pend = 0;
@@ -574,6 +609,19 @@ __device__ __forceinline__ void levels_flow_body(int32_t n, const int32_t* off, 
           pend = (1u << cnt) - 1u;
           k += cnt;
         }
+      }
+      if (!fetched) {  // first pass: the rows are requested, now the next chunk's bounds
+        fetched = true;
+        cn = rem > 0 ? c + 1 : __shfl_sync(0xffffffffu, cn, 0);
+        const int32_t in = cn * 32 + lane;
+        if (cn < nchunks && in < n) {
+          const int32_t vn = rev ? n - 1 - in : in;
+          kn = off[vn];
+          en = off[vn + 1];
+          wvn = w[vn];
+        }
+      }
+      if (!done) {
         if (pend) {
           int64_t x[8];
 #pragma unroll
@@ -602,15 +650,13 @@ __device__ __forceinline__ void levels_flow_body(int32_t n, const int32_t* off, 
         if (sleep_cap) __nanosleep(sleep_ns);
       }
     }
-    if (lane == 0) atomicAdd(&ctr[1], 1);
+    if (throttled && lane == 0) atomicAdd(&ctr[kFlowFin], 1);
+    rem = rem > 0 ? rem - 1 : grain - 1;
+    c = cn;
+    k = kn;
+    e = en;
+    wv = wvn;
   }
-}
-
-__global__ void __launch_bounds__(128) k_levels_flow(int32_t n, const int32_t* off, const int32_t* nbr,
-                                                    const int64_t* cost, const int64_t* w, int64_t* val,
-                                                    int64_t* out, bool rev, int* ctr, int32_t ahead,
-                                                    unsigned sleep_cap) {
-  levels_flow_body(n, off, nbr, cost, w, val, out, rev, ctr, ahead, sleep_cap);
 }
 
 // Both directions of several graphs in one launch (blockIdx.y = pass): the t and b passes
@@ -625,8 +671,8 @@ struct FlowPass {
   int64_t* val;
   int64_t* out;
   bool rev;
-  int* ctr;
-  int32_t ahead, blocks;
+  int* ctr;  // kFlowCtr ints, zeroed
+  int32_t ahead, grain, blocks;
 };
 constexpr int kFlowBatch = 16;
 struct FlowBatch {
@@ -636,7 +682,7 @@ struct FlowBatch {
 __global__ void __launch_bounds__(128) k_levels_flow_batch(const __grid_constant__ FlowBatch b) {
   const FlowPass& P = b.p[blockIdx.y];
   if (static_cast<int32_t>(blockIdx.x) >= P.blocks) return;
-  levels_flow_body(P.n, P.off, P.nbr, P.cost, P.w, P.val, P.out, P.rev, P.ctr, P.ahead, b.sleep_cap);
+  levels_flow_body(P.n, P.off, P.nbr, P.cost, P.w, P.val, P.out, P.rev, P.ctr, P.ahead, P.grain, b.sleep_cap);
 }
 
 __global__ void k_kahn_init(KahnArgs a) {
@@ -907,10 +953,12 @@ void graph_adjacency_begin(DevGraph& g, AdjState& st) {
   st.keys_out.alloc(ctx, m);
   st.vals.alloc(ctx, m);
   // CSR by source
-  st.flags.alloc(ctx, 2);  // [0] sorted by source, [1] some row longer than 64
-  const int init[2] = {1, 0};
-  st.flags.upload(init, 2);
-  DP_LAUNCH(ctx, k_sorted_check, grid_for(m, B), B, 0, g.esrc.p, g.edst.p, m, st.flags.p);
+  st.flags.alloc(ctx, 4);  // [0] sorted by source, [1] some row longer than 64, [2] index order topological
+  const int init[4] = {1, 0, 1, 0};
+  st.flags.upload(init, 4);
+  st.span.alloc(ctx, 1);
+  st.span.zero();
+  DP_LAUNCH(ctx, k_sorted_check, grid_for(m, B), B, 0, g.esrc.p, g.edst.p, m, st.flags.p, st.span.p);
   st.cnt.zero();
   DP_LAUNCH(ctx, k_row_keys, grid_for(m, B), B, 0, g.esrc.p, g.edst.p, m, n, true, st.keys.p, st.vals.p, st.cnt.p);
   exclusive_scan_i32(ctx, st.cnt.p, g.out_off.p, (int64_t)n + 1);
@@ -920,6 +968,8 @@ void graph_adjacency_begin(DevGraph& g, AdjState& st) {
   download_bytes(ctx, &st.hs[0], st.flags.p, sizeof(int));
   download_bytes(ctx, &st.hs[1], g.out_off.p + n, sizeof(int32_t));
   download_bytes(ctx, &st.hs[2], st.flags.p + 1, sizeof(int));
+  download_bytes(ctx, &st.hs[3], st.flags.p + 2, sizeof(int));
+  download_bytes(ctx, &st.hspan, st.span.p, sizeof(unsigned long long));
 }
 
 void graph_adjacency_end(DevGraph& g, AdjState& st) {
@@ -929,6 +979,9 @@ void graph_adjacency_end(DevGraph& g, AdjState& st) {
   int endbit = bits_for(static_cast<uint64_t>(n));
   g.m_ok = st.hs[1];
   g.big_rows = st.hs[2] != 0;
+  g.topo_known = true;
+  g.index_topo = st.hs[3] == 1 && n > 0;
+  g.span_sum = st.hspan;
   if (st.hs[0] == 1) {
     DP_LAUNCH(ctx, k_iota, grid_for(m, B), B, 0, g.out_eid.p, (int64_t)m);
   } else {
@@ -999,6 +1052,17 @@ void levels_sweep_launch(DevGraph* const* gs, int64_t* const* tlevel, int64_t* c
 // Index-order check of several graphs with one host sync; ok[i] = index order topological.
 std::vector<char> graphs_index_topological(DevGraph* const* gs, int count, std::vector<unsigned long long>* spans) {
   dp_ctx* ctx = gs[0]->ctx;
+  bool known = true;  // all facts from graph_adjacency's round trip: no launch, no sync
+  for (int i = 0; i < count; ++i) known = known && gs[i]->topo_known;
+  if (known) {
+    std::vector<char> ok(count);
+    if (spans) spans->resize(count);
+    for (int i = 0; i < count; ++i) {
+      ok[i] = gs[i]->index_topo;
+      if (spans) (*spans)[i] = gs[i]->span_sum;
+    }
+    return ok;
+  }
   DevBuf<unsigned long long> chk(ctx, 2 * (size_t)count);
   std::vector<unsigned long long> init(2 * (size_t)count, 0ull);
   for (int i = 0; i < count; ++i) init[2 * i] = 1ull;
@@ -1025,18 +1089,65 @@ bool coarse_flow_wanted(int32_t n) { return n > kSeqMaxN && getenv("DP_COARSE_FL
 // one-CTA sweep for small or chain-like graphs (the coarse graph of fuse), the dataflow
 // kernel otherwise.  Returns false when the index order is not topological (caller uses
 // graph_kahn).
+// Dataflow launch plan of one graph from its summed edge span (u -> v: v - u).
+// Narrow wavefront (mean span under kFlowWideChunks chunks; config #4 deep): lookahead of
+// two mean spans, at least 64 chunks (more polling warps only cost when many graphs run
+// at once: 64 vs 256 chunks = 2.47 vs 2.33 ms alone, 707 vs 730 ms per 128-graph step),
+// one chunk per ticket, up to 32 warps per SM.  Wide wavefront (config #4 wide: 16 levels
+// of 65,536): no lookahead limit, so warps run far ahead and their rows load early, and
+// 8 warps per SM per pass -- measured on the B200 (tools/levels_probe.py, both passes):
+// 0.36 ms with the narrow plan, 0.10-0.12 ms with 8 warps per SM and no limit (fewer
+// polling warps, less L2 contention; 4 / 16 / 24 warps: 0.19 / 0.13 / 0.14 ms; a lookahead
+// of 128 chunks: 0.92 ms).  Tickets of more than one chunk measured slower (4 chunks: 0.16
+// ms).  DP_FLOW_AHEAD / _GRAIN / _WARPS (per SM) override.
+constexpr double kFlowWideChunks = 256.0;
+struct FlowPlan {
+  int32_t ahead, grain;
+  int blocks;
+};
+FlowPlan flow_plan(dp_ctx* ctx, const DevGraph& g, unsigned long long span_sum) {
+  const double mean_span = g.m_ok > 0 ? static_cast<double>(span_sum) / g.m_ok : 32.0;
+  FlowPlan pl{};
+  const bool wide = mean_span / 32.0 >= kFlowWideChunks;
+  pl.ahead = wide ? (1 << 30) : static_cast<int32_t>(std::max(64.0, 2.0 * mean_span / 32.0));
+  if (const char* s = getenv("DP_FLOW_AHEAD")) pl.ahead = atoi(s);
+  pl.grain = 1;
+  if (const char* s = getenv("DP_FLOW_GRAIN")) pl.grain = std::max(1, atoi(s));
+  const int32_t nchunks = (g.n + 31) / 32;
+  int32_t per_sm = wide ? 8 : 32;
+  if (const char* s = getenv("DP_FLOW_WARPS")) per_sm = atoi(s);
+  const int32_t warps =
+      std::max(1, std::min({nchunks, static_cast<int32_t>(std::min<int64_t>(pl.ahead + 32LL, 1 << 30)),
+                            ctx->num_sms * per_sm}));
+  pl.blocks = (warps + 3) / 4;
+  if (getenv("DP_DEBUG_FLOW"))
+    fprintf(stderr, "[flow] n=%d m=%d mean_span=%.1f wide=%d ahead=%d grain=%d warps=%d\n", g.n, g.m_ok, mean_span,
+            static_cast<int>(wide), pl.ahead, pl.grain, warps);
+  return pl;
+}
+unsigned flow_sleep_cap() {
+  unsigned sleep_cap = 256;
+  if (const char* s = getenv("DP_FLOW_SLEEP")) sleep_cap = static_cast<unsigned>(atoi(s));
+  return sleep_cap;
+}
+
 bool graph_levels_indexorder(DevGraph& g, int64_t* tlevel, int64_t* blevel, bool chainlike) {
   dp_ctx* ctx = g.ctx;
   const int32_t n = g.n;
   if (n == 0 || getenv("DP_LEVELS_KAHN")) return false;
-  DevBuf<unsigned long long> chk(ctx, 2);  // [0] ok flag, [1] span sum
-  const unsigned long long init[2] = {1ull, 0ull};
-  chk.upload(init, 2);
-  DP_LAUNCH(ctx, k_index_topo, grid_for(n, 256), 256, 0, g.in_off.p, g.in_src.p, n, reinterpret_cast<int*>(chk.p),
-            chk.p + 1);
-  unsigned long long h[2];
-  chk.download(h, 2);
-  sync(ctx);
+  unsigned long long h[2];  // [0] ok flag, [1] span sum
+  if (g.topo_known) {  // from graph_adjacency's round trip
+    h[0] = g.index_topo ? 1ull : 0ull;
+    h[1] = g.span_sum;
+  } else {
+    DevBuf<unsigned long long> chk(ctx, 2);
+    const unsigned long long init[2] = {1ull, 0ull};
+    chk.upload(init, 2);
+    DP_LAUNCH(ctx, k_index_topo, grid_for(n, 256), 256, 0, g.in_off.p, g.in_src.p, n, reinterpret_cast<int*>(chk.p),
+              chk.p + 1);
+    chk.download(h, 2);
+    sync(ctx);
+  }
   if (static_cast<int>(h[0]) != 1) return false;
   const bool sweep = (n <= kSeqMaxN || (chainlike && !coarse_flow_wanted(n))) && getenv("DP_LEVELS_FLOW") == nullptr;
 
@@ -1048,26 +1159,22 @@ bool graph_levels_indexorder(DevGraph& g, int64_t* tlevel, int64_t* blevel, bool
     g.processed = n;
     return true;
   }
-  // lookahead: two mean edge spans, in 32-node chunks, at least 64 chunks (a deep graph's
-  // wavefront needs few; more polling warps only cost when many graphs run at once:
-  // 64 vs 256 chunks = 2.47 vs 2.33 ms alone, 707 vs 730 ms per 128-graph step)
-  const double mean_span = g.m_ok > 0 ? static_cast<double>(h[1]) / g.m_ok : 32.0;
-  int32_t ahead = static_cast<int32_t>(std::min(1.0e6, std::max(64.0, 2.0 * mean_span / 32.0)));
-  if (const char* s = getenv("DP_FLOW_AHEAD")) ahead = atoi(s);
-  unsigned sleep_cap = 256;
-  if (const char* s = getenv("DP_FLOW_SLEEP")) sleep_cap = static_cast<unsigned>(atoi(s));
-  const int32_t nchunks = (n + 31) / 32;
-  const int32_t warps = std::max(1, std::min({nchunks, ahead + 32, ctx->num_sms * 32}));
-  const int blocks = (warps + 3) / 4;
+  FlowBatch fb{};
+  fb.sleep_cap = flow_sleep_cap();
+  const FlowPlan pl = flow_plan(ctx, g, h[1]);
   DevBuf<int64_t> f(ctx, n);
-  DevBuf<int> ctr(ctx, 4);
+  DevBuf<int> ctr(ctx, 2 * kFlowCtr);
   f.fill_bytes(0xff);
   ctr.zero();
-  DP_LAUNCH(ctx, k_levels_flow, blocks, 128, 0, n, g.in_off.p, g.in_src.p, g.in_cost.p, g.w.p, f.p, tlevel, false,
-            ctr.p, ahead, sleep_cap);
   DP_CUDA(cudaMemsetAsync(blevel, 0xff, sizeof(int64_t) * n, ctx->stream));
-  DP_LAUNCH(ctx, k_levels_flow, blocks, 128, 0, n, g.out_off.p, g.out_dst.p, g.out_cost.p, g.w.p, blevel, blevel,
-            true, ctr.p + 2, ahead, sleep_cap);
+  fb.p[0] = FlowPass{n, g.in_off.p, g.in_src.p, g.in_cost.p, g.w.p, f.p, tlevel, false, ctr.p, pl.ahead, pl.grain,
+                     pl.blocks};
+  fb.p[1] = FlowPass{n, g.out_off.p, g.out_dst.p, g.out_cost.p, g.w.p, blevel, blevel, true, ctr.p + kFlowCtr, pl.ahead,
+                     pl.grain,
+                     pl.blocks};
+  k_levels_flow_batch<<<dim3(pl.blocks, 2), 128, 0, ctx->stream>>>(fb);
+  ++ctx->launches;
+  DP_CUDA(cudaGetLastError());
   g.processed = n;
   return true;
 }
@@ -1099,10 +1206,9 @@ std::vector<char> graphs_levels_indexorder(DevGraph* const* gs, int count, int64
   }
   if (!sg.empty()) levels_sweep_launch(sg.data(), st.data(), sb.data(), static_cast<int>(sg.size()));
   if (flow.empty()) return ok;
-  unsigned sleep_cap = 256;
-  if (const char* e = getenv("DP_FLOW_SLEEP")) sleep_cap = static_cast<unsigned>(atoi(e));
+  const unsigned sleep_cap = flow_sleep_cap();
   std::vector<DevBuf<int64_t>> fval(flow.size());
-  DevBuf<int> ctr(ctx, 4 * flow.size());
+  DevBuf<int> ctr(ctx, 2 * kFlowCtr * flow.size());
   ctr.zero();
   for (size_t q0 = 0; q0 < flow.size(); q0 += kFlowBatch / 2) {
     const size_t k = std::min<size_t>(kFlowBatch / 2, flow.size() - q0);
@@ -1113,21 +1219,17 @@ std::vector<char> graphs_levels_indexorder(DevGraph* const* gs, int count, int64
       const int i = flow[q0 + q];
       DevGraph& g = *gs[i];
       const int32_t n = g.n;
-      const double mean_span = g.m_ok > 0 ? static_cast<double>(spans[i]) / g.m_ok : 32.0;
-      int32_t ahead = static_cast<int32_t>(std::min(1.0e6, std::max(64.0, 2.0 * mean_span / 32.0)));
-      if (const char* e = getenv("DP_FLOW_AHEAD")) ahead = atoi(e);
-      const int32_t nchunks = (n + 31) / 32;
-      const int32_t warps = std::max(1, std::min({nchunks, ahead + 32, ctx->num_sms * 32}));
-      const int blocks = (warps + 3) / 4;
+      const FlowPlan pl = flow_plan(ctx, g, spans[i]);
+      const int blocks = pl.blocks, ahead = pl.ahead;
       gridx = std::max(gridx, blocks);
       fval[q0 + q].alloc(ctx, n);
       fval[q0 + q].fill_bytes(0xff);
       DP_CUDA(cudaMemsetAsync(blevel[i], 0xff, sizeof(int64_t) * n, ctx->stream));
-      int* c = ctr.p + 4 * (q0 + q);
+      int* c = ctr.p + 2 * kFlowCtr * (q0 + q);
       b.p[2 * q] = FlowPass{n, g.in_off.p, g.in_src.p, g.in_cost.p, g.w.p, fval[q0 + q].p, tlevel[i], false, c, ahead,
-                            blocks};
-      b.p[2 * q + 1] = FlowPass{n, g.out_off.p, g.out_dst.p, g.out_cost.p, g.w.p, blevel[i], blevel[i], true, c + 2,
-                                ahead, blocks};
+                            pl.grain, blocks};
+      b.p[2 * q + 1] = FlowPass{n, g.out_off.p, g.out_dst.p, g.out_cost.p, g.w.p, blevel[i], blevel[i], true,
+                                c + kFlowCtr, ahead, pl.grain, blocks};
     }
     k_levels_flow_batch<<<dim3(gridx, 2 * static_cast<unsigned>(k)), 128, 0, ctx->stream>>>(b);
     ++ctx->launches;

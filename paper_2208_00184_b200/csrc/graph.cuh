@@ -25,6 +25,9 @@ struct DevGraph {
   bool has_adj = false;
   bool big_rows = false;  // some CSR row is longer than 64 (duplicate-edge check sorts)
   int32_t m_ok = 0;
+  bool topo_known = false;          // index_topo / span_sum set by graph_adjacency
+  bool index_topo = false;          // every resolved edge u -> v has u < v
+  unsigned long long span_sum = 0;  // sum of v - u over the resolved edges
   DevBuf<int32_t> out_off, out_eid, in_off, in_eid, out_dst, in_src;
   // costs
   bool has_cost = false;
@@ -71,7 +74,9 @@ struct AdjState {
   DevBuf<int32_t> cnt, vals;
   DevBuf<uint32_t> keys, keys_out;
   DevBuf<int> flags;
-  int hs[3] = {0, 0, 0};
+  DevBuf<unsigned long long> span;
+  int hs[4] = {0, 0, 0, 0};
+  unsigned long long hspan = 0;
 };
 void graph_adjacency_begin(DevGraph& g, AdjState& st);
 void graph_adjacency_end(DevGraph& g, AdjState& st);

@@ -1,6 +1,12 @@
 // peel_dp.cu — latency-engineered topological peel (ordering.cpp:40-114) and the
 // streaming breakpoint DP (fusion.cpp:126-162) that consumes its output.
 //
+// The reference peel is a deque used as a stack for DFS/CPD (freed children pushed to the
+// head, so the highest-priority freed child is emitted right after its parent — pinned by
+// test_ordering.cpp:104-135) and as a FIFO for M-TOPO.  Both comparators of a policy are
+// one static total order, so each node gets a 32-bit rank (lower = emitted first among
+// simultaneously available nodes): CPD (cpath desc, id asc), DFS / M (id asc).
+//
 // Peel (one warp).  Per CSR slot the warp loads one 16-byte record
 //   { child, rank(child), row_start(child), out_degree(child) }
 // so a popped stack entry already names its own row and a freed child can be pushed
@@ -2423,6 +2429,24 @@ int32_t peel_dp_stream(DevGraph& g, const int64_t* cpath, int32_t range, int64_t
   PeelDpHandle h(peel_dp_prepare(g, cpath, range, limit, seq, pos_of, prev_cut, first_exceed));
   peel_dp_launch(g.ctx, &h.j, 1);
   return scalar_to_host(g.ctx, h.j->st.counters.p + 1);
+}
+
+// Node indices sorted by id ascending (identity for dense ids): the rank of DFS / M-TOPO.
+namespace {
+__global__ void k_iota32(int32_t* a, int32_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = static_cast<int32_t>(i);
+}
+}  // namespace
+
+void node_order_by_id(DevGraph& g, DevBuf<int32_t>& by_id) {
+  dp_ctx* ctx = g.ctx;
+  by_id.alloc(ctx, g.n > 0 ? g.n : 1);
+  if (g.dense_ids) {
+    DP_LAUNCH(ctx, k_iota32, grid_for(g.n, 256), 256, 0, by_id.p, g.n);
+  } else if (g.n) {
+    DP_CUDA(cudaMemcpyAsync(by_id.p, g.sorted_idx.p, sizeof(int32_t) * g.n, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
 }
 
 }  // namespace dpb

@@ -131,10 +131,15 @@ def _levels_same(gpu, oracle, g):
         same(x, y, nm)
 
 
+@pytest.mark.parametrize("warps", [None, "1", "64"])
 @pytest.mark.parametrize("shape", ["deep", "wide", "chain", "hub", "long_rows"])
-def test_levels_dataflow(gpu, oracle, shape):
+def test_levels_dataflow(gpu, oracle, monkeypatch, shape, warps):
     """Index-topological graphs above the sweep limit take the dataflow kernel
-    (k_levels_flow): deep and wide layers, a near-chain, in-degree hubs, rows > 8."""
+    (k_levels_flow_batch): deep and wide layers, a near-chain (inputs inside the warp's own
+    chunk), in-degree hubs, rows > 8; with the default warp count, one warp per SM per pass
+    and more warps than fit on the GPU at once (tickets are only taken by running warps)."""
+    if warps is not None:
+        monkeypatch.setenv("DP_FLOW_WARPS", warps)
     g = {"deep": lambda: layered(31, 60000, 500),
          "wide": lambda: layered(32, 80000, 20000),
          "chain": lambda: layered(33, 20000, 2, fan_lo=1, fan_hi=2),
@@ -143,10 +148,13 @@ def test_levels_dataflow(gpu, oracle, shape):
     _levels_same(gpu, oracle, g)
 
 
+@pytest.mark.parametrize("grain", ["1", "3", "8"])
 @pytest.mark.parametrize("ahead", ["1", "3", "100000"])
-def test_levels_dataflow_lookahead(gpu, oracle, monkeypatch, ahead):
-    # the lookahead only throttles ticket holders: any value must give the same levels
+def test_levels_dataflow_lookahead(gpu, oracle, monkeypatch, ahead, grain):
+    # the lookahead only throttles ticket holders and a ticket's grain only groups chunks:
+    # any values must give the same levels
     monkeypatch.setenv("DP_FLOW_AHEAD", ahead)
+    monkeypatch.setenv("DP_FLOW_GRAIN", grain)
     _levels_same(gpu, oracle, layered(35, 40000, 700))
 
 
