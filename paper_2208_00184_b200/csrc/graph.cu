@@ -8,6 +8,7 @@
 //   comm_time                     src/graph.cpp:200-204     (no FMA; llround)
 //   compute_levels                src/graph.cpp:217-269     (int64 max-plus; any topo order)
 #include <algorithm>
+#include <climits>
 #include <cstring>
 #include <sstream>
 
@@ -549,7 +550,7 @@ constexpr int kFlowCtr = 64;  // ints of counters per pass
 __device__ __forceinline__ void levels_flow_body(int32_t n, const int32_t* off, const int32_t* nbr,
                                                  const int64_t* cost, const int64_t* w, int64_t* val, int64_t* out,
                                                  bool rev, int* ctr, int32_t ahead, int32_t grain,
-                                                 unsigned sleep_cap) {
+                                                 unsigned sleep_cap, int prefetch) {
   const int lane = threadIdx.x & 31;
   const int32_t nchunks = (n + 31) >> 5;
   // Software pipeline over a warp's chunks: the next ticket is taken when the current chunk
@@ -590,6 +591,7 @@ __device__ __forceinline__ void levels_flow_body(int32_t n, const int32_t* off, 
     int32_t kn = 0, en = 0;
     int64_t wvn = 0;
     bool fetched = false;  // next chunk's bounds requested
+    bool pf = prefetch != 0;  // next chunk's rows still to be prefetched into L2
     int64_t mx = 0;
     bool done = !valid;
     unsigned pend = 0;
@@ -642,6 +644,23 @@ __device__ __forceinline__ void levels_flow_body(int32_t n, const int32_t* off, 
           progress = true;
         }
       }
+      if (pf) {
+        // the first poll's values are back, so the next chunk's bounds (requested before
+        // them) are too: one bulk L2 prefetch of its whole row span per array (the rows of
+        // 32 consecutive nodes are contiguous), so its row loads hit L2 instead of HBM
+        pf = false;
+        const bool has = kn < en;
+        const int32_t lo = __reduce_min_sync(0xffffffffu, has ? kn : INT_MAX);
+        const int32_t hi = __reduce_max_sync(0xffffffffu, has ? en : 0);
+        if (lane == 0 && lo < hi) {
+          const int32_t lo4 = lo & ~3, hi4 = (hi + 3) & ~3;  // 16-byte aligned spans
+          const int32_t lo2 = lo & ~1, hi2 = (hi + 1) & ~1;
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nbr + lo4),
+                       "r"(static_cast<unsigned>(4 * (hi4 - lo4))) : "memory");
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(cost + lo2),
+                       "r"(static_cast<unsigned>(8 * (hi2 - lo2))) : "memory");
+        }
+      }
       if (__all_sync(0xffffffffu, done)) break;
       if (__any_sync(0xffffffffu, progress)) {
         sleep_ns = 0;
@@ -678,11 +697,13 @@ constexpr int kFlowBatch = 16;
 struct FlowBatch {
   FlowPass p[kFlowBatch];
   unsigned sleep_cap;
+  int prefetch;  // bulk L2 prefetch of the next chunk's rows (DP_FLOW_NO_PREFETCH: off)
 };
 __global__ void __launch_bounds__(128) k_levels_flow_batch(const __grid_constant__ FlowBatch b) {
   const FlowPass& P = b.p[blockIdx.y];
   if (static_cast<int32_t>(blockIdx.x) >= P.blocks) return;
-  levels_flow_body(P.n, P.off, P.nbr, P.cost, P.w, P.val, P.out, P.rev, P.ctr, P.ahead, P.grain, b.sleep_cap);
+  levels_flow_body(P.n, P.off, P.nbr, P.cost, P.w, P.val, P.out, P.rev, P.ctr, P.ahead, P.grain, b.sleep_cap,
+                   b.prefetch);
 }
 
 __global__ void k_kahn_init(KahnArgs a) {
@@ -1161,6 +1182,7 @@ bool graph_levels_indexorder(DevGraph& g, int64_t* tlevel, int64_t* blevel, bool
   }
   FlowBatch fb{};
   fb.sleep_cap = flow_sleep_cap();
+  fb.prefetch = getenv("DP_FLOW_NO_PREFETCH") == nullptr;
   const FlowPlan pl = flow_plan(ctx, g, h[1]);
   DevBuf<int64_t> f(ctx, n);
   DevBuf<int> ctr(ctx, 2 * kFlowCtr);
@@ -1214,6 +1236,7 @@ std::vector<char> graphs_levels_indexorder(DevGraph* const* gs, int count, int64
     const size_t k = std::min<size_t>(kFlowBatch / 2, flow.size() - q0);
     FlowBatch b{};
     b.sleep_cap = sleep_cap;
+    b.prefetch = getenv("DP_FLOW_NO_PREFETCH") == nullptr;
     int gridx = 1;
     for (size_t q = 0; q < k; ++q) {
       const int i = flow[q0 + q];
