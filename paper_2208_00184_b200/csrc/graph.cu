@@ -376,7 +376,8 @@ __device__ __forceinline__ void kahn_pull_warp(const KahnArgs& a, int32_t v) {
 // rows (CSC for tlevel, CSR backwards for blevel) into shared memory, then warp 0 walks
 // the tile with the running finish/blevel values in shared memory: per node one gather
 // per in-edge and a two-step 64-bit max (redux.sync on high then low words).
-constexpr int kSeqMaxN = 16384;  // power of two: the value ring is indexed with a mask
+constexpr int kSeqMaxN = 16384;  // graphs up to this size always take the one-CTA sweep
+constexpr int kSeqRing = 8192;   // power of two: sweep values kept in shared memory
 constexpr int kSeqTile = 4096;   // edges staged per tile
 constexpr int kSeqTileN = 2048;  // nodes staged per tile
 
@@ -405,7 +406,7 @@ __device__ __forceinline__ int64_t warp_max_nonneg(int64_t x) {
 
 // forward: tlevel[v] = max(0, max_{u->v} f[u] + c), f[u] = tlevel[u] + w[u]
 // backward (rev): blevel[v] = w[v] + max(0, max_{v->s} blevel[s] + c)
-// Values of the last kSeqMaxN sweep positions live in a shared-memory ring; older ones
+// Values of the last kSeqRing sweep positions live in a shared-memory ring; older ones
 // (graphs larger than the ring) are read from `gval` in HBM/L2 with ld.global.cg (the
 // sweep writes them there too), so any n works and chain-like graphs hit the ring.
 // One CTA per graph (independent graphs of a batched call share the launch).
@@ -420,11 +421,13 @@ struct SeqArgs {
 };
 constexpr int kSeqBatch = 8;
 struct SeqBatch {
-  SeqArgs a[kSeqBatch];
+  SeqArgs a[2][kSeqBatch];  // [0] forward (t-levels), [1] backward (b-levels)
 };
 
-__global__ void __launch_bounds__(1024) k_levels_seq(const __grid_constant__ SeqBatch batch, bool rev) {
-  const SeqArgs& A = batch.a[blockIdx.x];
+// blockIdx.y = direction: the two passes are independent and run on two SMs at once.
+__global__ void __launch_bounds__(1024) k_levels_seq(const __grid_constant__ SeqBatch batch) {
+  const bool rev = blockIdx.y != 0;
+  const SeqArgs& A = batch.a[blockIdx.y][blockIdx.x];
   const int32_t n = A.n;
   const int32_t* off = A.off;
   const int32_t* nbr = A.nbr;
@@ -433,13 +436,15 @@ __global__ void __launch_bounds__(1024) k_levels_seq(const __grid_constant__ Seq
   int64_t* out = A.out;
   int64_t* gval = A.gval;
   extern __shared__ int64_t sm64[];
-  int64_t* val = sm64;                                         // ring [kSeqMaxN]: f (fwd) or blevel (bwd)
-  int64_t* ec = val + kSeqMaxN;                                // [kSeqTile]
+  int64_t* val = sm64;                                         // ring [kSeqRing]: f (fwd) or blevel (bwd)
+  int64_t* ec = val + kSeqRing;                                // [kSeqTile]
   int64_t* wt = ec + kSeqTile;                                 // [kSeqTileN]
-  int32_t* en = reinterpret_cast<int32_t*>(wt + kSeqTileN);    // [kSeqTile]
+  int64_t* bmax = wt + kSeqTileN;                              // [kSeqTileN]
+  int32_t* en = reinterpret_cast<int32_t*>(bmax + kSeqTileN);  // [kSeqTile]
   int32_t* ot = en + kSeqTile;                                 // [kSeqTileN + 1]
+  int32_t* icnt = ot + kSeqTileN + 1;                          // [kSeqTileN]
   __shared__ int32_t tile_hi;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   int32_t done = 0;  // nodes processed (in sweep order)
   while (done < n) {
     // tile: sweep positions [done, hi) with at most kSeqTile edges (at least one node)
@@ -468,7 +473,7 @@ __global__ void __launch_bounds__(1024) k_levels_seq(const __grid_constant__ Seq
         const int32_t pu = rev ? n - 1 - u : u;
         const bool before = pu < done;
         en[k] = before ? -1 : u;
-        ec[k] = before ? (done - pu <= kSeqMaxN ? val[pu & (kSeqMaxN - 1)] : __ldcg(gval + u)) + c : c;
+        ec[k] = before ? (done - pu <= kSeqRing ? val[pu & (kSeqRing - 1)] : __ldcg(gval + u)) + c : c;
       }
     }
     for (int32_t i = done + threadIdx.x; i <= hi; i += blockDim.x) {
@@ -481,32 +486,69 @@ __global__ void __launch_bounds__(1024) k_levels_seq(const __grid_constant__ Seq
       }
     }
     __syncthreads();
+    if (fits) {
+      // per node (one warp each): the max over sources swept before the tile, and the
+      // in-tile sources compacted to the row's front -- the walk below then touches only
+      // the chain it depends on (one shared read per in-tile source, none otherwise)
+      for (int32_t i = done + warp; i < hi; i += nwarps) {
+        const int32_t rb = (rev ? ot[i + 1 - done] : ot[i - done]) - e0;
+        const int32_t re = (rev ? ot[i - done] : ot[i + 1 - done]) - e0;
+        int64_t bm = 0;
+        int32_t cnt = 0;
+        for (int32_t k0 = rb; k0 < re; k0 += 32) {
+          const int32_t k = k0 + lane;
+          const bool act = k < re;
+          const int32_t u = act ? en[k] : -1;
+          const int64_t x = act ? ec[k] : 0;
+          if (act && u < 0) bm = max(bm, x);
+          const unsigned intra = __ballot_sync(0xffffffffu, u >= 0);
+          __syncwarp();  // every lane read its slot before the compacted writes below
+          if (u >= 0) {
+            const int32_t p = rb + cnt + __popc(intra & ((1u << lane) - 1u));
+            en[p] = u;
+            ec[p] = x;
+          }
+          cnt += __popc(intra);
+          __syncwarp();
+        }
+        bm = warp_max_nonneg(bm);
+        if (lane == 0) {
+          bmax[i - done] = bm;
+          icnt[i - done] = cnt;
+        }
+      }
+      __syncthreads();
+    }
     if (warp == 0) {
       for (int32_t i = done; i < hi; ++i) {
         const int32_t v = rev ? n - 1 - i : i;
         const int32_t b = rev ? ot[i + 1 - done] : ot[i - done], e = rev ? ot[i - done] : ot[i + 1 - done];
         int64_t mx = 0;
-        for (int32_t k = b + lane; k < e; k += 32) {
-          const int32_t u = fits ? en[k - e0] : nbr[k];
-          if (fits) {
-            const int64_t x = ec[k - e0];
-            if (u < 0) {
-              mx = max(mx, x);
-            } else {
+        if (fits) {
+          const int32_t cnt = icnt[i - done];
+          mx = bmax[i - done];
+          if (cnt > 0) {
+            int64_t m = lane == 0 ? mx : 0;
+            for (int32_t k = lane; k < cnt; k += 32) {
+              const int32_t u = en[b - e0 + k];
               const int32_t pu = rev ? n - 1 - u : u;  // in this tile: the ring holds it
-              mx = max(mx, val[pu & (kSeqMaxN - 1)] + x);
+              m = max(m, val[pu & (kSeqRing - 1)] + ec[b - e0 + k]);
             }
-          } else {
+            mx = warp_max_nonneg(m);
+          }
+        } else {
+          for (int32_t k = b + lane; k < e; k += 32) {
+            const int32_t u = nbr[k];
             const int64_t c = cost[k];
             const int32_t pu = rev ? n - 1 - u : u;  // sweep position of u (< i)
-            const int64_t fu = i - pu <= kSeqMaxN ? val[pu & (kSeqMaxN - 1)] : __ldcg(gval + u);
+            const int64_t fu = i - pu <= kSeqRing ? val[pu & (kSeqRing - 1)] : __ldcg(gval + u);
             mx = max(mx, fu + c);
           }
+          mx = warp_max_nonneg(mx);
         }
-        mx = warp_max_nonneg(mx);
         if (lane == 0) {
           const int64_t vv = mx + wt[i - done];  // f[v] = tlevel + w (fwd); blevel (bwd)
-          val[i & (kSeqMaxN - 1)] = vv;
+          val[i & (kSeqRing - 1)] = vv;
           if (gval) __stcg(gval + v, vv);
           out[v] = rev ? vv : mx;
         }
@@ -1049,24 +1091,30 @@ void graph_costs(DevGraph& g, dp_comm_t comm) {
 // caller), one launch per direction.
 void levels_sweep_launch(DevGraph* const* gs, int64_t* const* tlevel, int64_t* const* blevel, int count) {
   dp_ctx* ctx = gs[0]->ctx;
-  const size_t sm = sizeof(int64_t) * (kSeqMaxN + kSeqTile + kSeqTileN) + sizeof(int32_t) * (kSeqTile + kSeqTileN + 1);
+  const size_t sm =
+      sizeof(int64_t) * (kSeqRing + kSeqTile + 2 * kSeqTileN) + sizeof(int32_t) * (kSeqTile + 2 * kSeqTileN + 1);
   static bool attr = false;
   if (!attr) {
     DP_CUDA(cudaFuncSetAttribute(k_levels_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
     attr = true;
   }
-  std::vector<DevBuf<int64_t>> gval(count);
+  std::vector<DevBuf<int64_t>> gval(2 * static_cast<size_t>(count));  // per direction (they run at once)
   for (int b0 = 0; b0 < count; b0 += kSeqBatch) {
     const int k = std::min(kSeqBatch, count - b0);
-    SeqBatch fwd{}, bwd{};
+    SeqBatch sb{};
     for (int q = 0; q < k; ++q) {
       DevGraph& g = *gs[b0 + q];
-      if (g.n > kSeqMaxN) gval[b0 + q].alloc(ctx, g.n);
-      fwd.a[q] = SeqArgs{g.n, g.in_off.p, g.in_src.p, g.in_cost.p, g.w.p, tlevel[b0 + q], gval[b0 + q].p};
-      bwd.a[q] = SeqArgs{g.n, g.out_off.p, g.out_dst.p, g.out_cost.p, g.w.p, blevel[b0 + q], gval[b0 + q].p};
+      if (g.n > kSeqRing) {
+        gval[2 * (b0 + q)].alloc(ctx, g.n);
+        gval[2 * (b0 + q) + 1].alloc(ctx, g.n);
+      }
+      sb.a[0][q] = SeqArgs{g.n, g.in_off.p, g.in_src.p, g.in_cost.p, g.w.p, tlevel[b0 + q], gval[2 * (b0 + q)].p};
+      sb.a[1][q] =
+          SeqArgs{g.n, g.out_off.p, g.out_dst.p, g.out_cost.p, g.w.p, blevel[b0 + q], gval[2 * (b0 + q) + 1].p};
     }
-    DP_LAUNCH(ctx, k_levels_seq, k, 1024, sm, fwd, false);
-    DP_LAUNCH(ctx, k_levels_seq, k, 1024, sm, bwd, true);
+    k_levels_seq<<<dim3(k, 2), 1024, sm, ctx->stream>>>(sb);
+    ++ctx->launches;
+    DP_CUDA(cudaGetLastError());
   }
 }
 
