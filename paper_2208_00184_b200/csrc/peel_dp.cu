@@ -23,6 +23,7 @@
 // recurrence of fusion.cu on shared-memory operands.  Peel and DP overlap, so the
 // sequential part of fuse() costs max(peel, DP) instead of their sum.
 #include <algorithm>
+#include <cstddef>
 #include <cstdlib>
 #include <memory>
 #include <vector>
@@ -82,6 +83,8 @@ struct PeelArgs {
   long long* debug;      // optional: peel warp cycles
   bool prefetch;         // v6: prefetch the rows of a pushed child's children to L2
   const int* skip;       // *skip != 0: the order was produced by the fixed-point peel (fixpoint.cu)
+  const uint32_t* dense16;  // v6 dense mode (nullptr: off): initial in-degrees, 16 bits each
+  const int* dense_bad;     // *dense_bad != 0: an in-degree >= 65,535 (dense mode off)
 };
 
 // The peel warp.  Shared memory: stack cache (kStackCache int4) + freed buffer.
@@ -466,6 +469,21 @@ __device__ __forceinline__ bool v6_dec(V6Smem<BB>& S, int32_t* gover, int32_t c,
   return false;
 }
 
+// Dense mode (graphs of at most 2 x (2^(BB+1) + 2^(BB-1)) nodes, every in-degree < 65,535):
+// the remaining in-degree of EVERY node lives in shared memory as a 16-bit counter (two per
+// word, over the hash table's and overflow counts' storage), so a decrement is one shared
+// atomic -- no bucket probe, no global counter for in-degrees >= 127 or spilled buckets.
+// Parallel edges are rejected by validation, so a row decrements each child once and a
+// counter never goes below zero (no borrow into its neighbour).
+template <int BB>
+constexpr int32_t v6_dense_cap() {
+  return 2 * ((2 << BB) + (1 << (BB - 1)));
+}
+__device__ __forceinline__ uint32_t v6_dense_dec(uint32_t* dw, int32_t c) {
+  const uint32_t sh = (static_cast<uint32_t>(c) & 1u) * 16u;
+  return (atomicSub(&dw[c >> 1], 1u << sh) >> sh) & 0xffffu;  // remaining before this decrement
+}
+
 // Loads stack entries [lo, hi] (ids from the global stack, rows from the ELL) into the cache.
 template <int BB>
 __device__ void v6_fill(const PeelArgs& a, V6Smem<BB>& S, int32_t lo, int32_t hi, int lane) {
@@ -489,8 +507,16 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem<BB>& S) {
   const int lane = threadIdx.x & 31;
   const long long t_start = clock64();
   constexpr int32_t SC = kV6Stack;
-  for (int i = lane; i < (2 << BB); i += 32) S.ht[i] = kV6Empty;
-  for (int i = lane; i < (1 << (BB - 1)); i += 32) S.ovc[i] = 0;
+  static_assert(offsetof(V6Smem<BB>, ovc) == offsetof(V6Smem<BB>, ht) + sizeof(uint32_t) * (2 << BB),
+                "dense counters span ht and ovc");
+  const bool dense = a.dense16 != nullptr && a.n <= v6_dense_cap<BB>() && *a.dense_bad == 0;
+  uint32_t* const dw = S.ht;  // dense mode: counters over ht + ovc
+  if (dense) {
+    for (int i = lane; i < (a.n + 1) / 2; i += 32) dw[i] = a.dense16[i];
+  } else {
+    for (int i = lane; i < (2 << BB); i += 32) S.ht[i] = kV6Empty;
+    for (int i = lane; i < (1 << (BB - 1)); i += 32) S.ovc[i] = 0;
+  }
   const int32_t nsrc = *a.nsrc;
   int32_t top = nsrc - 1;
   int32_t base = max(0, nsrc - SC / 2);
@@ -539,6 +565,7 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem<BB>& S) {
         if (cm.x >= 0) {
           const int code = (cm.y >> 24) & 127;
           if (code == 1) fr = true;
+          else if (dense) fr = v6_dense_dec(dw, cm.x) == 1u;
           else if (code == 127) fr = atomicSub(a.rem_big + cm.x, 1) == 1;
           else fr = v6_dec(S, a.gover, cm.x, code);
         }
@@ -589,7 +616,14 @@ __device__ void peel_warp_v6(const PeelArgs& a, V6Smem<BB>& S) {
     int4 crow = make_int4(-1, 0, -1, 0);
     if (cq.x >= 0) crow = ell6l[static_cast<int64_t>(cq.x) * 4];
     bool fr = false;
-    if (lane < 8 && my.x >= 0) {
+    if (dense) {
+      if (lane < 8 && my.x >= 0) {
+        const uint32_t code = (static_cast<uint32_t>(my.y) >> 24) & 127u;
+        const uint32_t rem = code == 1u ? 1u : v6_dense_dec(dw, my.x);
+        fr = rem == 1u;
+        if (pf && rem == 2u) prefetch_l2(ell6 + static_cast<int64_t>(my.x) * 4);
+      }
+    } else if (lane < 8 && my.x >= 0) {
       // branch-light table step: one bucket load; remaining = table value on a hit, the
       // initial in-degree on a first touch (code == 1 frees without touching the table)
       const uint32_t code = (static_cast<uint32_t>(my.y) >> 24) & 127u, uc = static_cast<uint32_t>(my.x);
@@ -1986,6 +2020,16 @@ __global__ void k_scatter_pos_of(const int32_t* seq, int32_t n, int32_t* pos_of)
     pos_of[seq[p]] = static_cast<int32_t>(p);
 }
 
+__global__ void k_dense16(const int32_t* in_off, int32_t n, uint32_t* words, int* bad) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; 2 * j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = static_cast<int32_t>(2 * j);
+    const int32_t d0 = in_off[v + 1] - in_off[v];
+    const int32_t d1 = v + 1 < n ? in_off[v + 2] - in_off[v + 1] : 0;
+    if (d0 >= 65535 || d1 >= 65535) atomicExch(bad, 1);
+    words[j] = static_cast<uint32_t>(d0 & 0xffff) | (static_cast<uint32_t>(d1 & 0xffff) << 16);
+  }
+}
+
 __global__ void k_indeg_init2(const int32_t* in_off, int32_t n, int32_t* indeg) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
     indeg[v] = in_off[v + 1] - in_off[v];
@@ -2061,8 +2105,16 @@ void peel_prepare_end(DevGraph& g, PeelState& st, bool force_v5) {
   const int32_t* nsrc_p = st.fpos.p + n;
   const int32_t* by_rank = st.by_rank.p;
   const int32_t* rank = st.rank.p;
-  st.v6 = st.stack_mode && n < (1 << 24) && static_cast<int64_t>(m) <= 6 * static_cast<int64_t>(n) && !force_v5 &&
-          getenv("DP_PEEL_V5") == nullptr;
+  // v6 for sparse graphs (m <= 6n), and in dense mode for graphs whose rows mostly exceed
+  // v5's 32 on-chip slots (m > 32n: config #4 wide's coarse graph, 45 children per node:
+  // 78 -> 50 ms; the deep one, 27 per node, stays on v5: 4.4 vs 7.1 ms).
+  // DP_PEEL_V6_DENSE=0 / 1: never / always when dense mode applies.
+  const bool dense_ok = n <= v6_dense_cap<kV6BucketBits>() && getenv("DP_PEEL_NO_DENSE") == nullptr;
+  const char* v6d = getenv("DP_PEEL_V6_DENSE");
+  const bool v6_dense =
+      dense_ok && (v6d ? v6d[0] == '1' : static_cast<int64_t>(m) > 32 * static_cast<int64_t>(n));
+  st.v6 = st.stack_mode && n < (1 << 24) && (static_cast<int64_t>(m) <= 6 * static_cast<int64_t>(n) || v6_dense) &&
+          !force_v5 && getenv("DP_PEEL_V5") == nullptr;
   if (st.v6) {
     st.ell6.alloc(ctx, (size_t)n * 4);
     DP_LAUNCH(ctx, k_ell6, grid_for(n, B), B, 0, g.in_off.p, g.out_off.p, g.out_dst.p, rank, n,
@@ -2077,6 +2129,12 @@ void peel_prepare_end(DevGraph& g, PeelState& st, bool force_v5) {
     st.gover.alloc(ctx, n);
     st.gover.zero();
     st.spill.alloc(ctx, m > 0 ? m : 1);
+    if (n <= v6_dense_cap<kV6BucketBits>() && getenv("DP_PEEL_NO_DENSE") == nullptr) {
+      st.dense16.alloc(ctx, (n + 1) / 2);
+      st.dense_bad.alloc(ctx, 1);
+      st.dense_bad.zero();
+      DP_LAUNCH(ctx, k_dense16, grid_for((n + 1) / 2, B), B, 0, g.in_off.p, n, st.dense16.p, st.dense_bad.p);
+    }
     return;
   }
   st.gstack.alloc(ctx, (size_t)n + 1);
@@ -2154,6 +2212,8 @@ static PeelArgs peel_args(DevGraph& g, PeelState& st, int32_t* seq, int32_t* pos
   a.gover = st.gover.p;
   a.prefetch = getenv("DP_PEEL_NO_PREFETCH") == nullptr;
   a.skip = st.skip.p;
+  a.dense16 = st.dense16.p;
+  a.dense_bad = st.dense_bad.p;
   return a;
 }
 

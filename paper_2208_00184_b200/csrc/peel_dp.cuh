@@ -20,6 +20,8 @@ struct PeelState {
   DevBuf<int2> cmeta;
   DevBuf<int32_t> gsid;
   DevBuf<int32_t> gover;
+  DevBuf<uint32_t> dense16;  // v6 dense mode: 16-bit in-degrees, two per word (small graphs)
+  DevBuf<int> dense_bad;     // set when some in-degree does not fit 16 bits
   // ranks and sources (peel_prepare_begin)
   DevBuf<int32_t> by_rank, rank, flag, fpos;
   // tree peel (fixpoint.cu): the job until tree_run launched it; skip = 1 on the device and

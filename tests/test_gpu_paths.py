@@ -49,19 +49,49 @@ def _orders(gpu, oracle, g):
         same(x, y, nm)
 
 
-@pytest.fixture
-def warp_peel(monkeypatch):
-    """The one-warp peel's special paths are the point: no tree peel first."""
+@pytest.fixture(params=["dense", "hash"])
+def warp_peel(monkeypatch, request):
+    """The one-warp peel's special paths are the point: no tree peel first; remaining
+    in-degrees as dense 16-bit counters (graphs up to 81,920 nodes) or in the hash table."""
     monkeypatch.setenv("DP_PEEL_NO_FIXPOINT", "1")
+    if request.param == "hash":
+        monkeypatch.setenv("DP_PEEL_NO_DENSE", "1")
 
 
 def test_peel_high_indegree(gpu, oracle, warp_peel):
     _orders(gpu, oracle, _fanin_hub())
 
 
-def test_peel_long_rows(gpu, oracle, warp_peel):
-    # fan-out up to 30 from the previous layer: many rows longer than 8
+@pytest.mark.parametrize("v6", [None, "1"])
+def test_peel_long_rows(gpu, oracle, warp_peel, monkeypatch, v6):
+    # fan-out up to 30 from the previous layer: many rows longer than 8 (v5's 32-slot rows,
+    # or v6's CSR path with dense counters when forced)
+    if v6:
+        monkeypatch.setenv("DP_PEEL_V6_DENSE", v6)
     g = layered(9, 6000, 60, fan_lo=6, fan_hi=30)
+    _orders(gpu, oracle, g)
+
+
+def test_peel_v6_dense_wide_rows(gpu, oracle, warp_peel):
+    # more than 32 children per node on average: v6 in dense mode by default (hash mode: v5)
+    _orders(gpu, oracle, layered(19, 8000, 200, fan_lo=30, fan_hi=60))
+
+
+@pytest.mark.parametrize("n", [81920, 81921])
+def test_peel_dense_limit(gpu, oracle, warp_peel, n):
+    # the dense mode's node limit (k_peel2: 2 x (2^15 + 2^13) counters) and one past it
+    _orders(gpu, oracle, layered(17, n, 3000, fan_lo=2, fan_hi=12))
+
+
+def test_peel_dense_huge_indegree(gpu, oracle, warp_peel):
+    # an in-degree of 65,535 does not fit a 16-bit counter: the peel falls back to the table
+    n = 66000
+    rng = np.random.default_rng(4)
+    src = np.concatenate([np.arange(65535), np.arange(65535, n - 1)])
+    dst = np.concatenate([np.full(65535, n - 1), np.arange(65536, n)])
+    o = np.lexsort((dst, src))
+    g = Graph(np.arange(n), rng.integers(1, 100, n), np.ones(n, np.int64), src[o], dst[o],
+              rng.integers(0, 1 << 20, n - 1))
     _orders(gpu, oracle, g)
 
 
