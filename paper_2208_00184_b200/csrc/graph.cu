@@ -94,17 +94,23 @@ __global__ void k_row_keys(const int32_t* esrc, const int32_t* edst, int32_t m, 
 __global__ void k_sorted_check(const int32_t* esrc, const int32_t* edst, int32_t m, int* flag,
                                unsigned long long* span) {
   unsigned long long sp = 0;
+  bool unsorted = false, cyclic = false;  // one atomic per warp at the end, not per edge
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
     const int32_t s = esrc[e], d = edst[e];
-    bool ok = s >= 0 && d >= 0 && (e == 0 || esrc[e - 1] <= s);
-    if (!ok) atomicExch(flag, 0);
+    unsorted |= !(s >= 0 && d >= 0 && (e == 0 || esrc[e - 1] <= s));
     if (s >= 0 && d >= 0) {
-      if (s >= d) atomicExch(flag + 2, 0);
+      if (s >= d) cyclic = true;
       else sp += static_cast<unsigned long long>(d - s);
     }
   }
   for (int o = 16; o; o >>= 1) sp += __shfl_xor_sync(0xffffffffu, sp, o);
-  if ((threadIdx.x & 31) == 0 && sp) atomicAdd(span, sp);
+  unsorted = __any_sync(0xffffffffu, unsorted);
+  cyclic = __any_sync(0xffffffffu, cyclic);
+  if ((threadIdx.x & 31) == 0) {
+    if (sp) atomicAdd(span, sp);
+    if (unsorted) atomicExch(flag, 0);
+    if (cyclic) atomicExch(flag + 2, 0);
+  }
 }
 
 __global__ void k_iota(int32_t* a, int64_t n) {

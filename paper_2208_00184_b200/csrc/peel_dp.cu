@@ -2041,7 +2041,12 @@ __global__ void k_max_abs(const int64_t* x, int32_t n, unsigned long long* out) 
     const int64_t v = x[i] < 0 ? -x[i] : x[i];
     m = static_cast<unsigned long long>(v) > m ? static_cast<unsigned long long>(v) : m;
   }
-  atomicMax(out, m);
+  // one atomic per warp (one per thread serialised ~600K same-address atomics: 0.4 ms)
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, m, o);
+    m = y > m ? y : m;
+  }
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
 }
 
 __global__ void k_out_sum(const int32_t* out_off, const int64_t* out_cost, int32_t n, int64_t* out_sum) {

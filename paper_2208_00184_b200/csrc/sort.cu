@@ -7,9 +7,11 @@
 //                 items): per-tile digit histogram in shared memory -> hist[digit][tile]
 //   scan          exclusive scan of the digit-major histogram = every (digit, tile)'s
 //                 first output slot (the same scan as exclusive_scan_i32 below)
-//   k_rs_scatter  re-reads the tile; a key's rank inside the tile is (same-digit keys in
-//                 earlier warps) + (in earlier rounds of its warp) + (lower lanes of its
-//                 round, __match_any_sync); keys and values go to base + rank.
+//   k_rs_scatter  re-reads the tile; a key's rank among its digit inside the tile is
+//                 (same-digit keys in earlier warps) + (in earlier rounds of its warp) +
+//                 (lower lanes of its round, __match_any_sync); the tile is reordered by
+//                 digit in shared memory and written out in tile order, so each digit's
+//                 run goes to consecutive global slots (coalesced stores).
 // Items are read in order and ranked in order, so equal digits keep their input order
 // (stability, which CSR/CSC construction relies on: graph_index.cpp:36-41).
 // Scans: per-tile reduce -> scan of the tile sums (recursively) -> per-tile scan + offset.
@@ -56,13 +58,18 @@ template <typename K, typename V>
 __global__ void __launch_bounds__(kRsWarps * 32) k_rs_scatter(const K* kin, const V* vin, K* kout, V* vout,
                                                               int64_t count, int shift, int32_t ntiles,
                                                               const int32_t* offs) {
-  __shared__ int32_t wcnt[kRsWarps][256];  // per-warp digit counts; then per-warp digit offsets
-  __shared__ int32_t base[256];
+  __shared__ int32_t wcnt[kRsWarps][256];  // per-warp digit counts; then offsets inside the tile
+  __shared__ int32_t base[256];            // global slot of the tile's first key of each digit
+  __shared__ int32_t tstart[256];          // tile position of the tile's first key of each digit
+  extern __shared__ unsigned char rs_stage[];  // the tile's keys and values in digit order
+  K* sk = reinterpret_cast<K*>(rs_stage);
+  V* sv = reinterpret_cast<V*>(sk + kRsTile);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < kRsWarps * 256; i += blockDim.x) (&wcnt[0][0])[i] = 0;
   for (int d = threadIdx.x; d < 256; d += blockDim.x) base[d] = offs[static_cast<int64_t>(d) * ntiles + blockIdx.x];
   __syncthreads();
-  const int64_t w0 = static_cast<int64_t>(blockIdx.x) * kRsTile + static_cast<int64_t>(warp) * kRsRounds * 32;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kRsTile;
+  const int64_t w0 = t0 + static_cast<int64_t>(warp) * kRsRounds * 32;
   K key[kRsRounds];
   V val[kRsRounds];
   int32_t rank[kRsRounds];
@@ -85,7 +92,10 @@ __global__ void __launch_bounds__(kRsWarps * 32) k_rs_scatter(const K* kin, cons
     __syncwarp();
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < 256; d += blockDim.x) {
+  // digit d's keys occupy tile positions [tstart[d], tstart[d] + total(d)); warp w's part of
+  // them starts at tstart[d] + (digit-d keys of warps before w)
+  if (threadIdx.x < 256) {
+    const int d = threadIdx.x;
     int32_t s = 0;
 #pragma unroll
     for (int w = 0; w < kRsWarps; ++w) {
@@ -93,16 +103,48 @@ __global__ void __launch_bounds__(kRsWarps * 32) k_rs_scatter(const K* kin, cons
       wcnt[w][d] = s;
       s += c;
     }
+    tstart[d] = s;  // total for now; scanned below
+  }
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the 256 digit totals (8 per lane)
+    int32_t v[8], sum = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      v[q] = tstart[lane * 8 + q];
+      sum += v[q];
+    }
+    int32_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    int32_t run = inc - sum;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      tstart[lane * 8 + q] = run;
+      run += v[q];
+    }
   }
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < kRsRounds; ++r) {
     if (rank[r] >= 0) {
       const uint32_t d = digit_of(key[r], shift);
-      const int64_t at = static_cast<int64_t>(base[d]) + wcnt[warp][d] + rank[r];
-      kout[at] = key[r];
-      vout[at] = val[r];
+      const int32_t at = tstart[d] + wcnt[warp][d] + rank[r];
+      sk[at] = key[r];
+      sv[at] = val[r];
     }
+  }
+  __syncthreads();
+  // write out in tile order: consecutive positions of one digit go to consecutive slots
+  const int32_t nt = static_cast<int32_t>(count - t0 < kRsTile ? count - t0 : kRsTile);
+  for (int32_t i = threadIdx.x; i < nt; i += blockDim.x) {
+    const K kk = sk[i];
+    const uint32_t d = digit_of(kk, shift);
+    const int64_t at = static_cast<int64_t>(base[d]) + (i - tstart[d]);
+    kout[at] = kk;
+    vout[at] = sv[i];
   }
 }
 
@@ -210,6 +252,13 @@ void radix_sort(dp_ctx* ctx, const K* ki, K* ko, const V* vi, V* vo, int64_t cou
     tk.alloc(ctx, count);
     tv.alloc(ctx, count);
   }
+  const size_t stage = static_cast<size_t>(kRsTile) * (sizeof(K) + sizeof(V));
+  static bool attr = false;  // per (K, V) instantiation
+  if (!attr) {
+    DP_CUDA(cudaFuncSetAttribute(k_rs_scatter<K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(stage)));
+    attr = true;
+  }
   // ping-pong so that the last pass writes ko / vo and the inputs are never written
   const K* sk = ki;
   const V* sv = vi;
@@ -222,7 +271,7 @@ void radix_sort(dp_ctx* ctx, const K* ki, K* ko, const V* vi, V* vo, int64_t cou
     ++ctx->launches;
     DP_CUDA(cudaGetLastError());
     scan_impl<int32_t, false>(ctx, hist.p, offs.p, static_cast<int64_t>(256) * tiles);
-    k_rs_scatter<K, V><<<tiles, kRsWarps * 32, 0, ctx->stream>>>(sk, sv, dk, dv, count, shift, tiles, offs.p);
+    k_rs_scatter<K, V><<<tiles, kRsWarps * 32, stage, ctx->stream>>>(sk, sv, dk, dv, count, shift, tiles, offs.p);
     ++ctx->launches;
     DP_CUDA(cudaGetLastError());
     sk = dk;
