@@ -33,11 +33,27 @@
 // 2 and 3 read the rows once more, 4 reads the CSC once (fixpoint_launch).
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "fixpoint.cuh"
 #include "graph.cuh"
 
 namespace dpb {
 namespace {
+namespace cg = cooperative_groups;
+
+// CTAs per cluster of a single graph's tree peel.  A cluster pays three cluster barriers per
+// level, so it only helps wide levels: measured (profiles/r2cc_*) the Kahn phase at config #4
+// wide (16 levels of 65,536) 16.5 ms on one CTA -> 2.6 ms on 8 -> 1.4 ms on 16; at deep (977
+// levels of 1,024) 15.8 -> 20.1 / 20.7 ms.  Wide = mean edge span (index order) of at least
+// kTreeWideSpan nodes.  DP_TREE_CLUSTER = 1 / 4 / 8 / 16 forces the size for every graph.
+constexpr double kTreeWideSpan = 8192.0;
+int tree_cluster(bool wide) {
+  const char* e = getenv("DP_TREE_CLUSTER");
+  if (!e) return wide ? 16 : 1;
+  const int v = atoi(e);
+  return v == 4 || v == 8 || v == 16 ? v : 1;
+}
 
 // One graph alone: 1,024 threads (a level of the deep config is one node per thread).  Several
 // graphs per call: 512 threads per CTA, which leaves room on the SM for other graphs'
@@ -96,20 +112,35 @@ __device__ void roots_scan(const TreeArgs& a, int32_t nsrc, const int32_t* size,
   }
 }
 
-template <typename TT>
+// CL > 1 (one graph alone): phase 1 runs on a thread-block cluster of CL CTAs (CL SMs'
+// load/store and atomic throughput: phase 1 is ~2 global atomics + 2 L2 loads per edge,
+// which one SM issues at ~1 per cycle) with cluster barriers between its steps; the
+// per-CTA totals of the next-level numbering meet in CTA 0's shared memory (DSMEM).
+// Phases 2-4 stay on CTA 0 (rank != 0 exits after phase 1).  Values written by other CTAs
+// are read through L2 (ld.cg); the cluster barrier orders them (release / acquire).
+template <typename TT, int CL>
 __global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(const __grid_constant__ TreeBatch batch) {
-  const TreeArgs& a = batch.a[blockIdx.x];
+  const TreeArgs& a = batch.a[blockIdx.x / CL];
   __shared__ int32_t ws[32];
+  __shared__ int32_t ctot[2][CL];  // cluster: per-CTA totals of one numbering step (CTA 0's copy)
+  __shared__ int32_t cloc[CL];
   const int tid = threadIdx.x;
+  int rank = 0;
+  if constexpr (CL > 1) rank = static_cast<int>(cg::this_cluster().block_rank());
+  constexpr int32_t SPAN = CL * TT::kThreads;
+  auto csync = [&]() {
+    if constexpr (CL > 1) cg::this_cluster().sync();
+    else __syncthreads();
+  };
   const int32_t n = a.n;
   const int32_t nsrc = *a.nsrc;
-  for (int32_t v = tid; v < n; v += TT::kThreads) {
+  for (int32_t v = rank * TT::kThreads + tid; v < n; v += SPAN) {
     a.best[v] = -1;
     a.indeg[v] = a.in_off[v + 1] - a.in_off[v];
   }
-  for (int32_t i = tid; i < nsrc; i += TT::kThreads) a.seq0[i] = a.roots[i];
-  if (tid == 0) a.lvl_off[0] = 0;
-  __syncthreads();
+  for (int32_t i = rank * TT::kThreads + tid; i < nsrc; i += SPAN) a.seq0[i] = a.roots[i];
+  if (tid == 0 && rank == 0) a.lvl_off[0] = 0;
+  csync();
   // ---- 1: breadth-first order s0 and the freeing forest T0
   long long clk = clock64();  // phase clocks (DP_DEBUG_FIXPOINT): info[3..6], in 1,024 cycles
   auto phase = [&](int i) {
@@ -121,36 +152,58 @@ __global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(
   };
   int32_t lb = 0, le = nsrc, L = 0;
   while (lb < le) {
-    if (tid == 0) a.lvl_off[L + 1] = le;
+    if (tid == 0 && rank == 0) a.lvl_off[L + 1] = le;
     if (L >= a.max_levels) {
-      if (tid == 0) a.info[0] = 2;
+      if (tid == 0 && rank == 0) a.info[0] = 2;
       return;
     }
-    for (int32_t i = lb + tid; i < le; i += TT::kThreads) {
-      const int32_t v = a.seq0[i];
+    // a level that fits one sweep of the CTA(s) keeps each thread's row (node, bounds, up to
+    // 8 children) in registers from the relaxation to the numbering step
+    const bool one = le - lb <= SPAN;
+    int32_t rkb = 0, rke = 0;
+    int32_t cc[8];
+    for (int32_t i = lb + rank * TT::kThreads + tid; i < le; i += SPAN) {
+      const int32_t v = ldcg(a.seq0 + i);
       const int32_t kb = a.out_off[v], ke = a.out_off[v + 1];
-      for (int32_t k = kb; k < ke; ++k) {
-        const int32_t c = a.rowc[k];
-        atomicMax(a.best + c, i);
-        atomicSub(a.indeg + c, 1);
+      if (ke - kb <= 8) {  // the row's loads first, then its atomics (no load between them)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) cc[q] = kb + q < ke ? a.rowc[kb + q] : 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (kb + q < ke) {
+            atomicMax(a.best + cc[q], i);
+            atomicSub(a.indeg + cc[q], 1);
+          }
+      } else {
+        for (int32_t k = kb; k < ke; ++k) {
+          const int32_t c = a.rowc[k];
+          atomicMax(a.best + c, i);
+          atomicSub(a.indeg + c, 1);
+        }
       }
+      rkb = kb;
+      rke = ke;
     }
-    __syncthreads();
-    int32_t carry = 0;
-    for (int32_t i0 = lb; i0 < le; i0 += TT::kThreads) {
-      const int32_t i = i0 + tid;
+    csync();
+    int32_t carry = 0, par = 0;
+    for (int32_t i0 = lb; i0 < le; i0 += SPAN) {
+      const int32_t i = i0 + rank * TT::kThreads + tid;
       int32_t kb = 0, ke = 0, cnt = 0;
       // (the T0 children of position i will be positions [cs[i], cs[i + 1]) of s0)
       unsigned hit = 0;
-      int32_t cc[8];
       if (i < le) {
-        const int32_t v = a.seq0[i];
-        kb = a.out_off[v];
-        ke = a.out_off[v + 1];
+        if (one) {
+          kb = rkb;
+          ke = rke;
+        } else {
+          const int32_t v = ldcg(a.seq0 + i);
+          kb = a.out_off[v];
+          ke = a.out_off[v + 1];
+        }
         if (ke - kb <= 8) {
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            cc[q] = kb + q < ke ? a.rowc[kb + q] : 0;
+            if (!one) cc[q] = kb + q < ke ? a.rowc[kb + q] : 0;
             if (kb + q < ke && ldcg(a.best + cc[q]) == i && ldcg(a.indeg + cc[q]) == 0) hit |= 1u << q;
           }
           cnt = __popc(hit);
@@ -163,9 +216,25 @@ __global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(
       }
       int32_t tot;
       const int32_t ex = block_scan<TT>(cnt, &tot, ws);
-      if (i < le) a.cs[i] = le + carry + ex;
+      int32_t before = 0, all = tot;  // numbering of the CTAs of lower rank; of the whole step
+      if constexpr (CL > 1) {
+        int32_t* slot0 = cg::this_cluster().map_shared_rank(&ctot[par][0], 0);
+        if (tid == 0) slot0[rank] = tot;
+        cg::this_cluster().sync();
+        if (tid < CL) cloc[tid] = slot0[tid];
+        __syncthreads();
+        all = 0;
+#pragma unroll
+        for (int r = 0; r < CL; ++r) {
+          before += r < rank ? cloc[r] : 0;
+          all += cloc[r];
+        }
+        __syncthreads();  // cloc is rewritten by the next step
+        par ^= 1;
+      }
+      if (i < le) a.cs[i] = le + carry + before + ex;
       if (cnt) {
-        int32_t o = le + carry + ex;
+        int32_t o = le + carry + before + ex;
         if (ke - kb <= 8) {
 #pragma unroll
           for (int q = 0; q < 8; ++q)
@@ -177,17 +246,18 @@ __global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(
           }
         }
       }
-      carry += tot;
+      carry += all;
     }
-    __syncthreads();
+    csync();
     lb = le;
     le += carry;
     ++L;
   }
   if (le != n) {  // not a DAG: the one-warp peel reports it
-    if (tid == 0) a.info[0] = 3;
+    if (tid == 0 && rank == 0) a.info[0] = 3;
     return;
   }
+  if (rank != 0) return;  // phases 2-4 on CTA 0
   if (tid == 0) a.cs[n] = n;
   __syncthreads();
   phase(0);
@@ -381,6 +451,7 @@ std::unique_ptr<TreeJob> fixpoint_prepare(DevGraph& g, const int32_t* by_rank, c
   const int32_t n = g.n, m = g.m_ok;
   std::unique_ptr<TreeJob> j(new TreeJob);
   j->ctx = ctx;
+  j->wide = g.topo_known && m > 0 && static_cast<double>(g.span_sum) / m >= kTreeWideSpan;
   j->rowc.alloc(ctx, m > 0 ? m : 1);
   DevBuf<int> flags(ctx, 1);
   flags.zero();
@@ -451,8 +522,42 @@ void fixpoint_launch_batch(dp_ctx* ctx, TreeJob* const* jobs, int count) {
       bytes += jobs[b0 + q]->bytes;
     }
     StageScope s(ctx, "peel (tree)", bytes);
-    if (count == 1) DP_LAUNCH(ctx, k_treepeel<TreeCfg<1024>>, k, 1024, 0, b);
-    else DP_LAUNCH(ctx, k_treepeel<TreeCfg<512>>, k, 512, 0, b);
+    if (count == 1 && tree_cluster(jobs[b0]->wide) > 1) {
+      const int cl = tree_cluster(jobs[b0]->wide);
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(static_cast<unsigned>(k * cl));
+      cfg.blockDim = dim3(1024);
+      cfg.stream = ctx->stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = static_cast<unsigned>(cl);
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      if (cl == 16) {
+        static bool np = false;
+        if (!np) {
+          DP_CUDA(cudaFuncSetAttribute(k_treepeel<TreeCfg<1024>, 16>,
+                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+          np = true;
+        }
+        DP_CUDA(cudaLaunchKernelEx(&cfg, k_treepeel<TreeCfg<1024>, 16>, b));
+      } else if (cl == 4) {
+        DP_CUDA(cudaLaunchKernelEx(&cfg, k_treepeel<TreeCfg<1024>, 4>, b));
+      } else {
+        DP_CUDA(cudaLaunchKernelEx(&cfg, k_treepeel<TreeCfg<1024>, 8>, b));
+      }
+      ++ctx->launches;
+    } else if (count == 1) {
+      k_treepeel<TreeCfg<1024>, 1><<<k, 1024, 0, ctx->stream>>>(b);
+      ++ctx->launches;
+      DP_CUDA(cudaGetLastError());
+    } else {
+      k_treepeel<TreeCfg<512>, 1><<<k, 512, 0, ctx->stream>>>(b);
+      ++ctx->launches;
+      DP_CUDA(cudaGetLastError());
+    }
   }
   if (getenv("DP_DEBUG_FIXPOINT")) {
     std::vector<int> h(8 * (size_t)count);

@@ -43,6 +43,7 @@ struct TreeJob {
   DevBuf<int> info;
   TreeArgs a{};
   double bytes = 0.0;  // algorithmic bytes (stage timing)
+  bool wide = false;   // mean edge span >= kTreeWideSpan: levels wide enough for a cluster
 };
 
 // The tree peel is tried for stack policies on graphs of at least 2,048 nodes (it gives up

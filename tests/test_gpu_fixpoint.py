@@ -74,14 +74,20 @@ CASES = {
 }
 
 
+@pytest.fixture(params=["1", "4", "8", "16"])
+def cluster(monkeypatch, request):
+    """CTAs of the single-graph tree peel's Kahn phase (thread-block cluster; 1 = one CTA)."""
+    monkeypatch.setenv("DP_TREE_CLUSTER", request.param)
+
+
 @pytest.mark.parametrize("case", sorted(CASES))
-def test_tree_orders(gpu, oracle, stats, case):
+def test_tree_orders(gpu, oracle, stats, cluster, case):
     """Every edge joins consecutive levels: the first tree is the peel order."""
     _orders(gpu, oracle, CASES[case](), case)
     assert stats().tolist() == [2, 0, 0, 0, 0]
 
 
-def test_tree_rounds_random_dag(gpu, oracle, stats, monkeypatch):
+def test_tree_rounds_random_dag(gpu, oracle, stats, cluster, monkeypatch):
     """Skip edges: the proof fails and fixed-point rounds converge (forced: the cost
     model's budget for these small graphs would hand them to the one-warp peel)."""
     monkeypatch.setenv("DP_PEEL_FIXPOINT", "1")
