@@ -68,6 +68,11 @@ struct TreeBatch {
 };
 
 __device__ __forceinline__ int32_t ldcg(const int32_t* p) { return __ldcg(p); }
+// child c is freed by this level and its T0 parent is position i
+__device__ __forceinline__ bool claimed(const int2* p, int32_t i) {
+  const int2 x = __ldcg(p);
+  return x.x == i && x.y == 0;
+}
 
 // Exclusive block scan over TT::kThreads threads; *total = sum.  All threads call.
 template <typename TT>
@@ -135,8 +140,7 @@ __global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(
   const int32_t n = a.n;
   const int32_t nsrc = *a.nsrc;
   for (int32_t v = rank * TT::kThreads + tid; v < n; v += SPAN) {
-    a.best[v] = -1;
-    a.indeg[v] = a.in_off[v + 1] - a.in_off[v];
+    a.bi[v] = make_int2(-1, a.in_off[v + 1] - a.in_off[v]);
   }
   for (int32_t i = rank * TT::kThreads + tid; i < nsrc; i += SPAN) a.seq0[i] = a.roots[i];
   if (tid == 0 && rank == 0) a.lvl_off[0] = 0;
@@ -171,14 +175,14 @@ __global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(
 #pragma unroll
         for (int q = 0; q < 8; ++q)
           if (kb + q < ke) {
-            atomicMax(a.best + cc[q], i);
-            atomicSub(a.indeg + cc[q], 1);
+            atomicMax(&a.bi[cc[q]].x, i);
+            atomicSub(&a.bi[cc[q]].y, 1);
           }
       } else {
         for (int32_t k = kb; k < ke; ++k) {
           const int32_t c = a.rowc[k];
-          atomicMax(a.best + c, i);
-          atomicSub(a.indeg + c, 1);
+          atomicMax(&a.bi[c].x, i);
+          atomicSub(&a.bi[c].y, 1);
         }
       }
       rkb = kb;
@@ -204,13 +208,13 @@ __global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             if (!one) cc[q] = kb + q < ke ? a.rowc[kb + q] : 0;
-            if (kb + q < ke && ldcg(a.best + cc[q]) == i && ldcg(a.indeg + cc[q]) == 0) hit |= 1u << q;
+            if (kb + q < ke && claimed(a.bi + cc[q], i)) hit |= 1u << q;
           }
           cnt = __popc(hit);
         } else {
           for (int32_t k = kb; k < ke; ++k) {
             const int32_t c = a.rowc[k];
-            cnt += (ldcg(a.best + c) == i && ldcg(a.indeg + c) == 0) ? 1 : 0;
+            cnt += claimed(a.bi + c, i) ? 1 : 0;
           }
         }
       }
@@ -242,7 +246,7 @@ __global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(
         } else {
           for (int32_t k = kb; k < ke; ++k) {
             const int32_t c = a.rowc[k];
-            if (ldcg(a.best + c) == i && ldcg(a.indeg + c) == 0) a.seq0[o++] = c;
+            if (claimed(a.bi + c, i)) a.seq0[o++] = c;
           }
         }
       }
@@ -308,7 +312,7 @@ __global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(
     if (b == e) continue;
     int32_t mx = -1;
     for (int32_t k = b; k < e; ++k) mx = max(mx, a.pre[a.in_src[k]]);
-    bad |= mx != ppre[ldcg(a.best + v)];
+    bad |= mx != ppre[__ldcg(&a.bi[v].x)];
   }
   int32_t* pos = a.pre;
   int rounds = 1;
@@ -467,8 +471,7 @@ std::unique_ptr<TreeJob> fixpoint_prepare(DevGraph& g, const int32_t* by_rank, c
   j->roots.alloc(ctx, n);
   DP_LAUNCH(ctx, k_roots, grid_for(n, B), B, 0, by_rank, flag, fpos, n, j->roots.p);
   j->seq0.alloc(ctx, n);
-  j->best.alloc(ctx, n);
-  j->indeg.alloc(ctx, n);
+  j->bi.alloc(ctx, n);
   j->size.alloc(ctx, n);
   j->pre.alloc(ctx, n);
   j->pre2.alloc(ctx, n);
@@ -488,8 +491,7 @@ std::unique_ptr<TreeJob> fixpoint_prepare(DevGraph& g, const int32_t* by_rank, c
   a.rowc = j->rowc.p;
   a.roots = j->roots.p;
   a.seq0 = j->seq0.p;
-  a.best = j->best.p;
-  a.indeg = j->indeg.p;
+  a.bi = j->bi.p;
   a.size = j->size.p;
   a.pre = j->pre.p;
   a.pre2 = j->pre2.p;

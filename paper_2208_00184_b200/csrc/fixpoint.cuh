@@ -15,8 +15,8 @@ struct TreeArgs {
   const int32_t* rowc;   // CSR children, each row sorted by rank (best first)
   const int32_t* roots;  // sources by rank
   int32_t* seq0;         // breadth-first order s0 (level-major)
-  int32_t* best;         // s0 position of the T0 parent
-  int32_t* indeg;
+  int2* bi;              // per node {s0 position of the T0 parent, remaining in-degree}: the
+                         // numbering step reads both with one 8-byte load
   int32_t* size;
   int32_t* pre;          // preorder positions
   int32_t* pre2;         // general rounds: second buffer
@@ -39,7 +39,8 @@ constexpr int kTreeBatch = 8;
 
 struct TreeJob {
   dp_ctx* ctx = nullptr;
-  DevBuf<int32_t> rowc, roots, seq0, best, indeg, size, pre, pre2, par, lvl_off, cs, psize, ppre;
+  DevBuf<int32_t> rowc, roots, seq0, size, pre, pre2, par, lvl_off, cs, psize, ppre;
+  DevBuf<int2> bi;
   DevBuf<int> info;
   TreeArgs a{};
   double bytes = 0.0;  // algorithmic bytes (stage timing)
