@@ -232,32 +232,54 @@ __global__ void __launch_bounds__(32) k_dp_generic(int32_t n, const int32_t* lo,
   }
 }
 
-// Cut traceback from n (fusion.cpp:164-169), staged through shared memory in windows.
-__global__ void k_traceback(const int32_t* prev_cut, int32_t n, uint8_t* is_cut) {
-  __shared__ int32_t buf[4096];
+// Cut traceback from n (fusion.cpp:164-169).  prev_cut is read in fixed windows of
+// kTbWin positions, double-buffered in shared memory: while thread 0 chases the cuts down
+// window k (one shared load per cut, ~n / 140 cuts at config #4), warps 1.. load window
+// k + 1.  A cut is at most R <= 256 positions below the previous one, so the chase always
+// continues in the next window.
+constexpr int32_t kTbWin = 24576;
+constexpr size_t kTbSmem = 2 * sizeof(int32_t) * kTbWin;
+__global__ void __launch_bounds__(1024) k_traceback(const int32_t* prev_cut, int32_t n, uint8_t* is_cut) {
+  extern __shared__ int32_t tbuf[];  // [2][kTbWin]
   __shared__ int32_t cur_s;
-  int32_t cur = n;
   if (threadIdx.x == 0) {
     is_cut[n] = 1;
     is_cut[0] = 1;
+    cur_s = n;
   }
-  while (cur > 0) {
-    const int32_t lo = max(1, cur - 4095);
-    for (int32_t i = threadIdx.x; i <= cur - lo; i += blockDim.x) buf[i] = prev_cut[lo + i];
-    __syncthreads();
+  // window k covers positions [max(1, n - (k + 1) W + 1), n - k W]
+  auto load = [&](int32_t k, int32_t* dst, int32_t t0, int32_t nt) {
+    const int32_t hi = n - k * kTbWin, lo = max(1, hi - kTbWin + 1);
+    for (int32_t i = t0; i <= hi - lo; i += nt) dst[i] = prev_cut[lo + i];
+  };
+  if (n > 0) load(0, tbuf, threadIdx.x, blockDim.x);
+  __syncthreads();
+  for (int32_t k = 0;; ++k) {
+    const int32_t hi = n - k * kTbWin, lo = max(1, hi - kTbWin + 1);
+    int32_t* cur = tbuf + (k & 1) * kTbWin;
     if (threadIdx.x == 0) {
-      int32_t c = cur;
+      int32_t c = cur_s;
       while (c >= lo && c > 0) {
-        int32_t p = buf[c - lo];
+        const int32_t p = cur[c - lo];
         is_cut[p] = 1;
         c = p;
       }
       cur_s = c;
+    } else if (threadIdx.x >= 32 && lo > 1) {
+      load(k + 1, tbuf + ((k + 1) & 1) * kTbWin, threadIdx.x - 32, blockDim.x - 32);
     }
     __syncthreads();
-    cur = cur_s;
-    __syncthreads();
+    if (cur_s <= 0 || lo <= 1) break;
   }
+}
+
+void traceback_launch(dp_ctx* ctx, const int32_t* prev_cut, int32_t n, uint8_t* is_cut) {
+  static bool attr = false;
+  if (!attr) {
+    DP_CUDA(cudaFuncSetAttribute(k_traceback, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTbSmem)));
+    attr = true;
+  }
+  DP_LAUNCH(ctx, k_traceback, 1, 1024, kTbSmem, prev_cut, n, is_cut);
 }
 
 __global__ void k_cut_scan_in(const uint8_t* is_cut, int32_t n, int32_t* f) {
@@ -527,7 +549,7 @@ void clusters_from_prev_cut(DevGraph& g, const int32_t* seq, const int32_t* prev
   out.n = n;
   DevBuf<uint8_t> is_cut(ctx, (size_t)n + 1);
   is_cut.zero();
-  DP_LAUNCH(ctx, k_traceback, 1, 256, 0, prev_cut, n, is_cut.p);
+  traceback_launch(ctx, prev_cut, n, is_cut.p);
   DevBuf<int32_t> f(ctx, (size_t)n + 1), fx(ctx, (size_t)n + 1);
   f.zero();
   DP_LAUNCH(ctx, k_cut_scan_in, grid_for(n, B), B, 0, is_cut.p, n, f.p);
@@ -794,7 +816,7 @@ void fuse_end_batch(DevGraph* const* gs, int count, FuseOut* const* outs, FuseSt
     const int32_t n = work_of(i).n;
     t.is_cut.alloc(ctx, (size_t)n + 1);
     t.is_cut.zero();
-    DP_LAUNCH(ctx, k_traceback, 1, 256, 0, fss[i]->prev_cut.p, n, t.is_cut.p);
+    traceback_launch(ctx, fss[i]->prev_cut.p, n, t.is_cut.p);
     t.f.alloc(ctx, (size_t)n + 1);
     t.fx.alloc(ctx, (size_t)n + 1);
     t.f.zero();
