@@ -123,13 +123,125 @@ __device__ void roots_scan(const TreeArgs& a, int32_t nsrc, const int32_t* size,
 // per-CTA totals of the next-level numbering meet in CTA 0's shared memory (DSMEM).
 // Phases 2-4 stay on CTA 0 (rank != 0 exits after phase 1).  Values written by other CTAs
 // are read through L2 (ld.cg); the cluster barrier orders them (release / acquire).
+// Fixed-point rounds after a failed proof (any_bad), then the emission of seq / pos_of and
+// the verdict; one CTA.  Called at the end of k_treepeel, or by its continuation launch
+// (mode 1) when the proof ran as a grid kernel and failed.
+template <typename TT, typename Phase>
+__device__ void tree_finish(const TreeArgs& a, int32_t L, int32_t nsrc, bool any_bad, int32_t* ws, Phase&& phase) {
+  const int tid = threadIdx.x;
+  const int32_t n = a.n;
+  int32_t* pos = a.pre;
+  int rounds = 1;
+  if (any_bad) {
+    // general rounds s <- preorder(T(s)) on the same levels (a T(s) parent is a
+    // predecessor, so it sits on a shallower level)
+    int32_t budget = a.max_rounds;
+    if (budget < 0) budget = max(0, (n / 8) / (6 * L + 8));
+    int32_t* nxt = a.pre2;
+    bool done = false;
+    for (int r = 0; r < budget && !done; ++r) {
+      ++rounds;
+      for (int32_t v = tid; v < n; v += TT::kThreads) {
+        int32_t bp = -1, bu = -1;
+        for (int32_t k = a.in_off[v]; k < a.in_off[v + 1]; ++k) {
+          const int32_t u = a.in_src[k];
+          const int32_t q = pos[u];
+          if (q > bp) {
+            bp = q;
+            bu = u;
+          }
+        }
+        a.par[v] = bu;
+      }
+      __syncthreads();
+      for (int32_t l = L - 1; l >= 0; --l) {
+        const int32_t b = a.lvl_off[l], e = a.lvl_off[l + 1];
+        for (int32_t i = b + tid; i < e; i += TT::kThreads) {
+          const int32_t v = a.seq0[i];
+          int32_t s = 1;
+          for (int32_t k = a.out_off[v]; k < a.out_off[v + 1]; ++k) {
+            const int32_t c = a.rowc[k];
+            if (a.par[c] == v) s += a.size[c];
+          }
+          a.size[v] = s;
+        }
+        __syncthreads();
+      }
+      roots_scan<TT>(a, nsrc, a.size, nxt, ws);
+      __syncthreads();
+      for (int32_t l = 0; l + 1 < L; ++l) {
+        const int32_t b = a.lvl_off[l], e = a.lvl_off[l + 1];
+        for (int32_t i = b + tid; i < e; i += TT::kThreads) {
+          const int32_t v = a.seq0[i];
+          int32_t acc = nxt[v] + 1;
+          for (int32_t k = a.out_off[v]; k < a.out_off[v + 1]; ++k) {
+            const int32_t c = a.rowc[k];
+            if (a.par[c] == v) {
+              nxt[c] = acc;
+              acc += a.size[c];
+            }
+          }
+        }
+        __syncthreads();
+      }
+      bool chg = false;
+      for (int32_t v = tid; v < n; v += TT::kThreads) chg |= nxt[v] != pos[v];
+      done = !__syncthreads_or(chg);
+      int32_t* t = pos;
+      pos = nxt;
+      nxt = t;
+    }
+    if (!done) {
+      if (tid == 0) {
+        a.info[0] = 4;
+        a.info[1] = L;
+        a.info[2] = rounds;
+      }
+      return;
+    }
+  }
+  for (int32_t v = tid; v < n; v += TT::kThreads) {
+    const int32_t p = pos[v];
+    a.seq[p] = v;
+    a.pos_of[v] = p;
+  }
+  __syncthreads();
+  phase(3);
+  if (tid == 0) {
+    __threadfence();
+    a.info[0] = 1;
+    a.info[1] = L;
+    a.info[2] = rounds;
+    *a.skip = 1;
+    *a.emitted = n;
+    *a.progress = n;
+  }
+}
+
 template <typename TT, int CL>
-__global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(const __grid_constant__ TreeBatch batch) {
+__global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(const __grid_constant__ TreeBatch batch,
+                                                                                      int mode) {
   const TreeArgs& a = batch.a[blockIdx.x / CL];
   __shared__ int32_t ws[32];
   __shared__ int32_t ctot[2][CL];  // cluster: per-CTA totals of one numbering step (CTA 0's copy)
   __shared__ int32_t cloc[CL];
   const int tid = threadIdx.x;
+  if (mode == 1) {  // continuation after the grid proof / emission (one CTA per graph)
+    if (a.info[0] != 5) return;
+    if (a.info[7] == 0) {  // proof held: the emission kernel wrote seq / pos_of
+      if (tid == 0) {
+        a.info[0] = 1;
+        a.info[2] = 1;
+        *a.skip = 1;
+        *a.emitted = a.n;
+        *a.progress = a.n;
+      }
+      return;
+    }
+    auto nophase = [](int) {};
+    tree_finish<TT>(a, a.info[1], *a.nsrc, true, ws, nophase);
+    return;
+  }
   int rank = 0;
   if constexpr (CL > 1) rank = static_cast<int>(cg::this_cluster().block_rank());
   constexpr int32_t SPAN = CL * TT::kThreads;
@@ -143,7 +255,10 @@ __global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(
     a.bi[v] = make_int2(-1, a.in_off[v + 1] - a.in_off[v]);
   }
   for (int32_t i = rank * TT::kThreads + tid; i < nsrc; i += SPAN) a.seq0[i] = a.roots[i];
-  if (tid == 0 && rank == 0) a.lvl_off[0] = 0;
+  if (tid == 0 && rank == 0) {
+    a.lvl_off[0] = 0;
+    a.info[7] = 0;
+  }
   csync();
   // ---- 1: breadth-first order s0 and the freeing forest T0
   long long clk = clock64();  // phase clocks (DP_DEBUG_FIXPOINT): info[3..6], in 1,024 cycles
@@ -305,6 +420,13 @@ __global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(
   for (int32_t i = tid; i < n; i += TT::kThreads) a.pre[a.seq0[i]] = ppre[i];
   __syncthreads();
   phase(1);
+  if (a.split && mode == 0) {  // proof and emission by the grid kernels below
+    if (tid == 0 && rank == 0) {
+      a.info[0] = 5;
+      a.info[1] = L;
+    }
+    return;
+  }
   // ---- 4: proof T(preorder(T0)) = T0
   bool bad = false;
   for (int32_t v = tid; v < n; v += TT::kThreads) {
@@ -314,93 +436,34 @@ __global__ void __launch_bounds__(TT::kThreads, 1024 / TT::kThreads) k_treepeel(
     for (int32_t k = b; k < e; ++k) mx = max(mx, a.pre[a.in_src[k]]);
     bad |= mx != ppre[__ldcg(&a.bi[v].x)];
   }
-  int32_t* pos = a.pre;
-  int rounds = 1;
   const bool any_bad = __syncthreads_or(bad);
   phase(2);
-  if (any_bad) {
-    // general rounds s <- preorder(T(s)) on the same levels (a T(s) parent is a
-    // predecessor, so it sits on a shallower level)
-    int32_t budget = a.max_rounds;
-    if (budget < 0) budget = max(0, (n / 8) / (6 * L + 8));
-    int32_t* nxt = a.pre2;
-    bool done = false;
-    for (int r = 0; r < budget && !done; ++r) {
-      ++rounds;
-      for (int32_t v = tid; v < n; v += TT::kThreads) {
-        int32_t bp = -1, bu = -1;
-        for (int32_t k = a.in_off[v]; k < a.in_off[v + 1]; ++k) {
-          const int32_t u = a.in_src[k];
-          const int32_t q = pos[u];
-          if (q > bp) {
-            bp = q;
-            bu = u;
-          }
-        }
-        a.par[v] = bu;
-      }
-      __syncthreads();
-      for (int32_t l = L - 1; l >= 0; --l) {
-        const int32_t b = a.lvl_off[l], e = a.lvl_off[l + 1];
-        for (int32_t i = b + tid; i < e; i += TT::kThreads) {
-          const int32_t v = a.seq0[i];
-          int32_t s = 1;
-          for (int32_t k = a.out_off[v]; k < a.out_off[v + 1]; ++k) {
-            const int32_t c = a.rowc[k];
-            if (a.par[c] == v) s += a.size[c];
-          }
-          a.size[v] = s;
-        }
-        __syncthreads();
-      }
-      roots_scan<TT>(a, nsrc, a.size, nxt, ws);
-      __syncthreads();
-      for (int32_t l = 0; l + 1 < L; ++l) {
-        const int32_t b = a.lvl_off[l], e = a.lvl_off[l + 1];
-        for (int32_t i = b + tid; i < e; i += TT::kThreads) {
-          const int32_t v = a.seq0[i];
-          int32_t acc = nxt[v] + 1;
-          for (int32_t k = a.out_off[v]; k < a.out_off[v + 1]; ++k) {
-            const int32_t c = a.rowc[k];
-            if (a.par[c] == v) {
-              nxt[c] = acc;
-              acc += a.size[c];
-            }
-          }
-        }
-        __syncthreads();
-      }
-      bool chg = false;
-      for (int32_t v = tid; v < n; v += TT::kThreads) chg |= nxt[v] != pos[v];
-      done = !__syncthreads_or(chg);
-      int32_t* t = pos;
-      pos = nxt;
-      nxt = t;
-    }
-    if (!done) {
-      if (tid == 0) {
-        a.info[0] = 4;
-        a.info[1] = L;
-        a.info[2] = rounds;
-      }
-      return;
-    }
+  tree_finish<TT>(a, L, nsrc, any_bad, ws, phase);
+}
+
+// Split proof (TreeArgs.split): every node's predecessor with the largest preorder position
+// must be its T0 parent -- a flat pass over the CSC, on the whole GPU instead of one CTA;
+// blockIdx.y = graph.  Then the emission seq[pre[v]] = v when no node failed.
+__global__ void k_tree_proof(const __grid_constant__ TreeBatch batch) {
+  const TreeArgs& a = batch.a[blockIdx.y];
+  if (a.info[0] != 5) return;
+  bool bad = false;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < a.n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t b = a.in_off[v], e = a.in_off[v + 1];
+    if (b == e) continue;
+    int32_t mx = -1;
+    for (int32_t k = b; k < e; ++k) mx = max(mx, __ldcg(a.pre + a.in_src[k]));
+    bad |= mx != __ldcg(a.ppre + __ldcg(&a.bi[v].x));
   }
-  for (int32_t v = tid; v < n; v += TT::kThreads) {
-    const int32_t p = pos[v];
-    a.seq[p] = v;
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.info + 7, 1);
+}
+__global__ void k_tree_emit(const __grid_constant__ TreeBatch batch) {
+  const TreeArgs& a = batch.a[blockIdx.y];
+  if (a.info[0] != 5 || __ldcg(a.info + 7) != 0) return;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < a.n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t p = __ldcg(a.pre + v);
+    a.seq[p] = static_cast<int32_t>(v);
     a.pos_of[v] = p;
-  }
-  __syncthreads();
-  phase(3);
-  if (tid == 0) {
-    __threadfence();
-    a.info[0] = 1;
-    a.info[1] = L;
-    a.info[2] = rounds;
-    *a.skip = 1;
-    *a.emitted = n;
-    *a.progress = n;
   }
 }
 
@@ -483,6 +546,7 @@ std::unique_ptr<TreeJob> fixpoint_prepare(DevGraph& g, const int32_t* by_rank, c
   j->info.alloc(ctx, 8);
   j->info.zero();
   TreeArgs& a = j->a;
+  a.split = getenv("DP_TREE_FUSED_PROOF") ? 0 : 1;
   a.n = n;
   a.nsrc = fpos + n;
   a.in_off = g.in_off.p;
@@ -544,20 +608,31 @@ void fixpoint_launch_batch(dp_ctx* ctx, TreeJob* const* jobs, int count) {
                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
           np = true;
         }
-        DP_CUDA(cudaLaunchKernelEx(&cfg, k_treepeel<TreeCfg<1024>, 16>, b));
+        DP_CUDA(cudaLaunchKernelEx(&cfg, k_treepeel<TreeCfg<1024>, 16>, b, 0));
       } else if (cl == 4) {
-        DP_CUDA(cudaLaunchKernelEx(&cfg, k_treepeel<TreeCfg<1024>, 4>, b));
+        DP_CUDA(cudaLaunchKernelEx(&cfg, k_treepeel<TreeCfg<1024>, 4>, b, 0));
       } else {
-        DP_CUDA(cudaLaunchKernelEx(&cfg, k_treepeel<TreeCfg<1024>, 8>, b));
+        DP_CUDA(cudaLaunchKernelEx(&cfg, k_treepeel<TreeCfg<1024>, 8>, b, 0));
       }
       ++ctx->launches;
     } else if (count == 1) {
-      k_treepeel<TreeCfg<1024>, 1><<<k, 1024, 0, ctx->stream>>>(b);
+      k_treepeel<TreeCfg<1024>, 1><<<k, 1024, 0, ctx->stream>>>(b, 0);
       ++ctx->launches;
       DP_CUDA(cudaGetLastError());
     } else {
-      k_treepeel<TreeCfg<512>, 1><<<k, 512, 0, ctx->stream>>>(b);
+      k_treepeel<TreeCfg<512>, 1><<<k, 512, 0, ctx->stream>>>(b, 0);
       ++ctx->launches;
+      DP_CUDA(cudaGetLastError());
+    }
+    if (b.a[0].split) {  // grid proof, grid emission, then the one-CTA continuation
+      int32_t maxn = 1;
+      for (int q = 0; q < k; ++q) maxn = std::max(maxn, b.a[q].n);
+      const dim3 grid(static_cast<unsigned>(grid_for(maxn, 256)), static_cast<unsigned>(k));
+      k_tree_proof<<<grid, 256, 0, ctx->stream>>>(b);
+      k_tree_emit<<<grid, 256, 0, ctx->stream>>>(b);
+      if (count == 1) k_treepeel<TreeCfg<1024>, 1><<<k, 1024, 0, ctx->stream>>>(b, 1);
+      else k_treepeel<TreeCfg<512>, 1><<<k, 512, 0, ctx->stream>>>(b, 1);
+      ctx->launches += 3;
       DP_CUDA(cudaGetLastError());
     }
   }

@@ -32,7 +32,9 @@ struct TreeArgs {
   int* skip;
   int* progress;
   int* emitted;
-  int* info;             // [0] status (1 ok, 2 too deep, 3 not a DAG, 4 budget), [1] levels, [2] rounds
+  int* info;             // [0] status (1 ok, 2 too deep, 3 not a DAG, 4 budget, 5 proof pending),
+                         // [1] levels, [2] rounds, [3..6] phase clocks, [7] proof failed (split)
+  int split;             // 1: the proof and the emission run as grid kernels (k_tree_proof / _emit)
 };
 
 constexpr int kTreeBatch = 8;

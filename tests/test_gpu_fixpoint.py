@@ -80,14 +80,21 @@ def cluster(monkeypatch, request):
     monkeypatch.setenv("DP_TREE_CLUSTER", request.param)
 
 
+@pytest.fixture(params=["split", "fused"])
+def proof(monkeypatch, request):
+    """The proof and emission as grid kernels after the tree kernel (default), or inside it."""
+    if request.param == "fused":
+        monkeypatch.setenv("DP_TREE_FUSED_PROOF", "1")
+
+
 @pytest.mark.parametrize("case", sorted(CASES))
-def test_tree_orders(gpu, oracle, stats, cluster, case):
+def test_tree_orders(gpu, oracle, stats, cluster, proof, case):
     """Every edge joins consecutive levels: the first tree is the peel order."""
     _orders(gpu, oracle, CASES[case](), case)
     assert stats().tolist() == [2, 0, 0, 0, 0]
 
 
-def test_tree_rounds_random_dag(gpu, oracle, stats, cluster, monkeypatch):
+def test_tree_rounds_random_dag(gpu, oracle, stats, cluster, proof, monkeypatch):
     """Skip edges: the proof fails and fixed-point rounds converge (forced: the cost
     model's budget for these small graphs would hand them to the one-warp peel)."""
     monkeypatch.setenv("DP_PEEL_FIXPOINT", "1")
@@ -97,7 +104,7 @@ def test_tree_rounds_random_dag(gpu, oracle, stats, cluster, monkeypatch):
     assert s[1] >= 3 and s[2:].sum() == 0, s
 
 
-def test_tree_budget_fallback(gpu, oracle, stats, monkeypatch):
+def test_tree_budget_fallback(gpu, oracle, stats, proof, monkeypatch):
     """No fixed-point rounds allowed: the one-warp peel must produce the order."""
     monkeypatch.setenv("DP_FIXPOINT_ROUNDS", "0")
     monkeypatch.setenv("DP_PEEL_FIXPOINT", "1")
