@@ -384,7 +384,7 @@ __device__ __forceinline__ void kahn_pull_warp(const KahnArgs& a, int32_t v) {
 // per in-edge and a two-step 64-bit max (redux.sync on high then low words).
 constexpr int kSeqMaxN = 16384;  // graphs up to this size always take the one-CTA sweep
 constexpr int kSeqRing = 8192;   // power of two: sweep values kept in shared memory
-constexpr int kSeqTile = 4096;   // edges staged per tile
+constexpr int kSeqTile = 8192;   // edges staged per tile
 constexpr int kSeqTileN = 2048;  // nodes staged per tile
 
 // ok = 0 unless every edge u->v has u < v; span += sum of (v - u) (how far ahead of a node

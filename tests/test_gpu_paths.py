@@ -140,11 +140,11 @@ def test_levels_indexorder_limit(gpu, oracle, n):
 
 
 def test_levels_indexorder_long_row(gpu, oracle):
-    # one node with more in-edges than a staged tile (6144): the sweep reads it from HBM
-    n = 9000
+    # one node with more in-edges than a staged tile (8,192 edges): the sweep reads it from HBM
+    n = 12000
     rng = np.random.default_rng(2)
-    src = list(range(7000)) + list(rng.integers(0, 8000, 3000))
-    dst = [8999] * 7000 + [int(x) + 1 + int(rng.integers(0, 999)) for x in rng.integers(0, 8000, 3000)]
+    src = list(range(9000)) + list(rng.integers(0, 11000, 3000))
+    dst = [11999] * 9000 + [int(x) + 1 + int(rng.integers(0, 999)) for x in rng.integers(0, 11000, 3000)]
     pairs = sorted({(s, d) for s, d in zip(src, dst) if s < d < n})
     g = Graph(np.arange(n), rng.integers(1, 100, n), np.ones(n, np.int64), [p[0] for p in pairs],
               [p[1] for p in pairs], rng.integers(0, 1 << 20, len(pairs)))
